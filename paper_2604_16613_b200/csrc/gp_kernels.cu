@@ -1,0 +1,943 @@
+// gp_kernels.cu -- sm_100a device pipeline of the DEM compiler.
+//
+// Replaces, stage by stage, the body of demc::compile_circuit
+// (/root/reference/proj/core/src/compile.cpp:23-53):
+//   lower_kernel      lower() (stepg.cpp:165-315) restricted to base slots, plus
+//                     EecMatrix::zeroed + init_leaves (eec.cpp:22-58)
+//   traverse_kernel   run_backward / Alg. 1 (eec.cpp:64-122) fused with the
+//                     per-source signature gather (eec.cpp:130-140), emitting
+//                     only nonzero signature words
+//   dedup_kernel ..   reduce_packed (dem.cpp:57-142): hash grouping with full
+//   gather_kernel     compare, sorted fp64 merge_prob fold, canonical order
+// All of it is integer / GF(2) / scalar fp64 work: no tensor cores. Every
+// kernel is bound by memory latency or bandwidth; see DESIGN.md.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "gp_device.h"
+
+namespace gp {
+
+namespace {
+
+constexpr int kTravStagesMax = 4;
+
+// ---------------------------------------------------------------- helpers
+
+__device__ __forceinline__ uint32_t find_u32(const uint32_t *base, uint32_t C, uint32_t x) {
+    // largest c in [0, C) with base[c] <= x (base has C + 1 nondecreasing entries)
+    uint32_t lo = 0, hi = C;
+    while (hi - lo > 1) {
+        uint32_t mid = (lo + hi) >> 1;
+        if (base[mid] <= x) lo = mid;
+        else hi = mid;
+    }
+    return lo;
+}
+
+__device__ __forceinline__ uint32_t find_u64(const uint64_t *base, uint32_t C, uint64_t x) {
+    uint32_t lo = 0, hi = C;
+    while (hi - lo > 1) {
+        uint32_t mid = (lo + hi) >> 1;
+        if (base[mid] <= x) lo = mid;
+        else hi = mid;
+    }
+    return lo;
+}
+
+__device__ __forceinline__ uint64_t mix64(uint64_t x) {
+    x ^= x >> 30;
+    x *= 0xbf58476d1ce4e5b9ull;
+    x ^= x >> 27;
+    x *= 0x94d049bb133111ebull;
+    x ^= x >> 31;
+    return x;
+}
+
+// merge_prob (dem.hpp:28-30) with explicit round-to-nearest ops: no FMA
+// contraction, bit-identical to the reference's x86-64 (no -march) build.
+__device__ __forceinline__ double merge_prob(double a, double b) {
+    return __dadd_rn(__dmul_rn(a, __dsub_rn(1.0, b)), __dmul_rn(b, __dsub_rn(1.0, a)));
+}
+
+__device__ __forceinline__ uint4 add4(uint4 a, uint4 b) {
+    return make_uint4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w);
+}
+
+template <class T>
+__device__ __forceinline__ const T *arr(const DevPlan &p, uint64_t off) {
+    return reinterpret_cast<const T *>(p.img + off);
+}
+
+// Components of each noise op as 4-bit masks (bit0 X on q0, bit1 Z on q0,
+// bit2 X on q1, bit3 Z on q1); a level keeps a prefix of each table.
+// DEPOLARIZE2 (kPairTable, stepg.cpp:49-58): L0 IX IZ XI XX ZI ZZ, L1 adds
+// IY XZ YI ZX, L2 adds XY YX YY YZ ZY. DEPOLARIZE1 (stepg.cpp:75-83): X Z, then Y.
+__constant__ uint8_t kDep2Mask[15] = {4, 8, 1, 5, 2, 10, 12, 9, 3, 6, 13, 7, 15, 11, 14};
+__constant__ uint8_t kDep1Mask[3] = {1, 2, 3};
+
+__host__ __device__ __forceinline__ uint32_t noise_components(uint32_t kind, uint32_t level) {
+    if (kind <= 1) return 1;
+    if (kind == 2) return level == 0 ? 2 : 3;
+    return level == 0 ? 6 : level == 1 ? 10 : 15;
+}
+
+// ---------------------------------------------------------------- PTX wrappers
+// Bulk async copy global -> shared, completion counted on an mbarrier
+// (the non-tensor TMA path: SASS UBLKCP).
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void mbar_fence_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t *bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+
+__device__ __forceinline__ bool mbar_try_wait(uint64_t *bar, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+    while (!mbar_try_wait(bar, parity)) {
+    }
+}
+
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+
+__device__ __forceinline__ void fence_proxy_async() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+// ---------------------------------------------------------------- K1 lowering
+// Part A: one warp per (circuit, layer): the gates of layer i fix the base
+// successors of boundary i-1 (stepg.cpp:196-234; untouched nodes stay idle =
+// word 0 from the memset), M/MR gates publish their flip-source probability,
+// noise ops publish their components' probabilities (p, p/3, p/15 with IEEE
+// division, stepg.cpp:66-103).
+// Part B: one thread per detector / observable toggles its bit into the leaf
+// rows of its measurements (init_leaves, eec.cpp:40-58).
+
+__global__ void lower_kernel(DevPlan p, uint32_t blocks_a) {
+    const uint32_t C = p.tot.C;
+    const CircuitMeta *meta = arr<CircuitMeta>(p, p.lay.meta);
+    if (blockIdx.x < blocks_a) {
+        const uint64_t gw = (uint64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+        const uint32_t lane = threadIdx.x & 31;
+        if (gw >= p.tot.layers) return;
+        const uint32_t *circ_layer = arr<uint32_t>(p, p.lay.circ_layer);
+        const uint32_t c = find_u32(circ_layer, C, (uint32_t)gw);
+        const CircuitMeta m = meta[c];
+        const uint32_t i = (uint32_t)gw - circ_layer[c];
+        const uint32_t li = m.layer_base + i;
+        const uint32_t *lay_gate = arr<uint32_t>(p, p.lay.lay_gate);
+        const uint32_t *lay_noise = arr<uint32_t>(p, p.lay.lay_noise);
+        const uint64_t *gates = arr<uint64_t>(p, p.lay.gates);
+        const double *flip = arr<double>(p, p.lay.meas_flip);
+        const uint64_t src_flip = m.src_base + m.src_noise;
+        for (uint32_t g = lay_gate[li] + lane; g < lay_gate[li + 1]; g += 32) {
+            const uint64_t w = gates[g];
+            const uint32_t lo = (uint32_t)w, hi = (uint32_t)(w >> 32);
+            const uint32_t q = lo & ((1u << kGateKindShift) - 1), kind = lo >> kGateKindShift;
+            if (kind == 3 || kind == 4) p.prob[src_flip + hi] = flip[m.meas_base + hi];
+            if (i == 0) continue;  // no boundary before layer 0
+            uint64_t *e = p.ell + m.ell_base + (uint64_t)(i - 1) * (2 * m.n);
+            const uint32_t x = 2 * q, z = 2 * q + 1;
+            switch (kind) {
+                case 0:  // H: X <-> Z
+                    e[x] = (uint64_t)kSuccNone << 32 | z;
+                    e[z] = (uint64_t)kSuccNone << 32 | x;
+                    break;
+                case 1: {  // CX q -> hi: X_c -> {X_c, X_t}, Z_c -> Z_c, X_t -> X_t, Z_t -> {Z_c, Z_t}
+                    const uint32_t xt = 2 * hi, zt = 2 * hi + 1;
+                    e[x] = (uint64_t)xt << 32 | x;
+                    e[z] = (uint64_t)kSuccNone << 32 | z;
+                    e[xt] = (uint64_t)kSuccNone << 32 | xt;
+                    e[zt] = (uint64_t)zt << 32 | z;
+                    break;
+                }
+                case 2:  // R
+                    e[x] = kEllDead;
+                    e[z] = kEllDead;
+                    break;
+                case 3:  // M: X -> {leaf, X}, Z -> none
+                    e[x] = (uint64_t)x << 32 | (kSuccLeaf | hi);
+                    e[z] = kEllDead;
+                    break;
+                default:  // MR: X -> {leaf}, Z -> none
+                    e[x] = (uint64_t)kSuccNone << 32 | (kSuccLeaf | hi);
+                    e[z] = kEllDead;
+                    break;
+            }
+        }
+        const uint64_t *noise = arr<uint64_t>(p, p.lay.noise);
+        const double *nprob = arr<double>(p, p.lay.noise_prob);
+        const uint32_t *nsrc = arr<uint32_t>(p, p.lay.noise_src);
+        for (uint32_t o = lay_noise[li] + lane; o < lay_noise[li + 1]; o += 32) {
+            const uint32_t kind = (uint32_t)noise[o] >> kNoiseKindShift;
+            const double pr = nprob[o];
+            const double pe = kind == 2 ? __ddiv_rn(pr, 3.0) : kind == 3 ? __ddiv_rn(pr, 15.0) : pr;
+            const uint32_t k = noise_components(kind, p.tot.level);
+            double *dst = p.prob + m.src_base + nsrc[o];
+            for (uint32_t j = 0; j < k; j++) dst[j] = pe;
+        }
+        return;
+    }
+    // Part B.
+    const uint64_t t = (uint64_t)(blockIdx.x - blocks_a) * blockDim.x + threadIdx.x;
+    if (t < p.tot.dets) {
+        const uint32_t c = find_u32(arr<uint32_t>(p, p.lay.circ_det), C, (uint32_t)t);
+        const CircuitMeta m = meta[c];
+        const uint32_t d = (uint32_t)t - arr<uint32_t>(p, p.lay.circ_det)[c];
+        const uint32_t *off = arr<uint32_t>(p, p.lay.det_off) + m.det_base;
+        const uint32_t *ms = arr<uint32_t>(p, p.lay.det_meas);
+        uint64_t *row = p.leaf + m.leaf_base + (uint64_t)(d >> 6) * m.M;
+        for (uint32_t k = off[d]; k < off[d + 1]; k++)
+            atomicXor((unsigned long long *)&row[ms[k]], 1ull << (d & 63));
+    } else if (t < p.tot.dets + p.tot.obss) {
+        const uint32_t to = (uint32_t)(t - p.tot.dets);
+        const uint32_t c = find_u32(arr<uint32_t>(p, p.lay.circ_obs), C, to);
+        const CircuitMeta m = meta[c];
+        const uint32_t o = to - arr<uint32_t>(p, p.lay.circ_obs)[c];
+        const uint32_t b = m.D + o;
+        const uint32_t *off = arr<uint32_t>(p, p.lay.obs_off) + m.obs_base;
+        const uint32_t *ms = arr<uint32_t>(p, p.lay.obs_meas);
+        uint64_t *row = p.leaf + m.leaf_base + (uint64_t)(b >> 6) * m.M;
+        for (uint32_t k = off[o]; k < off[o + 1]; k++)
+            atomicXor((unsigned long long *)&row[ms[k]], 1ull << (b & 63));
+    }
+}
+
+// ---------------------------------------------------------------- K2 traversal
+// One CTA per (circuit, 64-bit detector column tile). The CTA keeps the tile's
+// column of the class matrix for boundaries i+1 and i in shared memory
+// (2 x 2n words) and walks the boundaries backwards (Alg. 1, PAPER.md:199-232;
+// eec.cpp:111-122) with one CTA barrier per boundary -- no grid sync, no
+// per-layer launch. Each boundary's ELLPACK slice, noise ops and the leaf
+// words of the next layer's measurements are staged into a ring of shared
+// buffers by bulk async copies issued NST-1 boundaries ahead.
+// Time window: the tile starts at the last layer holding one of its
+// measurements and stops once its column is all zero below its first one.
+// Fused epilogue per boundary: every noise op placed there XORs <= 4 base
+// rows per component and emits only nonzero words (source, tile, bits).
+
+// Shared-memory carve-up of the traversal CTA: two state columns (boundary
+// i+1 and i, 2n words each) followed by `stages` staging buffers and one
+// mbarrier per stage. Word counts cover the 16-byte rounding of bulk copies.
+struct TravDims {
+    uint32_t n2, stages, ell_words, leaf_words, noise_words, src_words;
+    __host__ __device__ TravDims(uint32_t max_n, uint32_t max_meas, uint32_t max_noise, uint32_t k)
+        : n2(2 * max_n),
+          stages(k),
+          ell_words(2 * max_n),
+          leaf_words((max_meas + 3) & ~1u),
+          noise_words((max_noise + 3) & ~1u),
+          src_words((max_noise + 9) & ~3u) {}
+    __host__ __device__ size_t state_bytes() const { return (size_t)2 * n2 * 8; }
+    __host__ __device__ size_t stage_bytes() const {
+        return (size_t)(ell_words + leaf_words + noise_words) * 8 + (size_t)src_words * 4;
+    }
+    __host__ __device__ size_t total_bytes() const { return state_bytes() + stages * stage_bytes() + stages * 8; }
+    __device__ uint64_t *state(uint8_t *base, int which) const {
+        return reinterpret_cast<uint64_t *>(base) + (size_t)which * n2;
+    }
+    __device__ uint8_t *stage(uint8_t *base, int k) const { return base + state_bytes() + (size_t)k * stage_bytes(); }
+    __device__ uint64_t *bars(uint8_t *base) const { return reinterpret_cast<uint64_t *>(stage(base, stages)); }
+};
+
+__device__ __forceinline__ void emit(const DevPlan &p, uint64_t src, uint32_t tile, uint64_t bits) {
+    const uint32_t j = atomicAdd(&p.cnt[src], 1u);
+    if (j < p.K) {
+        p.rbits[src * p.K + j] = bits;
+        p.rtile[src * p.K + j] = tile;
+    } else {
+        atomicMax(&p.hdr->record_overflow, j + 1);
+    }
+}
+
+__global__ void __launch_bounds__(1024) traverse_kernel(DevPlan p, uint32_t stages, uint32_t max_n,
+                                                        uint32_t max_layer_noise, uint32_t max_layer_meas) {
+    extern __shared__ __align__(16) uint8_t smem[];
+    __shared__ uint32_t s_min_m, s_max_m;
+    __shared__ CircuitMeta s_meta;
+    __shared__ uint32_t s_c;
+
+    const uint32_t tid = threadIdx.x, nthr = blockDim.x;
+    if (tid == 0) {
+        s_c = find_u32(arr<uint32_t>(p, p.lay.circ_tile), p.tot.C, blockIdx.x);
+        s_meta = arr<CircuitMeta>(p, p.lay.meta)[s_c];
+        s_min_m = 0xFFFFFFFFu;
+        s_max_m = 0;
+    }
+    __syncthreads();
+    const CircuitMeta m = s_meta;
+    const uint32_t t = blockIdx.x - m.tile_base;
+    const uint32_t n2 = 2 * m.n;
+
+    // Measurement window of this tile's detectors / observables.
+    {
+        const uint32_t d0 = t * 64, d1 = min(d0 + 64, m.D);
+        const uint32_t *doff = arr<uint32_t>(p, p.lay.det_off) + m.det_base;
+        const uint32_t *dms = arr<uint32_t>(p, p.lay.det_meas);
+        uint32_t lo = 0xFFFFFFFFu, hi = 0;
+        for (uint32_t d = d0 + tid; d < d1; d += nthr)
+            for (uint32_t k = doff[d]; k < doff[d + 1]; k++) {
+                lo = min(lo, dms[k]);
+                hi = max(hi, dms[k]);
+            }
+        const uint32_t ob0 = max(d0, m.D), ob1 = min(t * 64 + 64, m.D + m.O);
+        const uint32_t *ooff = arr<uint32_t>(p, p.lay.obs_off) + m.obs_base;
+        const uint32_t *oms = arr<uint32_t>(p, p.lay.obs_meas);
+        for (uint32_t b = ob0; b < ob1; b++) {  // few observables: spread their entries
+            const uint32_t o = b - m.D;
+            for (uint32_t k = ooff[o] + tid; k < ooff[o + 1]; k += nthr) {
+                lo = min(lo, oms[k]);
+                hi = max(hi, oms[k]);
+            }
+        }
+        if (lo != 0xFFFFFFFFu) {
+            atomicMin(&s_min_m, lo);
+            atomicMax(&s_max_m, hi);
+        }
+    }
+    __syncthreads();
+    const uint32_t min_m = s_min_m, max_m = s_max_m;
+    if (min_m == 0xFFFFFFFFu) return;  // column all zero
+
+    const uint64_t *leafrow = p.leaf + m.leaf_base + (uint64_t)t * m.M;
+    const uint64_t src_flip = m.src_base + m.src_noise;
+
+    // Measurement-flip sources: their rows are the leaf rows (stepg.cpp:270-272).
+    {
+        const double *flip = arr<double>(p, p.lay.meas_flip) + m.meas_base;
+        for (uint32_t mm = min_m + tid; mm <= max_m; mm += nthr) {
+            if (flip[mm] > 0) {
+                const uint64_t w = leafrow[mm];
+                if (w) emit(p, src_flip + mm, t, w);
+            }
+        }
+    }
+
+    const uint32_t *lay_meas = arr<uint32_t>(p, p.lay.lay_meas) + m.layer_base;
+    const uint32_t *lay_noise = arr<uint32_t>(p, p.lay.lay_noise) + m.layer_base;
+    auto layer_of = [&](uint32_t mm) {  // largest i with lay_meas[i] <= mm
+        uint32_t lo = 0, hi = m.l;
+        while (hi - lo > 1) {
+            uint32_t mid = (lo + hi) >> 1;
+            if (lay_meas[mid] <= mm) lo = mid;
+            else hi = mid;
+        }
+        return lo;
+    };
+    const int first_layer = (int)layer_of(min_m);
+    const int b_hi = (int)layer_of(max_m) - 1;
+    if (b_hi < 0) return;
+
+    const TravDims L(max_n, max_layer_meas, max_layer_noise, stages);
+    uint64_t *bars = L.bars(smem);
+    uint64_t *st[2] = {L.state(smem, 0), L.state(smem, 1)};
+
+    const uint64_t *ell = p.ell + m.ell_base;
+    const uint64_t *noise = arr<uint64_t>(p, p.lay.noise);
+    const uint32_t *nsrc = arr<uint32_t>(p, p.lay.noise_src);
+
+    // Stage k holds boundary i: ELL slice of i, leaf words of layer i+1's
+    // measurements, noise ops of layer i (+ their source offsets).
+    auto issue = [&](int i, int k) {
+        uint8_t *sb = L.stage(smem, k);
+        uint64_t *s_ell = reinterpret_cast<uint64_t *>(sb);
+        uint64_t *s_leaf = s_ell + L.ell_words;
+        uint64_t *s_noise = s_leaf + L.leaf_words;
+        uint32_t *s_src = reinterpret_cast<uint32_t *>(s_noise + L.noise_words);
+        const uint32_t mb = lay_meas[i + 1], me = lay_meas[i + 2];  // i <= l - 2
+        const uint64_t leaf_a = (uint64_t)(leafrow + mb) & ~15ull;
+        const uint64_t leaf_e = ((uint64_t)(leafrow + me) + 15) & ~15ull;
+        const uint32_t n0 = lay_noise[i], n1 = lay_noise[i + 1];
+        const uint64_t noise_a = (uint64_t)(noise + n0) & ~15ull;
+        const uint64_t noise_e = ((uint64_t)(noise + n1) + 15) & ~15ull;
+        const uint64_t src_a = (uint64_t)(nsrc + n0) & ~15ull;
+        const uint64_t src_e = ((uint64_t)(nsrc + n1) + 15) & ~15ull;
+        const uint32_t b_ell = n2 * 8;
+        const uint32_t b_leaf = me > mb ? (uint32_t)(leaf_e - leaf_a) : 0;
+        const uint32_t b_noise = n1 > n0 ? (uint32_t)(noise_e - noise_a) : 0;
+        const uint32_t b_src = n1 > n0 ? (uint32_t)(src_e - src_a) : 0;
+        fence_proxy_async();
+        mbar_arrive_expect_tx(&bars[k], b_ell + b_leaf + b_noise + b_src);
+        bulk_g2s(s_ell, ell + (uint64_t)i * n2, b_ell, &bars[k]);
+        if (b_leaf) bulk_g2s(s_leaf, (const void *)leaf_a, b_leaf, &bars[k]);
+        if (b_noise) bulk_g2s(s_noise, (const void *)noise_a, b_noise, &bars[k]);
+        if (b_src) bulk_g2s(s_src, (const void *)src_a, b_src, &bars[k]);
+    };
+
+    if (tid == 0) {
+        for (uint32_t k = 0; k < stages; k++) mbar_init(&bars[k], 1);
+        mbar_fence_init();
+    }
+    for (uint32_t s = tid; s < n2; s += nthr) st[0][s] = 0;  // boundary b_hi + 1 is all zero
+    __syncthreads();
+    if (tid == 0)
+        for (int j = 0; j < (int)stages - 1 && b_hi - j >= 0; j++) issue(b_hi - j, j);
+
+    const uint32_t level = p.tot.level;
+    int cur = 0;  // st[cur] = boundary i + 1
+    int i = b_hi;
+    for (; i >= 0; i--) {
+        const int j = b_hi - i;
+        const int k = j % (int)stages;
+        mbar_wait(&bars[k], (uint32_t)(j / (int)stages) & 1u);
+        uint8_t *sb = L.stage(smem, k);
+        const uint64_t *s_ell = reinterpret_cast<const uint64_t *>(sb);
+        const uint64_t *s_leaf = s_ell + L.ell_words;
+        const uint64_t *s_noise = s_leaf + L.leaf_words;
+        const uint32_t *s_src = reinterpret_cast<const uint32_t *>(s_noise + L.noise_words);
+        const uint32_t mb = lay_meas[i + 1];
+        const uint32_t leaf_shift = (uint32_t)(((uint64_t)(leafrow + mb) & 15ull) >> 3);
+        const uint64_t *nxt = st[cur];
+        uint64_t *now = st[cur ^ 1];
+        bool any = false;
+        for (uint32_t s = tid; s < n2; s += nthr) {
+            const uint64_t w = s_ell[s];
+            uint64_t acc;
+            if (w == kEllIdle) {
+                acc = nxt[s];
+            } else {
+                acc = 0;
+                const uint32_t v0 = (uint32_t)w, v1 = (uint32_t)(w >> 32);
+                if (v0 != kSuccNone) acc ^= (v0 & kSuccLeaf) ? s_leaf[leaf_shift + (v0 & ~kSuccLeaf) - mb] : nxt[v0];
+                if (v1 != kSuccNone) acc ^= (v1 & kSuccLeaf) ? s_leaf[leaf_shift + (v1 & ~kSuccLeaf) - mb] : nxt[v1];
+            }
+            now[s] = acc;
+            any |= acc != 0;
+        }
+        const bool block_any = __syncthreads_or(any);
+        if (!block_any && first_layer > i) break;  // column is zero from here down
+        if (tid == 0 && i + 1 - (int)stages >= 0) issue(i + 1 - (int)stages, (j + (int)stages - 1) % (int)stages);
+        if (block_any) {
+            const uint32_t n0 = lay_noise[i], n1 = lay_noise[i + 1];
+            const uint32_t nshift = (uint32_t)(((uint64_t)(noise + n0) & 15ull) >> 3);
+            const uint32_t sshift = (uint32_t)(((uint64_t)(nsrc + n0) & 15ull) >> 2);
+            for (uint32_t o = tid; o < n1 - n0; o += nthr) {
+                const uint64_t w = s_noise[nshift + o];
+                const uint32_t lo = (uint32_t)w;
+                const uint32_t kind = lo >> kNoiseKindShift;
+                const uint32_t q0 = lo & ((1u << kNoiseKindShift) - 1), q1 = (uint32_t)(w >> 32);
+                const uint64_t src = m.src_base + s_src[sshift + o];
+                const uint64_t x0 = now[2 * q0], z0 = now[2 * q0 + 1];
+                if (kind <= 1) {
+                    const uint64_t v = kind == 0 ? x0 : z0;
+                    if (v) emit(p, src, t, v);
+                } else if (kind == 2) {
+                    const uint32_t nc = level == 0 ? 2 : 3;
+                    for (uint32_t c = 0; c < nc; c++) {
+                        const uint32_t mk = kDep1Mask[c];
+                        const uint64_t v = ((mk & 1) ? x0 : 0) ^ ((mk & 2) ? z0 : 0);
+                        if (v) emit(p, src + c, t, v);
+                    }
+                } else {
+                    const uint64_t x1 = now[2 * q1], z1 = now[2 * q1 + 1];
+                    if ((x0 | z0 | x1 | z1) == 0) continue;
+                    const uint32_t nc = level == 0 ? 6 : level == 1 ? 10 : 15;
+                    for (uint32_t c = 0; c < nc; c++) {
+                        const uint32_t mk = kDep2Mask[c];
+                        const uint64_t v = ((mk & 1) ? x0 : 0) ^ ((mk & 2) ? z0 : 0) ^ ((mk & 4) ? x1 : 0) ^
+                                           ((mk & 8) ? z1 : 0);
+                        if (v) emit(p, src + c, t, v);
+                    }
+                }
+            }
+        }
+        cur ^= 1;
+    }
+    // Drain bulk copies still in flight after an early exit.
+    if (i >= 0) {
+        const int lowest = max(0, i + 2 - (int)stages);  // issued: [lowest, i - 1]
+        for (int b = i - 1; b >= lowest; b--) {
+            const int j = b_hi - b;
+            mbar_wait(&bars[j % (int)stages], (uint32_t)(j / (int)stages) & 1u);
+        }
+    }
+}
+
+// ---------------------------------------------------------------- K3 dedup
+// Groups sources with identical sparse signatures (the exact-equality
+// grouping of reduce_packed, dem.cpp:73-91): an order-independent 64-bit key
+// over the (tile, word) records, open addressing with linear probing, and a
+// FULL record comparison before two sources are merged -- hash collisions
+// never merge distinct signatures (dem.cpp:73-78, test_dem.cpp:94-101).
+
+__device__ __forceinline__ bool same_signature(const DevPlan &p, uint64_t a, uint64_t b, uint32_t n) {
+    if (p.cnt[b] != n) return false;
+    for (uint32_t x = 0; x < n; x++) {
+        const uint32_t ta = p.rtile[a * p.K + x];
+        const uint64_t ba = p.rbits[a * p.K + x];
+        bool found = false;
+        for (uint32_t y = 0; y < n; y++)
+            if (p.rtile[b * p.K + y] == ta) {
+                found = p.rbits[b * p.K + y] == ba;
+                break;
+            }
+        if (!found) return false;
+    }
+    return true;
+}
+
+__global__ void dedup_kernel(DevPlan p) {
+    const uint64_t s = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= p.tot.sources) return;
+    if (p.hdr->record_overflow) return;
+    const uint32_t n = p.cnt[s];
+    if (n == 0) {  // empty signature: dropped (dem.cpp:93)
+        p.rep[s] = kSuccNone;
+        return;
+    }
+    const uint64_t *circ_src = arr<uint64_t>(p, p.lay.circ_src);
+    const uint32_t c = find_u64(circ_src, p.tot.C, s);
+    const uint64_t lo_s = circ_src[c], hi_s = circ_src[c + 1];
+    const uint32_t D = arr<CircuitMeta>(p, p.lay.meta)[c].D;
+    uint64_t h = mix64(0x9e3779b97f4a7c15ull + c);
+    uint32_t nd = 0, no = 0;
+    for (uint32_t x = 0; x < n; x++) {
+        const uint32_t tile = p.rtile[s * p.K + x];
+        const uint64_t bits = p.rbits[s * p.K + x];
+        h ^= mix64(bits ^ mix64(0x632be59bd9b4e019ull + tile));
+        const uint32_t b0 = tile * 64;
+        uint64_t dm;
+        if (b0 + 64 <= D) dm = ~0ull;
+        else if (b0 >= D) dm = 0;
+        else dm = (1ull << (D - b0)) - 1;
+        nd += __popcll(bits & dm);
+        no += __popcll(bits & ~dm);
+    }
+    h = mix64(h);
+    if (p.force_collisions) h = 42;
+    const uint64_t mykey = (h & 0xFFFFFFFF00000000ull) | (uint32_t)s;
+    uint64_t idx = (h ^ (h >> 31)) & p.table_mask;
+    uint32_t rep = kSuccNone;
+    while (true) {
+        unsigned long long cur = p.table[idx];
+        if (cur == ~0ull) {
+            cur = atomicCAS((unsigned long long *)&p.table[idx], ~0ull, (unsigned long long)mykey);
+            if (cur == ~0ull) {
+                rep = (uint32_t)s;
+                break;
+            }
+        }
+        if ((cur >> 32) == (mykey >> 32)) {
+            const uint32_t r = (uint32_t)cur;
+            if (r >= lo_s && r < hi_s && same_signature(p, s, r, n)) {
+                rep = r;
+                break;
+            }
+        }
+        idx = (idx + 1) & p.table_mask;
+    }
+    p.rep[s] = rep;
+    if (rep == (uint32_t)s) p.ecnt[s] = make_uint2(nd, no);
+    atomicAdd(&p.gcnt[rep], 1u);
+}
+
+// ---------------------------------------------------------------- scans
+// Exclusive scan of uint4 values produced by a functor: reduce tiles ->
+// scan tile sums in one CTA -> rescan tiles with offsets.
+
+constexpr int kScanThreads = 256, kScanItems = 8, kScanTile = kScanThreads * kScanItems;
+
+__device__ __forceinline__ uint4 warp_incl_scan(uint4 v) {
+    const uint32_t lane = threadIdx.x & 31;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        uint4 o;
+        o.x = __shfl_up_sync(0xffffffffu, v.x, d);
+        o.y = __shfl_up_sync(0xffffffffu, v.y, d);
+        o.z = __shfl_up_sync(0xffffffffu, v.z, d);
+        o.w = __shfl_up_sync(0xffffffffu, v.w, d);
+        if (lane >= (uint32_t)d) v = add4(v, o);
+    }
+    return v;
+}
+
+// Block-wide exclusive scan; returns the exclusive prefix and the block total.
+__device__ __forceinline__ uint4 block_excl_scan(uint4 v, uint4 *total) {
+    __shared__ uint4 warp_tot[32];
+    const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const uint4 incl = warp_incl_scan(v);
+    if (lane == 31) warp_tot[wid] = incl;
+    __syncthreads();
+    if (wid == 0) {
+        uint4 w = lane < nw ? warp_tot[lane] : make_uint4(0, 0, 0, 0);
+        w = warp_incl_scan(w);
+        if (lane < nw) warp_tot[lane] = w;
+    }
+    __syncthreads();
+    const uint4 before = wid ? warp_tot[wid - 1] : make_uint4(0, 0, 0, 0);
+    *total = warp_tot[nw - 1];
+    __syncthreads();
+    return add4(before, make_uint4(incl.x - v.x, incl.y - v.y, incl.z - v.z, incl.w - v.w));
+}
+
+template <class F>
+__global__ void scan_reduce_kernel(F f, uint64_t n, uint4 *bsum) {
+    const uint64_t base = (uint64_t)blockIdx.x * kScanTile;
+    uint4 acc = make_uint4(0, 0, 0, 0);
+    if (f.active(base)) {
+#pragma unroll
+        for (int k = 0; k < kScanItems; k++) {
+            const uint64_t idx = base + (uint64_t)k * kScanThreads + threadIdx.x;
+            if (idx < n) acc = add4(acc, f(idx));
+        }
+    }
+    uint4 tot;
+    block_excl_scan(acc, &tot);
+    if (threadIdx.x == 0) bsum[blockIdx.x] = tot;
+}
+
+__global__ void scan_blocks_kernel(uint4 *bsum, uint32_t nb, uint4 *total_out) {
+    const uint32_t per = (nb + blockDim.x - 1) / blockDim.x;
+    const uint32_t b0 = threadIdx.x * per, b1 = min(nb, b0 + per);
+    uint4 acc = make_uint4(0, 0, 0, 0);
+    for (uint32_t b = b0; b < b1; b++) acc = add4(acc, bsum[b]);
+    uint4 tot;
+    uint4 run = block_excl_scan(acc, &tot);
+    for (uint32_t b = b0; b < b1; b++) {
+        const uint4 v = bsum[b];
+        bsum[b] = run;
+        run = add4(run, v);
+    }
+    if (threadIdx.x == 0) *total_out = tot;
+}
+
+template <class F>
+__global__ void scan_apply_kernel(F f, uint64_t n, const uint4 *bsum, uint4 *out) {
+    const uint64_t base = (uint64_t)blockIdx.x * kScanTile;
+    if (!f.active(base)) return;
+    uint4 v[kScanItems];
+    uint4 acc = make_uint4(0, 0, 0, 0);
+#pragma unroll
+    for (int k = 0; k < kScanItems; k++) {
+        const uint64_t idx = base + (uint64_t)threadIdx.x * kScanItems + k;
+        v[k] = idx < n ? f(idx) : make_uint4(0, 0, 0, 0);
+        acc = add4(acc, v[k]);
+    }
+    uint4 tot;
+    uint4 run = add4(block_excl_scan(acc, &tot), bsum[blockIdx.x]);
+#pragma unroll
+    for (int k = 0; k < kScanItems; k++) {
+        const uint64_t idx = base + (uint64_t)threadIdx.x * kScanItems + k;
+        if (idx < n) out[idx] = run;
+        run = add4(run, v[k]);
+    }
+}
+
+struct SrcScanF {  // (edges, members, ids) per representative source
+    const uint32_t *rep, *gcnt;
+    const uint2 *ecnt;
+    const DeviceHeader *hdr;
+    __device__ bool active(uint64_t) const { return hdr->record_overflow == 0; }
+    __device__ uint4 operator()(uint64_t s) const {
+        if (rep[s] != (uint32_t)s) return make_uint4(0, 0, 0, 0);
+        const uint2 e = ecnt[s];
+        return make_uint4(1, gcnt[s], e.x + e.y, 0);
+    }
+};
+
+struct BucketScanF {
+    const uint32_t *bcount;
+    __device__ bool active(uint64_t) const { return true; }
+    __device__ uint4 operator()(uint64_t b) const { return make_uint4(bcount[b], 0, 0, 0); }
+};
+
+struct PosScanF {  // (detector ids, observable ids) in canonical order
+    const uint32_t *perm, *nd, *no;
+    const DeviceHeader *hdr;
+    __device__ bool active(uint64_t base) const { return base < hdr->num_edges; }
+    __device__ uint4 operator()(uint64_t q) const {
+        if (q >= hdr->num_edges) return make_uint4(0, 0, 0, 0);
+        const uint32_t e = perm[q];
+        return make_uint4(nd[e], no[e], 0, 0);
+    }
+};
+
+// ---------------------------------------------------------------- K5..K9
+
+__global__ void totals_kernel(DevPlan p, const uint4 *src_total) {
+    // after the source scan: publish edge / member / id totals, check capacity
+    const uint4 t = *src_total;
+    p.hdr->num_edges = t.x;
+    p.hdr->num_members = t.y;
+    if ((uint64_t)t.z > p.ids_cap) p.hdr->num_det_ids = 0xFFFFFFFFu;  // capacity overflow marker
+    p.e_moff[t.x] = t.y;
+    // per-circuit edge offsets
+    const uint64_t *circ_src = arr<uint64_t>(p, p.lay.circ_src);
+    for (uint32_t c = 0; c <= p.tot.C; c++) {
+        const uint64_t s0 = circ_src[c];
+        p.o_edge_off[c] = s0 < p.tot.sources ? p.sscan[s0].x : t.x;
+    }
+}
+
+__device__ __forceinline__ bool pipeline_failed(const DevPlan &p) {
+    return p.hdr->record_overflow != 0 || p.hdr->num_det_ids == 0xFFFFFFFFu;
+}
+
+// Scatter member probabilities next to their edge; record edge -> source.
+__global__ void scatter_kernel(DevPlan p) {
+    const uint64_t s = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= p.tot.sources || pipeline_failed(p)) return;
+    const uint32_t r = p.rep[s];
+    if (r == kSuccNone) return;
+    const uint4 sc = p.sscan[r];
+    const uint32_t pos = sc.y + atomicSub(&p.gcnt[r], 1u) - 1;
+    p.mprob[pos] = p.prob[s];
+    if (r == (uint32_t)s) {
+        p.e_src[sc.x] = r;
+        p.e_idoff[sc.x] = sc.z;
+        p.e_moff[sc.x] = sc.y;
+        const uint2 e = p.ecnt[r];
+        p.e_nd[sc.x] = e.x;
+        p.e_no[sc.x] = e.y;
+    }
+}
+
+// Per edge: sorted ascending fold from 0 (dem.cpp:97-106), id list expansion
+// (bit b < D -> detector b, else observable b - D; dem.cpp:108-116), bucket
+// by first detector for the canonical sort.
+__global__ void finalize_kernel(DevPlan p) {
+    const uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (pipeline_failed(p) || e >= p.hdr->num_edges) return;
+    const uint32_t m0 = p.e_moff[e], m1 = p.e_moff[e + 1], nm = m1 - m0;
+    double *mp = p.mprob + m0;
+    double acc = 0;
+    if (nm <= 32) {
+        double v[32];
+        for (uint32_t a = 0; a < nm; a++) {
+            const double x = mp[a];
+            uint32_t b = a;
+            while (b > 0 && v[b - 1] > x) {
+                v[b] = v[b - 1];
+                b--;
+            }
+            v[b] = x;
+        }
+        for (uint32_t a = 0; a < nm; a++) acc = merge_prob(acc, v[a]);
+    } else {  // rare large groups: in-place insertion sort in global memory
+        for (uint32_t a = 1; a < nm; a++) {
+            const double x = mp[a];
+            uint32_t b = a;
+            while (b > 0 && mp[b - 1] > x) {
+                mp[b] = mp[b - 1];
+                b--;
+            }
+            mp[b] = x;
+        }
+        for (uint32_t a = 0; a < nm; a++) acc = merge_prob(acc, mp[a]);
+    }
+    p.e_prob[e] = acc;
+
+    // ids: records sorted by tile, bits ascending
+    const uint32_t r = p.e_src[e];
+    const uint32_t n = p.cnt[r];
+    uint32_t order[16];
+    uint32_t nn = 0;
+    const uint32_t K = p.K;
+    for (uint32_t x = 0; x < n && x < 16; x++) {
+        const uint32_t tx = p.rtile[(uint64_t)r * K + x];
+        uint32_t b = nn++;
+        while (b > 0 && p.rtile[(uint64_t)r * K + order[b - 1]] > tx) {
+            order[b] = order[b - 1];
+            b--;
+        }
+        order[b] = x;
+    }
+    uint32_t *out = p.tid + p.e_idoff[e];
+    uint32_t w = 0;
+    for (uint32_t x = 0; x < nn; x++) {
+        const uint32_t tile = p.rtile[(uint64_t)r * K + order[x]];
+        uint64_t bits = p.rbits[(uint64_t)r * K + order[x]];
+        while (bits) {
+            const uint32_t b = __ffsll((long long)bits) - 1;
+            bits &= bits - 1;
+            out[w++] = tile * 64 + b;
+        }
+    }
+    const uint32_t c = find_u64(arr<uint64_t>(p, p.lay.circ_src), p.tot.C, r);
+    const CircuitMeta m = arr<CircuitMeta>(p, p.lay.meta)[c];
+    p.e_circ[e] = c;
+    const uint32_t bkt = m.bucket_base + (p.e_nd[e] ? out[0] + 1 : 0);
+    p.e_bucket[e] = bkt;
+    atomicAdd(&p.bcount[bkt], 1u);
+}
+
+__global__ void bucket_scatter_kernel(DevPlan p) {
+    const uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (pipeline_failed(p) || e >= p.hdr->num_edges) return;
+    const uint32_t b = p.e_bucket[e];
+    const uint32_t pos = p.boff[b].x + atomicSub(&p.bcount[b], 1u) - 1;
+    p.blist[pos] = (uint32_t)e;
+}
+
+// Canonical order (dem.cpp:122-127): std::vector lexicographic compare on
+// detectors (a prefix sorts first), then on observables.
+__device__ __forceinline__ int cmp_ids(const uint32_t *a, uint32_t na, const uint32_t *b, uint32_t nb) {
+    const uint32_t k = min(na, nb);
+    for (uint32_t x = 0; x < k; x++)
+        if (a[x] != b[x]) return a[x] < b[x] ? -1 : 1;
+    return na < nb ? -1 : na > nb ? 1 : 0;
+}
+
+__device__ __forceinline__ bool edge_less(const DevPlan &p, uint32_t a, uint32_t b) {
+    const uint32_t *ia = p.tid + p.e_idoff[a], *ib = p.tid + p.e_idoff[b];
+    const uint32_t nda = p.e_nd[a], ndb = p.e_nd[b];
+    const int c = cmp_ids(ia, nda, ib, ndb);
+    if (c) return c < 0;
+    return cmp_ids(ia + nda, p.e_no[a], ib + ndb, p.e_no[b]) < 0;
+}
+
+// Rank sort inside each bucket (edges sharing circuit and first detector):
+// all keys are distinct, so ranks form a permutation.
+__global__ void rank_kernel(DevPlan p) {
+    const uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (pipeline_failed(p) || e >= p.hdr->num_edges) return;
+    const uint32_t b = p.e_bucket[e];
+    const uint32_t lo = p.boff[b].x, hi = p.boff[b + 1].x;
+    uint32_t rank = 0;
+    for (uint32_t k = lo; k < hi; k++) {
+        const uint32_t o = p.blist[k];
+        if (o != (uint32_t)e && edge_less(p, o, (uint32_t)e)) rank++;
+    }
+    p.perm[lo + rank] = (uint32_t)e;
+}
+
+__global__ void gather_kernel(DevPlan p, const uint4 *pos_total) {
+    const uint64_t q = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (pipeline_failed(p)) return;
+    const uint32_t E = p.hdr->num_edges;
+    if (q == 0) {
+        const uint4 t = *pos_total;
+        p.o_det_off[E] = t.x;
+        p.o_obs_off[E] = t.y;
+        p.hdr->num_det_ids = t.x;
+        p.hdr->num_obs_ids = t.y;
+    }
+    if (q >= E) return;
+    const uint32_t e = p.perm[q];
+    const uint4 o = p.pscan[q];
+    p.o_det_off[q] = o.x;
+    p.o_obs_off[q] = o.y;
+    p.o_prob[q] = p.e_prob[e];
+    const uint32_t *ids = p.tid + p.e_idoff[e];
+    const uint32_t nd = p.e_nd[e], no = p.e_no[e];
+    const uint32_t D = arr<CircuitMeta>(p, p.lay.meta)[p.e_circ[e]].D;
+    for (uint32_t x = 0; x < nd; x++) p.o_det[o.x + x] = ids[x];
+    for (uint32_t x = 0; x < no; x++) p.o_obs[o.y + x] = ids[nd + x] - D;
+}
+
+template <class F>
+void launch_scan(F f, uint64_t n, uint4 *bsum, uint4 *out, uint4 *total, cudaStream_t st, int *launches) {
+    const uint32_t nb = (uint32_t)((n + kScanTile - 1) / kScanTile);
+    if (nb == 0) {
+        cudaMemsetAsync(total, 0, sizeof(uint4), st);
+        (*launches)++;
+        return;
+    }
+    scan_reduce_kernel<<<nb, kScanThreads, 0, st>>>(f, n, bsum);
+    scan_blocks_kernel<<<1, 1024, 0, st>>>(bsum, nb, total);
+    scan_apply_kernel<<<nb, kScanThreads, 0, st>>>(f, n, bsum, out);
+    *launches += 3;
+}
+
+uint32_t blocks_for(uint64_t n, uint32_t tpb) { return (uint32_t)((n + tpb - 1) / tpb); }
+
+}  // namespace
+
+bool traversal_smem(const BatchTotals &t, int device, size_t *bytes, int *stages, int *threads) {
+    int optin = 0;
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
+    const size_t budget = (size_t)optin - 1024;  // static shared variables + slack
+    int k = kTravStagesMax;
+    while (k > 2 && TravDims(t.max_n, t.max_layer_meas, t.max_layer_noise, k).total_bytes() > budget) k--;
+    *stages = k;
+    *bytes = TravDims(t.max_n, t.max_layer_meas, t.max_layer_noise, k).total_bytes();
+    const uint32_t n2 = 2 * t.max_n;
+    *threads = n2 <= 256 ? 128 : n2 <= 1024 ? 256 : n2 <= 4096 ? 512 : 1024;
+    return *bytes <= budget;
+}
+
+int enqueue_pipeline(const DevPlan &p, cudaStream_t st, const StageEvents *ev, cudaError_t *err) {
+    int launches = 0;
+    const uint64_t S = p.tot.sources;
+    // Zero / sentinel fills.
+    if (p.tot.ell) cudaMemsetAsync(p.ell, 0, p.tot.ell * 8, st), launches++;
+    if (p.tot.leaf) cudaMemsetAsync(p.leaf, 0, p.tot.leaf * 8, st), launches++;
+    cudaMemsetAsync(p.cnt, 0, S * 4 + 4, st), launches++;
+    cudaMemsetAsync(p.gcnt, 0, S * 4 + 4, st), launches++;
+    cudaMemsetAsync(p.table, 0xFF, (p.table_mask + 1) * 8, st), launches++;
+    cudaMemsetAsync(p.bcount, 0, p.tot.buckets * 4 + 4, st), launches++;
+    cudaMemsetAsync(p.hdr, 0, sizeof(DeviceHeader), st), launches++;
+
+    // K1 lowering.
+    {
+        const uint32_t tpb = 256;
+        const uint32_t ba = blocks_for(p.tot.layers, tpb / 32);
+        const uint32_t bb = blocks_for(p.tot.dets + p.tot.obss, tpb);
+        if (ba + bb) lower_kernel<<<ba + bb, tpb, 0, st>>>(p, ba), launches++;
+    }
+    if (ev) cudaEventRecord(ev->lowered, st);
+
+    // K2 traversal.
+    if (p.tot.tiles) {
+        size_t smem;
+        int stages, threads, dev;
+        cudaGetDevice(&dev);
+        traversal_smem(p.tot, dev, &smem, &stages, &threads);
+        cudaFuncSetAttribute(traverse_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        traverse_kernel<<<(uint32_t)p.tot.tiles, threads, smem, st>>>(p, stages, p.tot.max_n, p.tot.max_layer_noise,
+                                                                    p.tot.max_layer_meas);
+        launches++;
+    }
+    if (ev) cudaEventRecord(ev->traversed, st);
+
+    // K3..K9 reduce.
+    const uint32_t tpb = 256;
+    uint4 *totals = p.bsum + p.bsum_cap - 4;  // 3 scan totals live at the end of bsum
+    if (S) dedup_kernel<<<blocks_for(S, tpb), tpb, 0, st>>>(p), launches++;
+    launch_scan(SrcScanF{p.rep, p.gcnt, p.ecnt, p.hdr}, S, p.bsum, p.sscan, &totals[0], st, &launches);
+    totals_kernel<<<1, 1, 0, st>>>(p, &totals[0]), launches++;
+    if (S) {
+        scatter_kernel<<<blocks_for(S, tpb), tpb, 0, st>>>(p), launches++;
+        finalize_kernel<<<blocks_for(S, tpb), tpb, 0, st>>>(p), launches++;
+    }
+    launch_scan(BucketScanF{p.bcount}, p.tot.buckets + 1, p.bsum, p.boff, &totals[1], st, &launches);
+    if (S) {
+        bucket_scatter_kernel<<<blocks_for(S, tpb), tpb, 0, st>>>(p), launches++;
+        rank_kernel<<<blocks_for(S, tpb), tpb, 0, st>>>(p), launches++;
+    }
+    launch_scan(PosScanF{p.perm, p.e_nd, p.e_no, p.hdr}, S, p.bsum, p.pscan, &totals[2], st, &launches);
+    gather_kernel<<<blocks_for(S + 1, tpb), tpb, 0, st>>>(p, &totals[2]), launches++;
+    if (ev) cudaEventRecord(ev->reduced, st);
+    *err = cudaGetLastError();
+    return launches;
+}
+
+}  // namespace gp

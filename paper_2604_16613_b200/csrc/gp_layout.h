@@ -1,0 +1,96 @@
+// gp_layout.h -- device data layout shared by the host packer (gp_api.cpp)
+// and the sm_100a kernels (gp_kernels.cu).
+//
+// A batch of C circuits is uploaded as ONE contiguous staging image (one H2D
+// copy) holding the arrays below back to back, each 16-byte aligned and
+// padded so that 16-byte-granular bulk copies (cp.async.bulk) may over-read
+// by up to 16 bytes. All per-element indices are global across the batch
+// unless marked "local".
+#pragma once
+#include <stdint.h>
+
+namespace gp {
+
+// Successor encoding of the base-slot STEPG ELLPACK (one u64 per base node,
+// lo = first successor, hi = second; the reference's packing, stepg.hpp:85-91).
+// Only the 2n base slots are materialised: every correlated slot of the
+// reference (Y, XZ, ZX, XY, YX, YY, YZ, ZY; stepg.cpp:236-254) is the XOR of
+// same-boundary base rows, so sources are expanded onto base rows instead
+// (bit-identical; pinned by test_eec.cpp:84-99 and by our oracle parity).
+constexpr uint32_t kSuccNone = 0xFFFFFFFFu;      // kNoSuccessor (stepg.hpp:52)
+constexpr uint32_t kSuccLeaf = 0x80000000u;      // | local measurement index
+constexpr uint64_t kEllIdle = 0;                 // whole word 0: idle qubit, X->X / Z->Z
+constexpr uint64_t kEllDead = 0xFFFFFFFFFFFFFFFFull;  // R / Z into M: no successor
+
+// Gate word: lo = q0 | kind << 29, hi = q1 (CX) or local measurement index.
+// Noise word: lo = q0 | kind << 30, hi = q1.
+constexpr uint32_t kGateKindShift = 29;
+constexpr uint32_t kNoiseKindShift = 30;
+
+struct CircuitMeta {
+    uint32_t n, l, M, D, O, W;
+    uint32_t layer_base;   // index of layer 0 in the layer arrays (l + 1 entries per circuit)
+    uint32_t meas_base;    // global index of local measurement 0
+    uint32_t det_base;     // index of detector 0 in det_off (D + 1 entries per circuit)
+    uint32_t obs_base;     // index of observable 0 in obs_off (O + 1 entries per circuit)
+    uint32_t tile_base;    // global tile (64-bit detector column word) index
+    uint32_t src_noise;    // noise-derived sources; M flip-source slots follow
+    uint32_t bucket_base;  // canonical-order buckets (D + 1 per circuit)
+    uint32_t max_layer_noise;  // max noise ops in one layer
+    uint64_t src_base;     // global id of source 0
+    uint64_t ell_base;     // ELLPACK index of (boundary 0, slot 0); (l - 1) * 2n entries
+    uint64_t leaf_base;    // leaf matrix index of (tile 0, meas 0); W * M entries, tile-major
+};
+
+// Offsets (bytes) of every array inside one staging image.
+struct StageLayout {
+    uint64_t meta;        // CircuitMeta[C]
+    uint64_t circ_layer;  // u32[C + 1] cumulative layer count (for warp -> circuit search)
+    uint64_t circ_src;    // u64[C + 1] cumulative sources
+    uint64_t circ_tile;   // u32[C + 1] cumulative tiles
+    uint64_t circ_det;    // u32[C + 1] cumulative detectors
+    uint64_t circ_obs;    // u32[C + 1] cumulative observables
+    uint64_t lay_gate;    // u32[sum(l + 1)] global gate index of each layer start
+    uint64_t lay_noise;   // u32[sum(l + 1)] global noise index
+    uint64_t lay_meas;    // u32[sum(l + 1)] local measurement index
+    uint64_t gates;       // u64[G]
+    uint64_t noise;       // u64[N]
+    uint64_t noise_prob;  // f64[N]
+    uint64_t noise_src;   // u32[N] local source offset of the op's first component
+    uint64_t meas_flip;   // f64[sum M]
+    uint64_t det_off;     // u32[sum(D + 1)] global index into det_meas
+    uint64_t det_meas;    // u32[] local measurement ids
+    uint64_t obs_off;     // u32[sum(O + 1)]
+    uint64_t obs_meas;    // u32[]
+    uint64_t total;       // bytes
+};
+
+struct BatchTotals {
+    uint32_t C;
+    uint32_t level;
+    uint64_t layers;      // sum l
+    uint64_t layer_slots; // sum (l + 1)
+    uint64_t gates, noise, meas;
+    uint64_t det_slots, det_entries, obs_slots, obs_entries;
+    uint64_t dets, obss;
+    uint64_t tiles;
+    uint64_t sources;
+    uint64_t ell;         // sum (l - 1) * 2n
+    uint64_t leaf;        // sum W * M
+    uint64_t buckets;     // sum (D + 1)
+    uint32_t max_n;       // max qubits
+    uint32_t max_layer_noise;
+    uint32_t max_layer_meas;
+};
+
+// Header written by the device at the end of a compile (read back first).
+struct DeviceHeader {
+    uint32_t num_edges;
+    uint32_t num_det_ids;
+    uint32_t num_obs_ids;
+    uint32_t num_members;
+    uint32_t record_overflow;  // max records seen for one source if > slots, else 0
+    uint32_t pad[3];
+};
+
+}  // namespace gp
