@@ -1,0 +1,278 @@
+"""GPU parity: the sm_100a path (through the C ABI) against the reference.
+
+Checks, in order of strength:
+* byte-identical serialize_dem text vs the reference's golden fixtures and
+  vs reference outputs committed under tests/golden/generated;
+* at BASELINE.json full sizes: sha256 of the serialized DEM == the sha256 of
+  the reference's own output on the same circuit (tests/golden/full_size.json);
+* vs the C restatement oracle on edge cases the reference tests exercise
+  (collisions, zero probabilities, empty / noiseless circuits, errors).
+Bit-exact comparison throughout: ids exact and fp64 probabilities equal.
+"""
+
+import hashlib
+import json
+import subprocess
+import threading
+
+import numpy as np
+import pytest
+
+import paper_2604_16613_b200 as gp
+from oracle.bindings import parse_dem_text
+
+from .conftest import FIXTURES, GOLDEN, ROOT, fixture_case
+
+pytestmark = pytest.mark.gpu
+
+FULL = json.loads((GOLDEN / "full_size.json").read_text())
+
+
+def sha(s: str) -> str:
+    return hashlib.sha256(s.encode()).hexdigest()
+
+
+@pytest.mark.parametrize("fx", FIXTURES, ids=lambda p: p.name)
+def test_fixture_byte_identical(compiler, fx):
+    circuit, level, text, golden = fixture_case(fx)
+    dem = compiler.compile(circuit, level)
+    assert dem.hyperedges() == golden
+    assert dem.to_text() == text
+
+
+@pytest.mark.parametrize("name", ["rep_d3_r2", "rep_d5_r3", "surface_d3_r3", "surface_d4_r2",
+                                  "surface_d5_r5_si1000", "surface_d5_r3_onlyz"])
+@pytest.mark.parametrize("level", [0, 1, 2])
+def test_generated_golden_byte_identical(compiler, name, level):
+    d = GOLDEN / "generated"
+    circuit = gp.parse_circuit((d / f"{name}.circuit.txt").read_text())
+    assert compiler.compile(circuit, level).to_text() == (d / f"{name}.L{level}.dem").read_text()
+
+
+FULL_MAKERS = {
+    "bb72_r2_uniform": lambda: gp.gen_bb(6, 6, rounds=2, p=1e-3),
+    "bb72_branch3_r4": lambda: gp.gen_bb72_branch(3, rounds=4),
+    "surface_d3_r3_paper": lambda: gp.gen_surface(3, 3, 1e-3),
+    "surface_d11_r11_si1000": lambda: gp.gen_surface(11, 11, 1e-3, gp.NOISE_MODEL_SI1000),
+    "bb144_r12_uniform": lambda: gp.gen_bb144(12, 1e-3),
+    "surface_d25_r25_paper": lambda: gp.gen_surface(25, 25, 1e-3),
+}
+FULL_CASES = [(n, int(lv)) for n in FULL_MAKERS for lv in FULL[n]["levels"]]
+
+
+@pytest.mark.parametrize("name,level", FULL_CASES, ids=[f"{n}-L{lv}" for n, lv in FULL_CASES])
+def test_full_size_matches_reference_hash(compiler, name, level):
+    g = FULL_MAKERS[name]()
+    assert sha(g.to_text()) == FULL[name]["circuit_sha256"], "generator drifted from the golden circuit"
+    dem = compiler.compile(g, level)
+    want = FULL[name]["levels"][str(level)]
+    assert dem.num_edges == want["edges"]
+    assert sha(dem.to_text()) == want["dem_sha256"]
+
+
+def test_branch_batch_matches_reference_hashes(compiler):
+    info = FULL["bb72_branches_r6_L0"]["branches"]
+    gens = [gp.gen_bb72_branch(b["branch"]) for b in info]
+    for g, b in zip(gens, info):
+        assert sha(g.to_text()) == b["circuit_sha256"]
+    dems = compiler.compile_batch(gens, 0)
+    for d, b in zip(dems, info):
+        assert d.num_edges == b["edges"]
+        assert sha(d.to_text()) == b["dem_sha256"]
+
+
+def test_batch_equals_single_compiles(compiler, port):
+    gens = [gp.gen_surface(3, 2, 1e-3), gp.gen_repetition(3, 2, 1e-3), gp.parse_circuit("H 0\nTICK\nM 0\n"),
+            gp.gen_bb(6, 6, rounds=1, p=2e-3), gp.parse_circuit("R 0\nX_ERROR(0.1) 0\nTICK\nM 0\nDETECTOR rec[-1]\n"),
+            gp.gen_surface(5, 2, 1e-3, gp.NOISE_MODEL_SI1000)]
+    for level in (0, 1, 2):
+        batch = compiler.compile_batch(gens, level)
+        for g, d in zip(gens, batch):
+            c = g.to_circuit() if hasattr(g, "to_circuit") else g
+            assert d.hyperedges() == port.compile(c, level)[0]
+            assert d.hyperedges() == compiler.compile(g, level).hyperedges()
+
+
+@pytest.mark.parametrize("level", [0, 1, 2])
+def test_small_generated_vs_oracle(compiler, port, level):
+    for g in (gp.gen_surface(7, 3, 1e-3), gp.gen_bb72_branch(21, rounds=4), gp.gen_repetition(9, 5, 3e-3),
+              gp.gen_surface(4, 4, 2e-3, gp.NOISE_MODEL_UNIFORM)):
+        assert compiler.compile(g, level).hyperedges() == port.compile(g.to_circuit(), level)[0]
+
+
+def test_forced_hash_collisions_never_merge(port):
+    """test_dem.cpp:94-101 via the context's collision hook: every signature
+    hashes to one key; grouping must still follow full comparison."""
+    comp = gp.Compiler(0)
+    comp.set_option(gp.OPT_FORCE_HASH_COLLISIONS, 1)
+    for g in (gp.gen_surface(3, 3, 1e-3), gp.gen_repetition(5, 2, 1e-3)):
+        for level in (0, 2):
+            assert comp.compile(g, level).hyperedges() == port.compile(g.to_circuit(), level)[0]
+
+
+def test_record_slot_overflow_recovers(port):
+    """One inline slot per source: multi-word signatures overflow, the
+    context grows its slots and re-runs; output unchanged."""
+    comp = gp.Compiler(0)
+    comp.set_option(gp.OPT_RECORD_SLOTS, 1)
+    g = gp.gen_surface(11, 3, 1e-3)
+    assert comp.compile(g, 2).hyperedges() == port.compile(g.to_circuit(), 2)[0]
+
+
+def test_zero_probability_sources_retained(compiler, port):
+    """test_stepg.cpp:78-83: X_ERROR(0) is a source; its edge has p = 0."""
+    c = gp.parse_circuit("R 0\nX_ERROR(0) 0\nTICK\nM 0\nDETECTOR rec[-1]\n")
+    got = compiler.compile(c, 0).hyperedges()
+    assert got == port.compile(c, 0)[0] == [((0,), (), 0.0)]
+
+
+def test_noiseless_and_empty_circuits(compiler):
+    assert compiler.compile(gp.gen_surface(3, 2, 0.0), 2).num_edges == 0
+    assert compiler.compile(gp.parse_circuit("H 0\n"), 0).num_edges == 0
+    assert compiler.compile(gp.parse_circuit("X_ERROR(0.1) 0\nTICK\nM 0\n"), 0).num_edges == 0
+
+
+def test_observable_only_edges_and_same_qubit_pairs(compiler, port):
+    text = ("R 0 1\nTICK\nDEPOLARIZE2(0.3) 0 0\nX_ERROR(0.2) 1\nTICK\nM(0.05) 0 1\n"
+            "OBSERVABLE_INCLUDE(0) rec[-1]\nOBSERVABLE_INCLUDE(1)\n")
+    c = gp.parse_circuit(text)
+    for level in (0, 1, 2):
+        assert compiler.compile(c, level).hyperedges() == port.compile(c, level)[0]
+
+
+def test_invalid_argument_messages(compiler):
+    """eec.cpp:44-46 / 52-54 and stepg.cpp:172-174, verbatim."""
+    c = gp.parse_circuit("M 0\nDETECTOR rec[-1]\nOBSERVABLE_INCLUDE(0) rec[-1]\n")
+    bad = gp.Circuit(**{**c.__dict__, "det_meas": np.array([7], np.uint32)})
+    with pytest.raises(ValueError, match="^detector references a measurement without a leaf$"):
+        compiler.compile(bad, 0)
+    bad = gp.Circuit(**{**c.__dict__, "obs_meas": np.array([7], np.uint32)})
+    with pytest.raises(ValueError, match="^observable references a measurement without a leaf$"):
+        compiler.compile(bad, 0)
+    huge = gp.Circuit(**{**c.__dict__, "num_qubits": 1 << 27,
+                         "gate_offsets": np.zeros(6, np.uint32), "noise_offsets": np.zeros(6, np.uint32),
+                         "gate_kind": np.zeros(0, np.uint8), "gate_q0": np.zeros(0, np.uint32),
+                         "gate_q1": np.zeros(0, np.uint32), "gate_meas": np.zeros(0, np.int32),
+                         "gate_flip": np.zeros(0), "num_measurements": 0,
+                         "det_offsets": np.zeros(1, np.uint32), "det_meas": np.zeros(0, np.uint32),
+                         "obs_offsets": np.zeros(1, np.uint32), "obs_meas": np.zeros(0, np.uint32)})
+    with pytest.raises(ValueError, match="^circuit exceeds 32-bit node index space$"):
+        compiler.compile(huge, 2)
+    # the context stays usable after an error
+    assert compiler.compile(gp.gen_surface(3, 2, 1e-3), 0).num_edges == 46
+
+
+def test_repeatable_and_schedule_independent(compiler):
+    """acceptance.cpp:182-201: 20 repeats byte-identical; `threads` is inert."""
+    g = gp.gen_surface(5, 2, 1e-3)
+    first = compiler.compile(g, 2).to_text()
+    for _ in range(20):
+        assert compiler.compile(g, 2).to_text() == first
+    assert gp.compile_circuit(g, 2, threads=32).to_text() == first
+
+
+def test_concurrent_host_threads(port):
+    """Reentrancy: one context per host thread."""
+    g = gp.gen_surface(5, 3, 1e-3)
+    want = port.compile(g.to_circuit(), 1)[0]
+    errs = []
+
+    def work():
+        try:
+            for _ in range(5):
+                assert gp.compile_circuit(g, 1).hyperedges() == want
+        except Exception as e:  # pragma: no cover
+            errs.append(e)
+
+    ts = [threading.Thread(target=work) for _ in range(4)]
+    [t.start() for t in ts]
+    [t.join() for t in ts]
+    assert not errs
+
+
+def test_stats_are_filled(compiler):
+    stats = {}
+    gp.compile_circuit(gp.gen_surface(5, 5, 1e-3), 2, stats=stats)
+    assert stats["total_ns"] > 0 and stats["kernel_ns"] > 0 and stats["num_sources"] > 0
+    assert stats["total_ns"] >= stats["kernel_ns"]
+
+
+CPP_MAIN = r"""
+#include <cstdio>
+#include <fstream>
+#include <iostream>
+#include <sstream>
+#include <stdexcept>
+#include "demc/compile.hpp"
+// Reads the flat dump written by the test and compiles it through the
+// drop-in demc::compile_circuit (libgreenpeas), printing serialize_dem.
+int main(int argc, char **argv) {
+    std::ifstream in(argv[1]);
+    int level = std::atoi(argv[2]);
+    demc::Circuit c;
+    std::string tag;
+    c.layers.emplace_back();
+    while (in >> tag) {
+        if (tag == "Q") in >> c.num_qubits >> c.num_measurements;
+        else if (tag == "L") c.layers.emplace_back();
+        else if (tag == "G") {
+            int k; demc::GateOp g{}; in >> k >> g.q0 >> g.q1 >> g.meas_index >> g.flip_prob;
+            g.kind = (demc::GateKind)k; c.layers.back().gates.push_back(g);
+        } else if (tag == "N") {
+            int k; demc::NoiseOp n{}; in >> k >> n.prob >> n.q0 >> n.q1;
+            n.kind = (demc::NoiseKind)k; c.layers.back().noise.push_back(n);
+        } else if (tag == "D" || tag == "O") {
+            size_t cnt; in >> cnt; std::vector<uint32_t> ms(cnt);
+            for (auto &m : ms) in >> m;
+            if (tag == "D") c.detectors.push_back({(uint32_t)c.detectors.size(), ms});
+            else c.observables.push_back({(uint32_t)c.observables.size(), ms});
+        }
+    }
+    c.layers.pop_back();
+    try {
+        demc::CompileStats st;
+        demc::Dem d = demc::compile_circuit(c, (demc::CorrelationLevel)level, 1, &st);
+        std::cout << demc::serialize_dem(d);
+        std::cerr << "total_ns=" << st.total_ns << "\n";
+    } catch (const std::invalid_argument &e) {
+        std::cout << "invalid_argument: " << e.what() << "\n";
+    }
+    return 0;
+}
+"""
+
+
+def dump_flat(c, path):
+    lines = [f"Q {c.num_qubits} {c.num_measurements}"]
+    for i in range(c.num_layers):
+        for g in range(c.gate_offsets[i], c.gate_offsets[i + 1]):
+            lines.append(f"G {c.gate_kind[g]} {c.gate_q0[g]} {c.gate_q1[g]} {c.gate_meas[g]} {float(c.gate_flip[g])!r}")
+        for o in range(c.noise_offsets[i], c.noise_offsets[i + 1]):
+            lines.append(f"N {c.noise_kind[o]} {float(c.noise_prob[o])!r} {c.noise_q0[o]} {c.noise_q1[o]}")
+        lines.append("L")
+    for ms in c.detectors():
+        lines.append("D " + " ".join(map(str, [len(ms), *ms])))
+    for ms in c.observables():
+        lines.append("O " + " ".join(map(str, [len(ms), *ms])))
+    path.write_text("\n".join(lines) + "\n")
+
+
+def test_cpp_dropin_shim(tmp_path):
+    """A C++ caller of the reference API links libgreenpeas unchanged."""
+    from paper_2604_16613_b200._native import LIB_PATH
+    src = tmp_path / "main.cpp"
+    src.write_text(CPP_MAIN)
+    exe = tmp_path / "dropin"
+    subprocess.run(["g++", "-std=c++20", "-O1", f"-I{ROOT / 'include'}", str(src), str(LIB_PATH),
+                    f"-Wl,-rpath,{LIB_PATH.parent}", "-o", str(exe)], check=True)
+    for fx in FIXTURES:
+        circuit, level, text, _ = fixture_case(fx)
+        dump_flat(circuit, tmp_path / "c.txt")
+        out = subprocess.run([str(exe), str(tmp_path / "c.txt"), str(level)], capture_output=True, text=True,
+                             check=True)
+        assert out.stdout == text, fx.name
+    circuit, _, _, _ = fixture_case(FIXTURES[0])
+    bad = gp.Circuit(**{**circuit.__dict__, "det_meas": circuit.det_meas + 1000})
+    dump_flat(bad, tmp_path / "bad.txt")
+    out = subprocess.run([str(exe), str(tmp_path / "bad.txt"), "0"], capture_output=True, text=True, check=True)
+    assert out.stdout == "invalid_argument: detector references a measurement without a leaf\n"
