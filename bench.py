@@ -1,0 +1,357 @@
+"""Benchmark of the B200 DEM compile path (driver contract: one JSON line).
+
+Workload (default, config 5 of BASELINE.json): adaptive-branch circuits of the
+BB [[72,12,6]] code, 6 rounds, compiled at L0. Each rank owns its own
+--branches circuits (branch ids rank*B .. rank*B+B-1, weak scaling); a step
+compiles the rank's whole batch. No collective on the data path.
+
+  value  hyperedges/s with inputs resident in HBM: the device pipeline replayed
+         K times on the uploaded batch (gp_replay), CUDA-event timed, max over
+         ranks. The batch image is larger than L2 (noted in config).
+  e2e    the same metric through the public batch API (gp_compile_batch): host
+         circuits -> pinned staging -> H2D -> kernels -> D2H of the flat DEM,
+         every step; wall-timed around a barrier + synchronize.
+
+--impl reference times the reference CPU compiler (oracle/_ref, built from the
+reference sources) on the box's host cores with a std::thread pool (the
+demc_main.cpp:184-195 pattern) on a bounded sample of the same workload.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "hyperedges/sec and p50 DEM compile latency (ms) at 1/2/4/8 B200 vs CPU ref"
+UNIT = "hyperedges/s"
+L2_BYTES = 126 * 2**20
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+class Dist:
+    def __init__(self, gpus: int, backend: str):
+        self.ws, self.rank, self.local = dist_env()
+        self.pg = None
+        if self.ws > 1:
+            import torch
+            import torch.distributed as td
+            if backend == "nccl":
+                torch.cuda.set_device(self.local)
+            td.init_process_group(backend=backend)
+            self.td, self.torch = td, torch
+            self.pg = True
+        self.backend = backend
+
+    def barrier(self):
+        if self.pg:
+            if self.backend == "nccl":
+                self.td.barrier(device_ids=[self.local])
+            else:
+                self.td.barrier()
+
+    def max(self, x: float) -> float:
+        if not self.pg:
+            return x
+        dev = f"cuda:{self.local}" if self.backend == "nccl" else "cpu"
+        t = self.torch.tensor([float(x)], dtype=self.torch.float64, device=dev)
+        self.td.all_reduce(t, op=self.td.ReduceOp.MAX)
+        return float(t.item())
+
+    def sum(self, x: float) -> float:
+        if not self.pg:
+            return x
+        dev = f"cuda:{self.local}" if self.backend == "nccl" else "cpu"
+        t = self.torch.tensor([float(x)], dtype=self.torch.float64, device=dev)
+        self.td.all_reduce(t, op=self.td.ReduceOp.SUM)
+        return float(t.item())
+
+    def close(self):
+        if self.pg:
+            self.td.destroy_process_group()
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md)."""
+
+    def __init__(self, index: int):
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--id={index}", f"--query-gpu={q}",
+                                       "--format=csv,noheader,nounits", "-lms", "200"], stdout=self.f,
+                                      stderr=subprocess.DEVNULL)
+        except FileNotFoundError:
+            self.p = None
+
+    def stop(self) -> dict:
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.p.terminate()
+        self.p.wait()
+        rows = [r.split(",") for r in Path(self.f.name).read_text().splitlines() if r.count(",") >= 8]
+        os.unlink(self.f.name)
+        sm = [float(r[1]) for r in rows if r[1].strip().replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].strip().replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i].strip() == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+def build_branches(first: int, count: int):
+    import paper_2604_16613_b200 as gp
+    return [gp.gen_bb72_branch(first + b) for b in range(count)]
+
+
+def views_of(circuits):
+    from paper_2604_16613_b200 import _native as N
+    arr = (N.CircuitView * len(circuits))()
+    for i, c in enumerate(circuits):
+        arr[i] = c.view()[0]
+    return arr
+
+
+def reference_pool(circuits_text: list[str], level: int, threads: int):
+    """Reference compile_circuit on a thread pool; returns (edges, wall_s)."""
+    from oracle.bindings import RefLib
+    ref = RefLib()
+    handles = [ref.parse(t) for t in circuits_text]
+    edges, ns = ref.compile_pool(handles, level, threads)
+    return edges, ns / 1e9
+
+
+def cpu_info():
+    model = "unknown"
+    try:
+        for line in Path("/proc/cpuinfo").read_text().splitlines():
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return model, os.cpu_count() or 1
+
+
+def run_reference(args, dist):
+    """--impl reference: rank 0 times the reference CPU compiler."""
+    if dist.rank != 0:
+        return
+    import paper_2604_16613_b200 as gp  # generators only (host), no GPU use
+    threads = os.cpu_count() or 1
+    sample = args.ref_sample
+    texts = [gp.gen_bb72_branch(b).to_text() for b in range(sample)]
+    times, edges = [], 0
+    for i in range(args.warmup + args.steps):
+        e, wall = reference_pool(texts, args.level, threads)
+        if i >= args.warmup:
+            times.append(wall)
+            edges = e
+    wall = statistics.mean(times)
+    value = edges / wall
+    model, ncpu = cpu_info()
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "impl": "reference", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": wall * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "u64+f64", "data": "synthetic",
+        "config": {"workload": "bb72_adaptive_branches_r6_L0", "branches_per_step": sample, "level": args.level,
+                   "note": "bounded sample of the GPU arm's workload (same generator, branch ids 0..sample-1)"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
+                         "sample": f"{sample} BB72 r6 branch circuits per step, std::thread pool of {threads}",
+                         "cpu": model},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def single_circuit_block(compiler, ref_ok: bool, quick: bool):
+    """N=1 extras: p50 compile latency of single circuits (SURVEY 8d configs
+    1-4) through gp_compile (host circuit -> flat DEM in pinned memory), with
+    the reference CPU compiler's p50 on the same circuit."""
+    import paper_2604_16613_b200 as gp
+    cases = [("surface_d3_r3_paper", lambda: gp.gen_surface(3, 3, 1e-3), (0, 2)),
+             ("surface_d11_r11_si1000", lambda: gp.gen_surface(11, 11, 1e-3, gp.NOISE_MODEL_SI1000), (0, 2)),
+             ("bb144_r12_uniform", lambda: gp.gen_bb144(12, 1e-3), (0, 2)),
+             ("surface_d25_r25_paper", lambda: gp.gen_surface(25, 25, 1e-3), (0,))]
+    out = {}
+    ref = None
+    if ref_ok:
+        from oracle.bindings import RefLib
+        ref = RefLib()
+    for name, make, levels in cases:
+        g = make()
+        text = g.to_text() if ref else None
+        for lv in levels:
+            iters = 30 if "d25" in name else 200
+            for _ in range(5):
+                dem = compiler.compile(g, lv)
+            ts, ks = [], []
+            for _ in range(iters):
+                dem = compiler.compile(g, lv)
+                ts.append(compiler.last_stats["total_ns"])
+                ks.append(compiler.last_stats["kernel_ns"])
+            ts.sort()
+            p50 = ts[len(ts) // 2] / 1e6
+            entry = {"edges": dem.num_edges, "p50_ms": p50, "p99_ms": ts[int(len(ts) * 0.99) - 1] / 1e6,
+                     "kernel_p50_ms": sorted(ks)[len(ks) // 2] / 1e6, "hyperedges_per_s": dem.num_edges / (p50 / 1e3)}
+            if ref is not None and not (quick and "d25" in name):
+                riters = 1 if "d25" in name else (5 if "bb144" in name or "d11" in name else 20)
+                e, ns = ref.parse(text).time_compile(lv, riters)
+                rp50 = float(sorted(ns)[len(ns) // 2]) / 1e6
+                entry["ref_p50_ms"] = rp50
+                entry["ref_hyperedges_per_s"] = e / (rp50 / 1e3)
+                entry["speedup_p50"] = rp50 / p50
+            out[f"{name}_L{lv}"] = entry
+    return out
+
+
+def run_gpu(args, dist):
+    import paper_2604_16613_b200 as gp
+
+    ws, rank = dist.ws, dist.rank
+    device = dist.local if ws > 1 else 0
+    compiler = gp.Compiler(device)
+    B = args.branches
+    t_gen = time.time()
+    circuits = build_branches(rank * B, B)
+    views = views_of(circuits)
+    gen_s = time.time() - t_gen
+
+    # Warm-up through the public API (allocations, first-touch of pinned arenas).
+    for _ in range(args.warmup):
+        out, stats = compiler.compile_batch_raw(views, args.level)
+    edges = int(out.num_edges)
+    h2d = int(stats["h2d_bytes"])
+    d2h = int(stats["d2h_bytes"])
+    image_bytes = h2d
+
+    # --- value: device-resident replay, CUDA events, max over ranks ---------
+    flush = image_bytes < 2 * L2_BYTES
+    clocks = Clocks(device)  # sampled across both timed regions
+    time.sleep(1.5)  # nvidia-smi start-up
+    compiler.replay(args.warmup, flush)
+    dist.barrier()
+    rep = compiler.replay(args.steps, flush)
+    dist.barrier()
+    prof = compiler.profile_stages()
+    dev_s = dist.max(rep["kernel_ns"] / 1e9)
+    total_edges = dist.sum(edges)
+    value = total_edges * args.steps / dev_s
+    ms_per_step = dev_s / args.steps * 1e3
+    launches_per_step = int(rep["kernel_launches"])
+
+    # --- e2e: public batch API, host in / host out, every step ---------------
+    dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        out, stats = compiler.compile_batch_raw(views, args.level)
+    t1 = time.perf_counter()
+    dist.barrier()
+    clk = clocks.stop()
+    e2e_s = dist.max(t1 - t0)
+    e2e_value = total_edges * args.steps / e2e_s
+
+    # --- roofline of the dominant kernel ------------------------------------
+    from paper_2604_16613_b200 import _native as N
+    E = int(out.num_edges)
+    eoff = N.copy_u64(out.edge_offsets, len(circuits) + 1)
+    doff = N.copy_u64(out.det_offsets, E + 1)
+    ooff = N.copy_u64(out.obs_offsets, E + 1)
+    ab = {"traverse": 0, "reduce": 0, "total": 0}
+    for i, c in enumerate(circuits):  # B_alg is per circuit; sum over the batch
+        e0, e1 = int(eoff[i]), int(eoff[i + 1])
+        ids = int(doff[e1] - doff[e0] + ooff[e1] - ooff[e0])
+        for k, v in gp.algorithmic_bytes(gp.circuit_metrics(c, args.level), e1 - e0, ids).items():
+            ab[k] += v
+    stages = {k: v / args.steps for k, v in prof.items()}
+    dominant = max(stages, key=stages.get)
+    peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
+    peak = float(peaks.get("hbm_gbs", 6650.0))
+    peak_src = "measured" if "hbm_gbs" in peaks else "fallback"
+    part = "traverse" if dominant == "traverse" else "reduce"
+    dom_ns = stages[dominant]
+    achieved = ab[part] / dom_ns if dom_ns else 0.0  # bytes/ns == GB/s
+    roofline = {"bound": "hbm", "kernel": dominant, "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak, "traffic": None, "peak_source": peak_src,
+                "alg_bytes_per_launch": ab[part], "bytes_per_hyperedge": ab["total"] / max(E, 1),
+                "stage_ms": {k: v / 1e6 for k, v in stages.items()},
+                "pipeline_alg_gbs": ab["total"] / (rep["kernel_ns"] / args.steps)}
+    if args.ncu_traffic is not None:
+        roofline["traffic"] = args.ncu_traffic
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "u64+f64", "data": "synthetic",
+        "config": {"workload": "bb72_adaptive_branches_r6_L0", "branches_per_gpu": B, "total_branches": B * ws,
+                   "level": args.level, "hyperedges_per_step": int(total_edges),
+                   "parallelism": f"branch-sharded x{ws}, no collective",
+                   "l2": "inputs larger than L2" if not flush else "L2 flushed between timed iterations",
+                   "input_image_bytes_per_gpu": image_bytes, "generate_s": round(gen_s, 2)},
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                "ms_per_step": e2e_s / args.steps * 1e3},
+        "gpu_launches": launches_per_step * args.steps,
+        "roofline": roofline,
+        "clocks": clk,
+    }
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        model, ncpu = cpu_info()
+        sample = args.cpu_sample
+        texts = [circuits[b].to_text() for b in range(min(sample, B))]
+        threads = ncpu
+        e, wall = reference_pool(texts, args.level, threads)
+        line["cpu_baseline"] = {"value": e / wall, "unit": UNIT, "cores": threads, "kind": "reference",
+                                "sample": f"{len(texts)} of the {B} branch circuits, reference compile_circuit "
+                                          f"on a {threads}-thread pool ({wall:.2f} s wall)", "cpu": model}
+    if rank == 0 and ws == 1 and not args.no_single:
+        line["single_circuit"] = single_circuit_block(compiler, ref_ok=not args.no_cpu_baseline, quick=args.quick)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="greenpeas", choices=["greenpeas", "reference"])
+    ap.add_argument("--branches", type=int, default=4096, help="branch circuits per GPU")
+    ap.add_argument("--level", type=int, default=0)
+    ap.add_argument("--cpu-sample", type=int, default=1024)
+    ap.add_argument("--ref-sample", type=int, default=512)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-single", action="store_true")
+    ap.add_argument("--quick", action="store_true")
+    ap.add_argument("--ncu-traffic", type=float, default=None)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    ws, _, _ = dist_env()
+    dist = Dist(args.gpus, "nccl" if args.impl == "greenpeas" else "gloo") if ws > 1 else Dist(1, "none")
+    try:
+        if args.impl == "reference":
+            run_reference(args, dist)
+        else:
+            run_gpu(args, dist)
+    finally:
+        dist.close()
+
+
+if __name__ == "__main__":
+    main()

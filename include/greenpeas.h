@@ -150,6 +150,31 @@ gp_status gp_compile(gp_ctx *ctx, const gp_circuit_view *circuit, uint8_t level,
 gp_status gp_compile_batch(gp_ctx *ctx, const gp_circuit_view *circuits, size_t count,
                            uint8_t level, gp_dem_batch_view *out, gp_stats *stats);
 
+/* Benchmark hooks (not part of the reference API). gp_replay re-runs the
+ * device pipeline `iterations` times on the batch uploaded by the last
+ * successful compile on this context: inputs already resident in HBM, outputs
+ * left in HBM. flush_l2 != 0 overwrites a 256 MiB scratch buffer before each
+ * iteration, outside the timed region. stats->kernel_ns receives the summed
+ * device time (CUDA events around each pipeline), traverse_kernel_ns the
+ * summed traversal-kernel time, kernel_launches the launches per pipeline. */
+gp_status gp_replay(gp_ctx *ctx, uint32_t iterations, int flush_l2, gp_stats *stats);
+/* Per-stage device time (ns, summed over the last gp_replay) and stage
+ * names; returns the number of stages written (<= cap). */
+int gp_profile_stages(gp_ctx *ctx, uint64_t *ns, const char **names, int cap);
+
+/* Roofline accounting inputs of one circuit: N = l * 2n base
+ * nodes, N_e = non-sentinel successor references among them, C = base/leaf
+ * rows over all source expansions, S = sources (reference count), W, M. */
+typedef struct gp_metrics {
+    uint64_t base_nodes;
+    uint64_t succ_refs;
+    uint64_t source_rows;
+    uint64_t sources;
+    uint64_t words;
+    uint64_t measurements;
+} gp_metrics;
+gp_status gp_circuit_metrics(const gp_circuit_view *circuit, uint8_t level, gp_metrics *out);
+
 /* serialize_dem (dem.cpp:144-157): `error(<shortest round-trip>) D.. L..\n`.
  * Returns a malloc'd NUL-terminated string; release with gp_free. */
 char *gp_serialize_dem(const gp_dem_view *dem, size_t *len);

@@ -17,6 +17,8 @@ from .api import (  # noqa: F401
     Dem,
     GenCircuit,
     GreenpeasError,
+    algorithmic_bytes,
+    circuit_metrics,
     compile_circuit,
     gen_bb,
     gen_bb72_branch,

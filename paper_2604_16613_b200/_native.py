@@ -50,6 +50,11 @@ class DemBatchView(C.Structure):
     ]
 
 
+class Metrics(C.Structure):
+    _fields_ = [(n, C.c_uint64) for n in ("base_nodes", "succ_refs", "source_rows", "sources", "words",
+                                          "measurements")]
+
+
 class Stats(C.Structure):
     _fields_ = [(n, C.c_uint64) for n in (
         "lower_ns", "traverse_ns", "reduce_ns", "total_ns", "h2d_ns", "kernel_ns", "d2h_ns",
@@ -78,6 +83,9 @@ def lib() -> C.CDLL:
         L.gp_compile.argtypes = [vp, C.POINTER(CircuitView), C.c_uint8, C.POINTER(DemView), C.POINTER(Stats)]
         L.gp_compile_batch.argtypes = [vp, C.POINTER(CircuitView), C.c_size_t, C.c_uint8,
                                        C.POINTER(DemBatchView), C.POINTER(Stats)]
+        L.gp_replay.argtypes = [vp, C.c_uint32, C.c_int, C.POINTER(Stats)]
+        L.gp_profile_stages.argtypes = [vp, C.POINTER(C.c_uint64), C.POINTER(C.c_char_p), C.c_int]
+        L.gp_circuit_metrics.argtypes = [C.POINTER(CircuitView), C.c_uint8, C.POINTER(Metrics)]
         L.gp_serialize_dem.argtypes = [C.POINTER(DemView), C.POINTER(C.c_size_t)]
         L.gp_serialize_dem.restype = vp
         L.gp_free.argtypes = [vp]

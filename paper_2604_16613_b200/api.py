@@ -130,6 +130,19 @@ class Compiler:
         self.last_stats = st.as_dict()
         return _dem_from_view(out, 0, int(out.num_edges), out.num_detectors, out.num_observables)
 
+    def replay(self, iterations: int = 1, flush_l2: bool = False) -> dict:
+        """Re-runs the device pipeline on the last uploaded batch (inputs and
+        outputs resident in HBM); returns summed device times in ns."""
+        st = N.Stats()
+        self._check(self._lib.gp_replay(self._ctx, iterations, int(flush_l2), C.byref(st)))
+        return st.as_dict()
+
+    def profile_stages(self) -> dict:
+        ns = (C.c_uint64 * 32)()
+        names = (C.c_char_p * 32)()
+        n = self._lib.gp_profile_stages(self._ctx, ns, names, 32)
+        return {names[i].decode(): int(ns[i]) for i in range(n)}
+
     def compile_batch_raw(self, views, level=CorrelationLevel.L0):
         """Batch compile of prepared CircuitView array; returns (DemBatchView, stats)."""
         out = N.DemBatchView()
@@ -237,6 +250,24 @@ class GenCircuit:
             N.lib().gp_circuit_free(self._h)
         except Exception:
             pass
+
+
+def circuit_metrics(circuit, level) -> dict:
+    """SURVEY.md 8d inputs of the algorithmic-bytes formula for one circuit."""
+    v, keep = circuit.view() if hasattr(circuit, "view") else N.view_of(circuit)
+    m = N.Metrics()
+    N.lib().gp_circuit_metrics(C.byref(v), int(level), C.byref(m))
+    return {n: int(getattr(m, n)) for n, _ in m._fields_}
+
+
+def algorithmic_bytes(metrics: dict, edges: int, ids: int) -> dict:
+    """B_alg = 8N + 8W(N + M + N_e + C) + 8S + E(8 + 4 w), split
+    into the traversal part (dense Alg. 1 + leaf init + signature gather) and
+    the reduce part (probabilities in, compact DEM out); E*4*w = 4*ids."""
+    N_, W, M = metrics["base_nodes"], metrics["words"], metrics["measurements"]
+    trav = 8 * N_ + 8 * W * (N_ + M + metrics["succ_refs"] + metrics["source_rows"])
+    red = 8 * metrics["sources"] + 8 * edges + 4 * ids
+    return {"traverse": trav, "reduce": red, "total": trav + red}
 
 
 def gen_repetition(d: int, rounds: int, p: float) -> GenCircuit:

@@ -49,6 +49,13 @@ struct gp_ctx {
 
     std::vector<CircuitMeta> metas;
     std::vector<uint32_t> out_ndet, out_nobs;
+
+    // Last successful device plan (for gp_replay) and profiling state.
+    bool has_plan = false;
+    DevPlan last_plan{};
+    cudaEvent_t prof[gp::kProfCount] = {};
+    uint64_t prof_ns[gp::kProfCount] = {};
+    uint8_t *d_flush = nullptr;
 };
 
 namespace {
@@ -416,7 +423,7 @@ gp_status run_batch(gp_ctx *ctx, const gp_circuit_view *cs, size_t count, uint8_
         const size_t need = carve(ctx, p, t, nullptr, K, ids_cap);
         if ((st = ensure_device(ctx, &ctx->d_ws, &ctx->d_ws_cap, need)) != GP_OK) return st;
         carve(ctx, p, t, ctx->d_ws, K, ids_cap);
-        launches += gp::enqueue_pipeline(p, ctx->stream, &ctx->stage_ev, &e);
+        launches += gp::enqueue_pipeline(p, ctx->stream, &ctx->stage_ev, nullptr, &e);
         if (e != cudaSuccess) return cuda_fail(ctx, e, "kernel launch");
         e = cudaMemcpyAsync(ctx->h_hdr, p.hdr, sizeof(DeviceHeader), cudaMemcpyDeviceToHost, ctx->stream);
         if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
@@ -437,6 +444,8 @@ gp_status run_batch(gp_ctx *ctx, const gp_circuit_view *cs, size_t count, uint8_
         }
         break;
     }
+    ctx->last_plan = p;
+    ctx->has_plan = true;
     const uint64_t E = hdr.num_edges, nd = hdr.num_det_ids, no = hdr.num_obs_ids;
     size_t o = 0;
     auto take = [&](size_t bytes) {
@@ -528,6 +537,9 @@ void gp_ctx_destroy(gp_ctx *ctx) {
     if (ctx->h_hdr) cudaFreeHost(ctx->h_hdr);
     if (ctx->d_img) cudaFree(ctx->d_img);
     if (ctx->d_ws) cudaFree(ctx->d_ws);
+    if (ctx->d_flush) cudaFree(ctx->d_flush);
+    for (cudaEvent_t ev : ctx->prof)
+        if (ev) cudaEventDestroy(ev);
     for (cudaEvent_t ev : {ctx->ev_start, ctx->ev_h2d, ctx->ev_end, ctx->stage_ev.lowered, ctx->stage_ev.traversed,
                            ctx->stage_ev.reduced})
         if (ev) cudaEventDestroy(ev);
@@ -593,6 +605,96 @@ gp_status gp_compile_batch(gp_ctx *ctx, const gp_circuit_view *circuits, size_t 
     out->obs_offsets = ho.obs_off;
     out->obs_ids = ho.obs_ids;
     out->probs = ho.probs;
+    return GP_OK;
+}
+
+gp_status gp_replay(gp_ctx *ctx, uint32_t iterations, int flush_l2, gp_stats *stats) {
+    if (!ctx->has_plan) return fail(ctx, GP_ERR_INVALID_ARGUMENT, "gp_replay needs a previous successful compile");
+    cudaSetDevice(ctx->device);
+    constexpr size_t kFlush = 256ull << 20;  // > 126 MB L2
+    if (flush_l2 && !ctx->d_flush && cudaMalloc(&ctx->d_flush, kFlush) != cudaSuccess) {
+        cudaGetLastError();
+        return fail(ctx, GP_ERR_OUT_OF_MEMORY, "flush buffer");
+    }
+    for (cudaEvent_t &ev : ctx->prof)
+        if (!ev) cudaEventCreate(&ev);
+    std::fill(std::begin(ctx->prof_ns), std::end(ctx->prof_ns), 0);
+    uint64_t total = 0, trav = 0;
+    int launches = 0;
+    for (uint32_t it = 0; it < iterations; it++) {
+        if (flush_l2) cudaMemsetAsync(ctx->d_flush, it & 0xFF, kFlush, ctx->stream);
+        cudaError_t e;
+        launches = gp::enqueue_pipeline(ctx->last_plan, ctx->stream, nullptr, ctx->prof, &e);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+        if (e != cudaSuccess) return cuda_fail(ctx, e, "replay");
+        for (int k = 1; k < gp::kProfCount; k++)
+            ctx->prof_ns[k] += (uint64_t)(elapsed_ms(ctx->prof[k - 1], ctx->prof[k]) * 1e6);
+        total += (uint64_t)(elapsed_ms(ctx->prof[0], ctx->prof[gp::kProfCount - 1]) * 1e6);
+        trav += (uint64_t)(elapsed_ms(ctx->prof[gp::kProfLower], ctx->prof[gp::kProfTraverse]) * 1e6);
+    }
+    if (stats) {
+        *stats = gp_stats{};
+        stats->kernel_ns = total;
+        stats->traverse_kernel_ns = trav;
+        stats->traverse_ns = trav;
+        stats->kernel_launches = (uint64_t)launches;
+        stats->num_sources = ctx->last_plan.tot.sources;
+    }
+    return GP_OK;
+}
+
+int gp_profile_stages(gp_ctx *ctx, uint64_t *ns, const char **names, int cap) {
+    int n = 0;
+    for (int k = 1; k < gp::kProfCount && n < cap; k++, n++) {
+        if (ns) ns[n] = ctx->prof_ns[k];
+        if (names) names[n] = gp::kProfNames[k];
+    }
+    return n;
+}
+
+gp_status gp_circuit_metrics(const gp_circuit_view *v, uint8_t level, gp_metrics *out) {
+    *out = gp_metrics{};
+    const uint32_t n = v->num_qubits, l = v->num_layers;
+    out->base_nodes = (uint64_t)l * 2 * n;
+    out->words = ((uint64_t)v->num_detectors + v->num_observables + 63) / 64;
+    out->measurements = v->num_measurements;
+    std::vector<uint8_t> refs(n);
+    for (uint32_t i = 1; i < l; i++) {  // layer i shapes boundary i - 1
+        std::fill(refs.begin(), refs.end(), 2);  // idle: X -> X, Z -> Z
+        for (uint32_t g = v->gate_offsets[i]; g < v->gate_offsets[i + 1]; g++) {
+            const uint32_t q = v->gate_q0[g];
+            switch (v->gate_kind[g]) {
+                case GP_GATE_CX:
+                    refs[q] = 3;
+                    refs[v->gate_q1[g]] = 3;
+                    break;
+                case GP_GATE_R:
+                    refs[q] = 0;
+                    break;
+                case GP_GATE_MR:
+                    refs[q] = 1;
+                    break;
+                default:  // H: 2, M: leaf + X
+                    refs[q] = 2;
+            }
+        }
+        for (uint32_t q = 0; q < n; q++) out->succ_refs += refs[q];
+    }
+    static const uint8_t kDep2[15] = {4, 8, 1, 5, 2, 10, 12, 9, 3, 6, 13, 7, 15, 11, 14};
+    for (uint32_t o = 0; o < v->noise_offsets[l]; o++) {
+        const uint8_t k = v->noise_kind[o];
+        const uint32_t nc = components(k, level);
+        out->sources += nc;
+        if (k <= GP_NOISE_Z_ERROR) out->source_rows += 1;
+        else if (k == GP_NOISE_DEPOLARIZE1) out->source_rows += nc == 2 ? 2 : 4;
+        else
+            for (uint32_t c = 0; c < nc; c++) out->source_rows += (uint64_t)__builtin_popcount(kDep2[c]);
+    }
+    for (uint32_t g = 0; g < v->gate_offsets[l]; g++)
+        if ((v->gate_kind[g] == GP_GATE_M || v->gate_kind[g] == GP_GATE_MR) && v->gate_flip[g] > 0) {
+            out->sources++;
+            out->source_rows++;
+        }
     return GP_OK;
 }
 

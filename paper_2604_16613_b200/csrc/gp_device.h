@@ -63,11 +63,33 @@ struct StageEvents {
     cudaEvent_t lowered, traversed, reduced;
 };
 
+// Per-stage profile points (event recorded after each stage) for live
+// per-kernel timing inside bench.py; stage names in kProfNames.
+enum ProfStage {
+    kProfStart = 0,
+    kProfMemset,
+    kProfLower,
+    kProfTraverse,
+    kProfDedup,
+    kProfScanSrc,
+    kProfScatter,
+    kProfFinalize,
+    kProfScanBucket,
+    kProfBucketScatter,
+    kProfRank,
+    kProfScanPos,
+    kProfGather,
+    kProfCount
+};
+constexpr const char *kProfNames[kProfCount] = {"start",   "memset",     "lower",          "traverse", "dedup",
+                                                "scan_src", "scatter",   "finalize",       "scan_bucket",
+                                                "bucket_scatter", "rank", "scan_pos",      "gather"};
+
 // Enqueues the whole device pipeline on `stream`: lowering, traversal,
 // reduce, canonical order, output gather. Returns the number of kernel
 // launches (memsets included). `events` may be null.
 int enqueue_pipeline(const DevPlan &p, cudaStream_t stream, const StageEvents *events,
-                     cudaError_t *err);
+                     const cudaEvent_t *prof, cudaError_t *err);
 
 // Dynamic shared memory the traversal kernel needs for a batch, and the
 // number of staging buffers it will use; returns false if a circuit is too

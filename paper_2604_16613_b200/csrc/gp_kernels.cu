@@ -69,12 +69,10 @@ __device__ __forceinline__ const T *arr(const DevPlan &p, uint64_t off) {
     return reinterpret_cast<const T *>(p.img + off);
 }
 
-// Components of each noise op as 4-bit masks (bit0 X on q0, bit1 Z on q0,
-// bit2 X on q1, bit3 Z on q1); a level keeps a prefix of each table.
+// Components of each noise op (traverse_kernel) as 4-bit masks (bit0 X on
+// q0, bit1 Z on q0, bit2 X on q1, bit3 Z on q1); a level keeps a prefix.
 // DEPOLARIZE2 (kPairTable, stepg.cpp:49-58): L0 IX IZ XI XX ZI ZZ, L1 adds
 // IY XZ YI ZX, L2 adds XY YX YY YZ ZY. DEPOLARIZE1 (stepg.cpp:75-83): X Z, then Y.
-__constant__ uint8_t kDep2Mask[15] = {4, 8, 1, 5, 2, 10, 12, 9, 3, 6, 13, 7, 15, 11, 14};
-__constant__ uint8_t kDep1Mask[3] = {1, 2, 3};
 
 __host__ __device__ __forceinline__ uint32_t noise_components(uint32_t kind, uint32_t level) {
     if (kind <= 1) return 1;
@@ -268,14 +266,18 @@ struct TravDims {
     __device__ uint64_t *bars(uint8_t *base) const { return reinterpret_cast<uint64_t *>(stage(base, stages)); }
 };
 
-__device__ __forceinline__ void emit(const DevPlan &p, uint64_t src, uint32_t tile, uint64_t bits) {
-    const uint32_t j = atomicAdd(&p.cnt[src], 1u);
+__device__ __forceinline__ void put_record(const DevPlan &p, uint64_t src, uint32_t j, uint32_t tile,
+                                           uint64_t bits) {
     if (j < p.K) {
         p.rbits[src * p.K + j] = bits;
         p.rtile[src * p.K + j] = tile;
     } else {
         atomicMax(&p.hdr->record_overflow, j + 1);
     }
+}
+
+__device__ __forceinline__ void emit(const DevPlan &p, uint64_t src, uint32_t tile, uint64_t bits) {
+    put_record(p, src, atomicAdd(&p.cnt[src], 1u), tile, bits);
 }
 
 __global__ void __launch_bounds__(1024) traverse_kernel(DevPlan p, uint32_t stages, uint32_t max_n,
@@ -450,22 +452,36 @@ __global__ void __launch_bounds__(1024) traverse_kernel(DevPlan p, uint32_t stag
                     const uint64_t v = kind == 0 ? x0 : z0;
                     if (v) emit(p, src, t, v);
                 } else if (kind == 2) {
-                    const uint32_t nc = level == 0 ? 2 : 3;
-                    for (uint32_t c = 0; c < nc; c++) {
-                        const uint32_t mk = kDep1Mask[c];
-                        const uint64_t v = ((mk & 1) ? x0 : 0) ^ ((mk & 2) ? z0 : 0);
-                        if (v) emit(p, src + c, t, v);
-                    }
+                    if ((x0 | z0) == 0) continue;
+                    // X, Z (+ Y at L1+): all slot claims in flight before any store
+                    const uint64_t v[3] = {x0, z0, level ? x0 ^ z0 : 0};
+                    uint32_t slot[3];
+#pragma unroll
+                    for (int c = 0; c < 3; c++)
+                        if (v[c]) slot[c] = atomicAdd(&p.cnt[src + c], 1u);
+#pragma unroll
+                    for (int c = 0; c < 3; c++)
+                        if (v[c]) put_record(p, src + c, slot[c], t, v[c]);
                 } else {
                     const uint64_t x1 = now[2 * q1], z1 = now[2 * q1 + 1];
                     if ((x0 | z0 | x1 | z1) == 0) continue;
                     const uint32_t nc = level == 0 ? 6 : level == 1 ? 10 : 15;
-                    for (uint32_t c = 0; c < nc; c++) {
-                        const uint32_t mk = kDep2Mask[c];
-                        const uint64_t v = ((mk & 1) ? x0 : 0) ^ ((mk & 2) ? z0 : 0) ^ ((mk & 4) ? x1 : 0) ^
-                                           ((mk & 8) ? z1 : 0);
-                        if (v) emit(p, src + c, t, v);
+                    constexpr uint8_t kMask[15] = {4, 8, 1, 5, 2, 10, 12, 9, 3, 6, 13, 7, 15, 11, 14};
+                    uint64_t v[15];
+                    uint32_t slot[15];
+#pragma unroll
+                    for (int c = 0; c < 15; c++) {
+                        const uint32_t mk = kMask[c];
+                        v[c] = (uint32_t)c < nc ? ((mk & 1) ? x0 : 0) ^ ((mk & 2) ? z0 : 0) ^ ((mk & 4) ? x1 : 0) ^
+                                                      ((mk & 8) ? z1 : 0)
+                                                : 0;
                     }
+#pragma unroll
+                    for (int c = 0; c < 15; c++)
+                        if (v[c]) slot[c] = atomicAdd(&p.cnt[src + c], 1u);
+#pragma unroll
+                    for (int c = 0; c < 15; c++)
+                        if (v[c]) put_record(p, src + c, slot[c], t, v[c]);
                 }
             }
         }
@@ -858,7 +874,6 @@ void launch_scan(F f, uint64_t n, uint4 *bsum, uint4 *out, uint4 *total, cudaStr
     const uint32_t nb = (uint32_t)((n + kScanTile - 1) / kScanTile);
     if (nb == 0) {
         cudaMemsetAsync(total, 0, sizeof(uint4), st);
-        (*launches)++;
         return;
     }
     scan_reduce_kernel<<<nb, kScanThreads, 0, st>>>(f, n, bsum);
@@ -884,17 +899,23 @@ bool traversal_smem(const BatchTotals &t, int device, size_t *bytes, int *stages
     return *bytes <= budget;
 }
 
-int enqueue_pipeline(const DevPlan &p, cudaStream_t st, const StageEvents *ev, cudaError_t *err) {
+int enqueue_pipeline(const DevPlan &p, cudaStream_t st, const StageEvents *ev, const cudaEvent_t *prof,
+                     cudaError_t *err) {
     int launches = 0;
+    auto mark = [&](int k) {
+        if (prof) cudaEventRecord(prof[k], st);
+    };
+    mark(kProfStart);
     const uint64_t S = p.tot.sources;
     // Zero / sentinel fills.
-    if (p.tot.ell) cudaMemsetAsync(p.ell, 0, p.tot.ell * 8, st), launches++;
-    if (p.tot.leaf) cudaMemsetAsync(p.leaf, 0, p.tot.leaf * 8, st), launches++;
-    cudaMemsetAsync(p.cnt, 0, S * 4 + 4, st), launches++;
-    cudaMemsetAsync(p.gcnt, 0, S * 4 + 4, st), launches++;
-    cudaMemsetAsync(p.table, 0xFF, (p.table_mask + 1) * 8, st), launches++;
-    cudaMemsetAsync(p.bcount, 0, p.tot.buckets * 4 + 4, st), launches++;
-    cudaMemsetAsync(p.hdr, 0, sizeof(DeviceHeader), st), launches++;
+    if (p.tot.ell) cudaMemsetAsync(p.ell, 0, p.tot.ell * 8, st);
+    if (p.tot.leaf) cudaMemsetAsync(p.leaf, 0, p.tot.leaf * 8, st);
+    cudaMemsetAsync(p.cnt, 0, S * 4 + 4, st);
+    cudaMemsetAsync(p.gcnt, 0, S * 4 + 4, st);
+    cudaMemsetAsync(p.table, 0xFF, (p.table_mask + 1) * 8, st);
+    cudaMemsetAsync(p.bcount, 0, p.tot.buckets * 4 + 4, st);
+    cudaMemsetAsync(p.hdr, 0, sizeof(DeviceHeader), st);
+    mark(kProfMemset);
 
     // K1 lowering.
     {
@@ -903,6 +924,7 @@ int enqueue_pipeline(const DevPlan &p, cudaStream_t st, const StageEvents *ev, c
         const uint32_t bb = blocks_for(p.tot.dets + p.tot.obss, tpb);
         if (ba + bb) lower_kernel<<<ba + bb, tpb, 0, st>>>(p, ba), launches++;
     }
+    mark(kProfLower);
     if (ev) cudaEventRecord(ev->lowered, st);
 
     // K2 traversal.
@@ -916,25 +938,31 @@ int enqueue_pipeline(const DevPlan &p, cudaStream_t st, const StageEvents *ev, c
                                                                     p.tot.max_layer_meas);
         launches++;
     }
+    mark(kProfTraverse);
     if (ev) cudaEventRecord(ev->traversed, st);
 
     // K3..K9 reduce.
     const uint32_t tpb = 256;
     uint4 *totals = p.bsum + p.bsum_cap - 4;  // 3 scan totals live at the end of bsum
     if (S) dedup_kernel<<<blocks_for(S, tpb), tpb, 0, st>>>(p), launches++;
+    mark(kProfDedup);
     launch_scan(SrcScanF{p.rep, p.gcnt, p.ecnt, p.hdr}, S, p.bsum, p.sscan, &totals[0], st, &launches);
     totals_kernel<<<1, 1, 0, st>>>(p, &totals[0]), launches++;
-    if (S) {
-        scatter_kernel<<<blocks_for(S, tpb), tpb, 0, st>>>(p), launches++;
-        finalize_kernel<<<blocks_for(S, tpb), tpb, 0, st>>>(p), launches++;
-    }
+    mark(kProfScanSrc);
+    if (S) scatter_kernel<<<blocks_for(S, tpb), tpb, 0, st>>>(p), launches++;
+    mark(kProfScatter);
+    if (S) finalize_kernel<<<blocks_for(S, tpb), tpb, 0, st>>>(p), launches++;
+    mark(kProfFinalize);
     launch_scan(BucketScanF{p.bcount}, p.tot.buckets + 1, p.bsum, p.boff, &totals[1], st, &launches);
-    if (S) {
-        bucket_scatter_kernel<<<blocks_for(S, tpb), tpb, 0, st>>>(p), launches++;
-        rank_kernel<<<blocks_for(S, tpb), tpb, 0, st>>>(p), launches++;
-    }
+    mark(kProfScanBucket);
+    if (S) bucket_scatter_kernel<<<blocks_for(S, tpb), tpb, 0, st>>>(p), launches++;
+    mark(kProfBucketScatter);
+    if (S) rank_kernel<<<blocks_for(S, tpb), tpb, 0, st>>>(p), launches++;
+    mark(kProfRank);
     launch_scan(PosScanF{p.perm, p.e_nd, p.e_no, p.hdr}, S, p.bsum, p.pscan, &totals[2], st, &launches);
+    mark(kProfScanPos);
     gather_kernel<<<blocks_for(S + 1, tpb), tpb, 0, st>>>(p, &totals[2]), launches++;
+    mark(kProfGather);
     if (ev) cudaEventRecord(ev->reduced, st);
     *err = cudaGetLastError();
     return launches;
