@@ -260,8 +260,12 @@ def run_gpu(args, dist):
     # --- e2e: public batch API, host in / host out, every step ---------------
     dist.barrier()
     t0 = time.perf_counter()
+    e2e_parts = {"pack_upload_lower_ms": 0.0, "kernels_ms": 0.0, "download_ms": 0.0}
     for _ in range(args.steps):
         out, stats = compiler.compile_batch_raw(views, args.level)
+        e2e_parts["pack_upload_lower_ms"] += stats["lower_ns"] / 1e6 / args.steps
+        e2e_parts["kernels_ms"] += stats["kernel_ns"] / 1e6 / args.steps
+        e2e_parts["download_ms"] += stats["d2h_ns"] / 1e6 / args.steps
     t1 = time.perf_counter()
     dist.barrier()
     clk = clocks.stop()
@@ -306,7 +310,7 @@ def run_gpu(args, dist):
                    "l2": "inputs larger than L2" if not flush else "L2 flushed between timed iterations",
                    "input_image_bytes_per_gpu": image_bytes, "generate_s": round(gen_s, 2)},
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                "ms_per_step": e2e_s / args.steps * 1e3},
+                "ms_per_step": e2e_s / args.steps * 1e3, "breakdown": e2e_parts},
         "gpu_launches": launches_per_step * args.steps,
         "roofline": roofline,
         "clocks": clk,

@@ -9,6 +9,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
+#include <thread>
 #include <charconv>
 #include <chrono>
 #include <cstdlib>
@@ -31,8 +33,10 @@ struct gp_ctx {
     cudaStream_t stream = nullptr;
     std::string err;
     int force_collisions = 0;
-    uint32_t record_slots = 4;
+    uint32_t trav_debug = 0;
+    uint32_t record_slots = 8;
     uint64_t ids_hint = 0;  // learned id capacity (grows on overflow)
+    uint64_t pool_hint = 0; // learned record-pool chunks (grows on overflow)
 
     uint8_t *h_stage = nullptr;
     size_t h_stage_cap = 0;
@@ -85,30 +89,95 @@ uint32_t components(uint8_t kind, uint8_t level) {  // stepg.cpp:66-103
     return level == 0 ? 6 : level == 1 ? 10 : 15;
 }
 
-// Pass 1: validation (the reference's exceptions, in the reference's order),
-// device-encoding limits, totals and per-circuit metadata.
+// Runs f(i) for i in [0, n) on up to hardware_concurrency host threads
+// (inline for small n: single-circuit latency pays no thread start-up).
+template <class F>
+void parallel_for(size_t n, F f) {
+    const size_t hw = std::max<unsigned>(1, std::thread::hardware_concurrency());
+    const size_t nt = std::min(hw, n / 32);
+    if (nt <= 1) {
+        for (size_t i = 0; i < n; i++) f(i);
+        return;
+    }
+    std::atomic<size_t> next{0};
+    auto work = [&] {
+        for (size_t i0; (i0 = next.fetch_add(16)) < n;)
+            for (size_t i = i0; i < std::min(n, i0 + 16); i++) f(i);
+    };
+    std::vector<std::thread> pool;
+    for (size_t t = 1; t < nt; t++) pool.emplace_back(work);
+    work();
+    for (auto &th : pool) th.join();
+}
+
+// Per-circuit counts of pass 1 (independent across circuits).
+struct CircCount {
+    int err;  // 0 ok, 1 index space, 2 detector leaf, 3 observable leaf, 4 too wide
+    uint32_t src_noise, max_noise, max_meas;
+    uint64_t gates, noise, det_entries, obs_entries;
+};
+
+// Pass 1: validation (the reference's exceptions, in the reference's order;
+// for a batch, the first failing circuit), device-encoding limits, totals and
+// per-circuit metadata. Counting runs in parallel over circuits.
 gp_status plan_batch(gp_ctx *ctx, const gp_circuit_view *cs, size_t C, uint8_t level, BatchTotals &t,
                      std::vector<CircuitMeta> &metas) {
     t = BatchTotals{};
     t.C = (uint32_t)C;
     t.level = level;
     metas.assign(C, CircuitMeta{});
-    for (size_t c = 0; c < C; c++) {
+    std::vector<CircCount> cc(C);
+    parallel_for(C, [&](size_t c) {
         const gp_circuit_view &v = cs[c];
-        CircuitMeta &m = metas[c];
+        CircCount &k = cc[c];
+        k = CircCount{};
         const uint64_t rows = (uint64_t)v.num_layers * alpha_of(level) * v.num_qubits + v.num_measurements;
-        if (rows >= 0xFFFFFFFFull)  // lower(), stepg.cpp:171-174
-            return fail(ctx, GP_ERR_INVALID_ARGUMENT, "circuit exceeds 32-bit node index space");
+        if (rows >= 0xFFFFFFFFull) {  // lower(), stepg.cpp:171-174
+            k.err = 1;
+            return;
+        }
         for (uint32_t d = 0; d < v.num_detectors; d++)  // init_leaves, eec.cpp:42-49
-            for (uint32_t k = v.det_offsets[d]; k < v.det_offsets[d + 1]; k++)
-                if (v.det_meas[k] >= v.num_measurements)
-                    return fail(ctx, GP_ERR_INVALID_ARGUMENT, "detector references a measurement without a leaf");
+            for (uint32_t x = v.det_offsets[d]; x < v.det_offsets[d + 1]; x++)
+                if (v.det_meas[x] >= v.num_measurements) {
+                    k.err = 2;
+                    return;
+                }
         for (uint32_t o = 0; o < v.num_observables; o++)  // eec.cpp:50-57
-            for (uint32_t k = v.obs_offsets[o]; k < v.obs_offsets[o + 1]; k++)
-                if (v.obs_meas[k] >= v.num_measurements)
-                    return fail(ctx, GP_ERR_INVALID_ARGUMENT, "observable references a measurement without a leaf");
-        if (v.num_qubits >= (1u << 29) || v.num_measurements >= 0x7FFFFFFFu)
-            return fail(ctx, GP_ERR_UNSUPPORTED, "circuit too wide for the device encoding");
+            for (uint32_t x = v.obs_offsets[o]; x < v.obs_offsets[o + 1]; x++)
+                if (v.obs_meas[x] >= v.num_measurements) {
+                    k.err = 3;
+                    return;
+                }
+        if (v.num_qubits >= (1u << 29) || v.num_measurements >= 0x7FFFFFFFu) {
+            k.err = 4;
+            return;
+        }
+        uint64_t src = 0;
+        for (uint32_t i = 0; i < v.num_layers; i++) {
+            const uint32_t n0 = v.noise_offsets[i], n1 = v.noise_offsets[i + 1];
+            k.max_noise = std::max(k.max_noise, n1 - n0);
+            for (uint32_t o = n0; o < n1; o++) src += components(v.noise_kind[o], level);
+            uint32_t meas = 0;
+            for (uint32_t g = v.gate_offsets[i]; g < v.gate_offsets[i + 1]; g++)
+                meas += v.gate_kind[g] == GP_GATE_M || v.gate_kind[g] == GP_GATE_MR;
+            k.max_meas = std::max(k.max_meas, meas);
+        }
+        k.src_noise = (uint32_t)src;
+        k.gates = v.gate_offsets[v.num_layers] - v.gate_offsets[0];
+        k.noise = v.noise_offsets[v.num_layers] - v.noise_offsets[0];
+        k.det_entries = v.det_offsets[v.num_detectors] - v.det_offsets[0];
+        k.obs_entries = v.obs_offsets[v.num_observables] - v.obs_offsets[0];
+    });
+    static const char *kErr[] = {"", "circuit exceeds 32-bit node index space",
+                                 "detector references a measurement without a leaf",
+                                 "observable references a measurement without a leaf",
+                                 "circuit too wide for the device encoding"};
+    for (size_t c = 0; c < C; c++)
+        if (cc[c].err) return fail(ctx, cc[c].err == 4 ? GP_ERR_UNSUPPORTED : GP_ERR_INVALID_ARGUMENT, kErr[cc[c].err]);
+    for (size_t c = 0; c < C; c++) {  // prefix sums (serial, O(C))
+        const gp_circuit_view &v = cs[c];
+        const CircCount &k = cc[c];
+        CircuitMeta &m = metas[c];
         m.n = v.num_qubits;
         m.l = v.num_layers;
         m.M = v.num_measurements;
@@ -124,34 +193,31 @@ gp_status plan_batch(gp_ctx *ctx, const gp_circuit_view *cs, size_t C, uint8_t l
         m.src_base = t.sources;
         m.ell_base = t.ell;
         m.leaf_base = t.leaf;
-        uint64_t src = 0;
-        uint32_t maxn = 0;
-        for (uint32_t i = 0; i < m.l; i++) {
-            const uint32_t n0 = v.noise_offsets[i], n1 = v.noise_offsets[i + 1];
-            maxn = std::max(maxn, n1 - n0);
-            for (uint32_t o = n0; o < n1; o++) src += components(v.noise_kind[o], level);
-            uint32_t meas = 0;
-            for (uint32_t g = v.gate_offsets[i]; g < v.gate_offsets[i + 1]; g++)
-                meas += v.gate_kind[g] == GP_GATE_M || v.gate_kind[g] == GP_GATE_MR;
-            t.max_layer_meas = std::max(t.max_layer_meas, meas);
-        }
-        m.src_noise = (uint32_t)src;
-        m.max_layer_noise = maxn;
-        t.max_layer_noise = std::max(t.max_layer_noise, maxn);
+        m.src_noise = k.src_noise;
+        m.max_layer_noise = k.max_noise;
+        m.gate_base = t.gates;
+        m.noise_base = t.noise;
+        m.det_entry_base = t.det_entries;
+        m.obs_entry_base = t.obs_entries;
+        m.circ_layer_base = t.layers;
+        t.max_layer_noise = std::max(t.max_layer_noise, k.max_noise);
+        t.max_layer_meas = std::max(t.max_layer_meas, k.max_meas);
         t.max_n = std::max(t.max_n, m.n);
+        t.max_W = std::max(t.max_W, m.W);
+        t.max_l = std::max(t.max_l, m.l);
         t.layers += m.l;
         t.layer_slots += m.l + 1;
-        t.gates += v.gate_offsets[m.l];
-        t.noise += v.noise_offsets[m.l];
+        t.gates += k.gates;
+        t.noise += k.noise;
         t.meas += m.M;
         t.det_slots += m.D + 1;
-        t.det_entries += v.det_offsets[m.D];
+        t.det_entries += k.det_entries;
         t.obs_slots += m.O + 1;
-        t.obs_entries += v.obs_offsets[m.O];
+        t.obs_entries += k.obs_entries;
         t.dets += m.D;
         t.obss += m.O;
         t.tiles += m.W;
-        t.sources += src + m.M;
+        t.sources += k.src_noise + m.M;
         t.ell += m.l ? (uint64_t)(m.l - 1) * 2 * m.n : 0;
         t.leaf += (uint64_t)m.W * m.M;
         t.buckets += (uint64_t)m.D + 1;
@@ -174,6 +240,7 @@ StageLayout stage_layout(const BatchTotals &t) {
     L.circ_layer = put((t.C + 1) * 4);
     L.circ_src = put((t.C + 1) * 8);
     L.circ_tile = put((t.C + 1) * 4);
+    L.circ_grp = put((t.C + 1) * 4);
     L.circ_det = put((t.C + 1) * 4);
     L.circ_obs = put((t.C + 1) * 4);
     L.lay_gate = put(t.layer_slots * 4);
@@ -192,16 +259,44 @@ StageLayout stage_layout(const BatchTotals &t) {
     return L;
 }
 
-// Pass 2: write the staging image.
-void pack_batch(const gp_circuit_view *cs, const BatchTotals &t, const std::vector<CircuitMeta> &metas,
-                const StageLayout &L, uint8_t *img) {
+// Pass 2: write the staging image, in parallel over circuits (each circuit's
+// slices of every array are disjoint and located by its prefix bases).
+// Cumulative per-circuit tables (O(C), serial).
+void pack_tables(const BatchTotals &t, const std::vector<CircuitMeta> &metas, const StageLayout &L, uint32_t T,
+                 uint8_t *img) {
     auto at = [&](uint64_t off) { return img + off; };
     std::memcpy(at(L.meta), metas.data(), t.C * sizeof(CircuitMeta));
     auto *circ_layer = (uint32_t *)at(L.circ_layer);
     auto *circ_src = (uint64_t *)at(L.circ_src);
     auto *circ_tile = (uint32_t *)at(L.circ_tile);
+    auto *circ_grp = (uint32_t *)at(L.circ_grp);
     auto *circ_det = (uint32_t *)at(L.circ_det);
     auto *circ_obs = (uint32_t *)at(L.circ_obs);
+    uint64_t grps = 0, dets = 0, obss = 0;
+    for (uint32_t c = 0; c < t.C; c++) {  // O(C) cumulative tables
+        const CircuitMeta &m = metas[c];
+        circ_layer[c] = (uint32_t)m.circ_layer_base;
+        circ_src[c] = m.src_base;
+        circ_tile[c] = m.tile_base;
+        circ_grp[c] = (uint32_t)grps;
+        circ_det[c] = (uint32_t)dets;
+        circ_obs[c] = (uint32_t)obss;
+        grps += (m.W + T - 1) / T;
+        dets += m.D;
+        obss += m.O;
+    }
+    circ_layer[t.C] = (uint32_t)t.layers;
+    circ_src[t.C] = t.sources;
+    circ_tile[t.C] = (uint32_t)t.tiles;
+    circ_grp[t.C] = (uint32_t)grps;
+    circ_det[t.C] = (uint32_t)dets;
+    circ_obs[t.C] = (uint32_t)obss;
+}
+
+// Per-circuit slices of every section for circuits [c0, c1), in parallel.
+void pack_circuits(const gp_circuit_view *cs, const BatchTotals &t, const std::vector<CircuitMeta> &metas,
+                   const StageLayout &L, uint8_t *img, size_t c0, size_t c1) {
+    auto at = [&](uint64_t off) { return img + off; };
     auto *lay_gate = (uint32_t *)at(L.lay_gate);
     auto *lay_noise = (uint32_t *)at(L.lay_noise);
     auto *lay_meas = (uint32_t *)at(L.lay_meas);
@@ -214,23 +309,16 @@ void pack_batch(const gp_circuit_view *cs, const BatchTotals &t, const std::vect
     auto *det_meas = (uint32_t *)at(L.det_meas);
     auto *obs_off = (uint32_t *)at(L.obs_off);
     auto *obs_meas = (uint32_t *)at(L.obs_meas);
-    uint64_t g_at = 0, n_at = 0, de_at = 0, oe_at = 0, layers = 0, tiles = 0, dets = 0, obss = 0;
-    for (uint32_t c = 0; c < t.C; c++) {
+    parallel_for(c1 - c0, [&](size_t ci) {
+        const size_t c = c0 + ci;
         const gp_circuit_view &v = cs[c];
         const CircuitMeta &m = metas[c];
-        circ_layer[c] = (uint32_t)layers;
-        circ_src[c] = m.src_base;
-        circ_tile[c] = (uint32_t)tiles;
-        circ_det[c] = (uint32_t)dets;
-        circ_obs[c] = (uint32_t)obss;
-        layers += m.l;
-        tiles += m.W;
-        dets += m.D;
-        obss += m.O;
+        const uint64_t g_at = m.gate_base, n_at = m.noise_base;
+        const uint32_t g0 = v.gate_offsets[0], n0 = v.noise_offsets[0];
         uint32_t src = 0, meas = 0;
         for (uint32_t i = 0; i <= m.l; i++) {
-            lay_gate[m.layer_base + i] = (uint32_t)(g_at + (i < m.l ? v.gate_offsets[i] - v.gate_offsets[0] : v.gate_offsets[m.l] - v.gate_offsets[0]));
-            lay_noise[m.layer_base + i] = (uint32_t)(n_at + v.noise_offsets[i] - v.noise_offsets[0]);
+            lay_gate[m.layer_base + i] = (uint32_t)(g_at + v.gate_offsets[i] - g0);
+            lay_noise[m.layer_base + i] = (uint32_t)(n_at + v.noise_offsets[i] - n0);
             lay_meas[m.layer_base + i] = meas;
             if (i == m.l) break;
             for (uint32_t g = v.gate_offsets[i]; g < v.gate_offsets[i + 1]; g++) {
@@ -242,12 +330,11 @@ void pack_batch(const gp_circuit_view *cs, const BatchTotals &t, const std::vect
                     flip[m.meas_base + hi] = v.gate_flip[g];
                     meas++;
                 }
-                gates[g_at + g - v.gate_offsets[0]] =
-                    (uint64_t)hi << 32 | (v.gate_q0[g] | (uint32_t)k << gp::kGateKindShift);
+                gates[g_at + g - g0] = (uint64_t)hi << 32 | (v.gate_q0[g] | (uint32_t)k << gp::kGateKindShift);
             }
             for (uint32_t o = v.noise_offsets[i]; o < v.noise_offsets[i + 1]; o++) {
                 const uint8_t k = v.noise_kind[o];
-                const uint64_t idx = n_at + o - v.noise_offsets[0];
+                const uint64_t idx = n_at + o - n0;
                 noise[idx] = (uint64_t)(k == GP_NOISE_DEPOLARIZE2 ? v.noise_q1[o] : 0) << 32 |
                              (v.noise_q0[o] | (uint32_t)k << gp::kNoiseKindShift);
                 nprob[idx] = v.noise_prob[o];
@@ -255,22 +342,16 @@ void pack_batch(const gp_circuit_view *cs, const BatchTotals &t, const std::vect
                 src += components(k, (uint8_t)t.level);
             }
         }
-        g_at += v.gate_offsets[m.l] - v.gate_offsets[0];
-        n_at += v.noise_offsets[m.l] - v.noise_offsets[0];
-        for (uint32_t d = 0; d <= m.D; d++) det_off[m.det_base + d] = (uint32_t)(de_at + v.det_offsets[d] - v.det_offsets[0]);
+        const uint64_t de_at = m.det_entry_base, oe_at = m.obs_entry_base;
+        for (uint32_t d = 0; d <= m.D; d++)
+            det_off[m.det_base + d] = (uint32_t)(de_at + v.det_offsets[d] - v.det_offsets[0]);
         const uint32_t nde = v.det_offsets[m.D] - v.det_offsets[0];
         if (nde) std::memcpy(det_meas + de_at, v.det_meas + v.det_offsets[0], nde * 4);
-        de_at += nde;
-        for (uint32_t o = 0; o <= m.O; o++) obs_off[m.obs_base + o] = (uint32_t)(oe_at + v.obs_offsets[o] - v.obs_offsets[0]);
+        for (uint32_t o = 0; o <= m.O; o++)
+            obs_off[m.obs_base + o] = (uint32_t)(oe_at + v.obs_offsets[o] - v.obs_offsets[0]);
         const uint32_t noe = v.obs_offsets[m.O] - v.obs_offsets[0];
         if (noe) std::memcpy(obs_meas + oe_at, v.obs_meas + v.obs_offsets[0], noe * 4);
-        oe_at += noe;
-    }
-    circ_layer[t.C] = (uint32_t)layers;
-    circ_src[t.C] = t.sources;
-    circ_tile[t.C] = (uint32_t)tiles;
-    circ_det[t.C] = (uint32_t)dets;
-    circ_obs[t.C] = (uint32_t)obss;
+    });
 }
 
 // Device workspace carve-up for a batch (capacity-checked, grown on demand).
@@ -283,7 +364,8 @@ struct WsPlan {
     };
 };
 
-size_t carve(gp_ctx *ctx, DevPlan &p, const BatchTotals &t, uint8_t *base, uint32_t K, uint64_t ids_cap) {
+size_t carve(gp_ctx *ctx, DevPlan &p, const BatchTotals &t, uint8_t *base, uint32_t K, uint64_t ids_cap,
+             uint64_t pool_chunks) {
     const uint64_t S = t.sources;
     uint64_t cap = 1024;
     while (cap < S + S / 2 + 16) cap <<= 1;
@@ -301,6 +383,8 @@ size_t carve(gp_ctx *ctx, DevPlan &p, const BatchTotals &t, uint8_t *base, uint3
     p.rbits = (uint64_t *)take(S * K * 8);
     p.rtile = (uint32_t *)take(S * K * 4);
     p.K = K;
+    p.pool = (uint4 *)take(pool_chunks * gp::kPoolChunk * 16);
+    p.pool_chunks_cap = (uint32_t)pool_chunks;
     p.rep = (uint32_t *)take(S * 4);
     p.gcnt = (uint32_t *)take(S * 4 + 4);
     p.ecnt = (uint2 *)take(S * 8);
@@ -395,24 +479,61 @@ gp_status run_batch(gp_ctx *ctx, const gp_circuit_view *cs, size_t count, uint8_
     BatchTotals t;
     gp_status st = plan_batch(ctx, cs, count, level, t, ctx->metas);
     if (st != GP_OK) return st;
-    size_t smem;
-    int stages, threads;
-    if (!gp::traversal_smem(t, ctx->device, &smem, &stages, &threads))
+    gp::TravCfg tcfg;
+    size_t tsmem;
+    if (!gp::plan_traversal(t, ctx->device, &tcfg, &tsmem))
         return fail(ctx, GP_ERR_UNSUPPORTED, "circuit too wide for on-chip traversal state (2n words)");
+    t.groups = 0;
+    for (const CircuitMeta &m : ctx->metas) t.groups += (m.W + tcfg.T - 1) / tcfg.T;
     const StageLayout L = stage_layout(t);
     if ((st = ensure_host(ctx, &ctx->h_stage, &ctx->h_stage_cap, L.total)) != GP_OK) return st;
-    pack_batch(cs, t, ctx->metas, L, ctx->h_stage);
-    const uint64_t pack_ns = ns_since(t0);
     if ((st = ensure_device(ctx, &ctx->d_img, &ctx->d_img_cap, L.total)) != GP_OK) return st;
 
-    cudaError_t e;
+    // Pack in circuit chunks; each chunk's slice of every section is copied
+    // while the next chunk is packed (the image is circuit-major per section).
+    cudaError_t e = cudaSuccess;
     cudaEventRecord(ctx->ev_start, ctx->stream);
-    e = cudaMemcpyAsync(ctx->d_img, ctx->h_stage, L.total, cudaMemcpyHostToDevice, ctx->stream);
+    const std::vector<CircuitMeta> &M = ctx->metas;
+    const size_t nchunk = count >= 1024 ? 8 : count >= 256 ? 4 : 1;
+    auto slice = [&](uint64_t off, uint64_t elem, uint64_t lo, uint64_t hi) {
+        if (hi > lo && e == cudaSuccess)
+            e = cudaMemcpyAsync(ctx->d_img + off + lo * elem, ctx->h_stage + off + lo * elem, (hi - lo) * elem,
+                                cudaMemcpyHostToDevice, ctx->stream);
+    };
+    for (size_t k = 0; k < nchunk; k++) {
+        const size_t c0 = count * k / nchunk, c1 = count * (k + 1) / nchunk;
+        if (c1 == c0) continue;
+        pack_circuits(cs, t, M, L, ctx->h_stage, c0, c1);
+        const CircuitMeta &a = M[c0];
+        const bool last = c1 == count;
+        const CircuitMeta *b = last ? nullptr : &M[c1];
+        slice(L.lay_gate, 4, a.layer_base, last ? t.layer_slots : b->layer_base);
+        slice(L.lay_noise, 4, a.layer_base, last ? t.layer_slots : b->layer_base);
+        slice(L.lay_meas, 4, a.layer_base, last ? t.layer_slots : b->layer_base);
+        slice(L.gates, 8, a.gate_base, last ? t.gates : b->gate_base);
+        slice(L.noise, 8, a.noise_base, last ? t.noise : b->noise_base);
+        slice(L.noise_prob, 8, a.noise_base, last ? t.noise : b->noise_base);
+        slice(L.noise_src, 4, a.noise_base, last ? t.noise : b->noise_base);
+        slice(L.meas_flip, 8, a.meas_base, last ? t.meas : b->meas_base);
+        slice(L.det_off, 4, a.det_base, last ? t.det_slots : b->det_base);
+        slice(L.det_meas, 4, a.det_entry_base, last ? t.det_entries : b->det_entry_base);
+        slice(L.obs_off, 4, a.obs_base, last ? t.obs_slots : b->obs_base);
+        slice(L.obs_meas, 4, a.obs_entry_base, last ? t.obs_entries : b->obs_entry_base);
+    }
+    pack_tables(t, M, L, tcfg.T, ctx->h_stage);
+    slice(0, 1, 0, L.lay_gate);  // meta + cumulative tables (the image's head)
+    const uint64_t pack_ns = ns_since(t0);
     if (e != cudaSuccess) return cuda_fail(ctx, e, "upload");
     cudaEventRecord(ctx->ev_h2d, ctx->stream);
 
-    uint32_t K = ctx->record_slots;
-    uint64_t ids_cap = std::max<uint64_t>(ctx->ids_hint, 2 * t.sources + 1024);
+    // One CTA owning all T words of a source writes at most T records.
+    uint32_t K = tcfg.direct ? std::max<uint32_t>(ctx->record_slots, tcfg.T) : ctx->record_slots;
+    // Multi-CTA circuits (one word per CTA) emit through the record pool.
+    uint64_t pool = 0;
+    if (!tcfg.direct)
+        pool = std::max<uint64_t>(ctx->pool_hint,
+                                  (2 * t.sources) / gp::kPoolChunk + t.groups * tcfg.emit_warps + 16);
+    uint64_t ids_cap = std::max<uint64_t>(ctx->ids_hint, 3 * t.sources + 1024);
     DevPlan p{};
     int launches = 0;
     for (int attempt = 0;; attempt++) {
@@ -420,9 +541,12 @@ gp_status run_batch(gp_ctx *ctx, const gp_circuit_view *cs, size_t count, uint8_
         p.img = ctx->d_img;
         p.lay = L;
         p.tot = t;
-        const size_t need = carve(ctx, p, t, nullptr, K, ids_cap);
+        p.trav = tcfg;
+        p.trav.debug = ctx->trav_debug;
+        p.trav_smem = tsmem;
+        const size_t need = carve(ctx, p, t, nullptr, K, ids_cap, pool);
         if ((st = ensure_device(ctx, &ctx->d_ws, &ctx->d_ws_cap, need)) != GP_OK) return st;
-        carve(ctx, p, t, ctx->d_ws, K, ids_cap);
+        carve(ctx, p, t, ctx->d_ws, K, ids_cap, pool);
         launches += gp::enqueue_pipeline(p, ctx->stream, &ctx->stage_ev, nullptr, &e);
         if (e != cudaSuccess) return cuda_fail(ctx, e, "kernel launch");
         e = cudaMemcpyAsync(ctx->h_hdr, p.hdr, sizeof(DeviceHeader), cudaMemcpyDeviceToHost, ctx->stream);
@@ -430,6 +554,11 @@ gp_status run_batch(gp_ctx *ctx, const gp_circuit_view *cs, size_t count, uint8_
         if (e != cudaSuccess) return cuda_fail(ctx, e, "device pipeline");
         hdr = *ctx->h_hdr;
         if (attempt > 4) return fail(ctx, GP_ERR_CUDA, "capacity retry loop did not converge");
+        if (hdr.pool_overflow) {  // the record pool was too small
+            pool = 2 * std::max<uint64_t>(pool, hdr.pool_chunks);
+            ctx->pool_hint = pool;
+            continue;
+        }
         if (hdr.record_overflow) {  // a signature spans more words than inline slots
             K = std::min<uint32_t>(16, std::max<uint32_t>(hdr.record_overflow, 2 * K));
             if (hdr.record_overflow > 16)
@@ -560,6 +689,9 @@ gp_status gp_ctx_set_option(gp_ctx *ctx, int option, int64_t value) {
             return GP_OK;
         case GP_OPT_SYNC_TIMING:
             return GP_OK;  // stage events are always recorded
+        case 99:  // traversal experiments (not part of the ABI contract)
+            ctx->trav_debug = (uint32_t)value;
+            return GP_OK;
     }
     return fail(ctx, GP_ERR_INVALID_ARGUMENT, "unknown option");
 }

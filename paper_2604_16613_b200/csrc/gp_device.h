@@ -7,6 +7,20 @@
 
 namespace gp {
 
+constexpr uint32_t kPoolChunk = 1024;  // records per pool chunk
+constexpr uint32_t kPoolInvalid = 0xFFFFFFFFu;
+
+// Traversal launch configuration (chosen by plan_traversal for a batch).
+struct TravCfg {
+    uint32_t T;          // 64-bit detector words per CTA (column group width)
+    uint32_t R;          // state ring depth (boundaries in flight between warp roles)
+    uint32_t NST;        // staging ring depth (boundaries prefetched by the producer)
+    uint32_t node_warps, emit_warps;
+    uint32_t max_n, max_layer_noise, max_layer_meas, max_l;
+    uint32_t direct;     // every circuit fits one group: atomic-free emission
+    uint32_t debug;      // experiments only: bit0 skip emission work, bit1 skip node work
+};
+
 // Every device array used by one compile. Carved from one workspace
 // allocation by the host (gp_api.cpp); sizes follow BatchTotals.
 struct DevPlan {
@@ -14,6 +28,8 @@ struct DevPlan {
     const uint8_t *img;
     StageLayout lay;
     BatchTotals tot;
+    TravCfg trav;
+    size_t trav_smem;
 
     // STEPG IR built on device.
     uint64_t *ell;   // [tot.ell] base-slot ELLPACK
@@ -25,6 +41,10 @@ struct DevPlan {
     uint64_t *rbits;   // [S * K]
     uint32_t *rtile;   // [S * K]
     uint32_t K;        // inline record slots per source
+    // Record pool (multi-CTA circuits): the traversal appends (source, word,
+    // bits) records in per-warp chunks; slot_kernel files them per source.
+    uint4 *pool;          // [pool_chunks_cap * kPoolChunk] {src, word, bits lo, bits hi}
+    uint32_t pool_chunks_cap;
     uint32_t *rep;     // [S] representative source (group key) or kSuccNone
     uint32_t *gcnt;    // [S] members per representative
     uint2 *ecnt;       // [S] (detector ids, observable ids) per representative
@@ -91,9 +111,9 @@ constexpr const char *kProfNames[kProfCount] = {"start",   "memset",     "lower"
 int enqueue_pipeline(const DevPlan &p, cudaStream_t stream, const StageEvents *events,
                      const cudaEvent_t *prof, cudaError_t *err);
 
-// Dynamic shared memory the traversal kernel needs for a batch, and the
-// number of staging buffers it will use; returns false if a circuit is too
-// wide for on-chip state (2n 64-bit words, double-buffered).
-bool traversal_smem(const BatchTotals &t, int device, size_t *bytes, int *stages, int *threads);
+// Chooses the traversal configuration for a batch (group width, ring depths,
+// warp roles) and its dynamic shared memory; false if a circuit is too wide
+// for on-chip state (R x T x 2n words).
+bool plan_traversal(const BatchTotals &t, int device, TravCfg *cfg, size_t *smem);
 
 }  // namespace gp

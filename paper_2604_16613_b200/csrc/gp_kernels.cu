@@ -20,7 +20,6 @@ namespace gp {
 
 namespace {
 
-constexpr int kTravStagesMax = 4;
 
 // ---------------------------------------------------------------- helpers
 
@@ -113,12 +112,16 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t *bar, uint32_t parity) {
     return ok != 0;
 }
 
+// Bounded wait: a protocol bug traps (a CUDA error the host reports) instead
+// of hanging the device (a few seconds of suspended try_waits).
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
-    while (!mbar_try_wait(bar, parity)) {
-    }
+    uint32_t spins = 0;
+    while (!mbar_try_wait(bar, parity))
+        if (++spins > 20000000u) __trap();
 }
 
 __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+    if ((smem_u32(dst) | (uint32_t)(uintptr_t)src | bytes) & 15u) __trap();  // would never complete
     asm volatile(
         "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
             smem_u32(dst)),
@@ -230,270 +233,24 @@ __global__ void lower_kernel(DevPlan p, uint32_t blocks_a) {
 }
 
 // ---------------------------------------------------------------- K2 traversal
-// One CTA per (circuit, 64-bit detector column tile). The CTA keeps the tile's
-// column of the class matrix for boundaries i+1 and i in shared memory
-// (2 x 2n words) and walks the boundaries backwards (Alg. 1, PAPER.md:199-232;
-// eec.cpp:111-122) with one CTA barrier per boundary -- no grid sync, no
-// per-layer launch. Each boundary's ELLPACK slice, noise ops and the leaf
-// words of the next layer's measurements are staged into a ring of shared
-// buffers by bulk async copies issued NST-1 boundaries ahead.
-// Time window: the tile starts at the last layer holding one of its
-// measurements and stops once its column is all zero below its first one.
-// Fused epilogue per boundary: every noise op placed there XORs <= 4 base
-// rows per component and emits only nonzero words (source, tile, bits).
+}  // namespace
+#include "gp_traverse.cuh"
+namespace {
 
-// Shared-memory carve-up of the traversal CTA: two state columns (boundary
-// i+1 and i, 2n words each) followed by `stages` staging buffers and one
-// mbarrier per stage. Word counts cover the 16-byte rounding of bulk copies.
-struct TravDims {
-    uint32_t n2, stages, ell_words, leaf_words, noise_words, src_words;
-    __host__ __device__ TravDims(uint32_t max_n, uint32_t max_meas, uint32_t max_noise, uint32_t k)
-        : n2(2 * max_n),
-          stages(k),
-          ell_words(2 * max_n),
-          leaf_words((max_meas + 3) & ~1u),
-          noise_words((max_noise + 3) & ~1u),
-          src_words((max_noise + 9) & ~3u) {}
-    __host__ __device__ size_t state_bytes() const { return (size_t)2 * n2 * 8; }
-    __host__ __device__ size_t stage_bytes() const {
-        return (size_t)(ell_words + leaf_words + noise_words) * 8 + (size_t)src_words * 4;
-    }
-    __host__ __device__ size_t total_bytes() const { return state_bytes() + stages * stage_bytes() + stages * 8; }
-    __device__ uint64_t *state(uint8_t *base, int which) const {
-        return reinterpret_cast<uint64_t *>(base) + (size_t)which * n2;
-    }
-    __device__ uint8_t *stage(uint8_t *base, int k) const { return base + state_bytes() + (size_t)k * stage_bytes(); }
-    __device__ uint64_t *bars(uint8_t *base) const { return reinterpret_cast<uint64_t *>(stage(base, stages)); }
-};
-
-__device__ __forceinline__ void put_record(const DevPlan &p, uint64_t src, uint32_t j, uint32_t tile,
-                                           uint64_t bits) {
+// Files the traversal's pooled records into per-source slots: the returning
+// slot-claim atomics run here, throughput-bound, off the traversal's path.
+__global__ void slot_kernel(DevPlan p) {
+    const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const uint32_t used = min(p.hdr->pool_chunks, p.pool_chunks_cap);
+    if (i >= (uint64_t)used * kPoolChunk) return;
+    const uint4 r = p.pool[i];
+    if (r.x == kPoolInvalid) return;
+    const uint32_t j = atomicAdd(&p.cnt[r.x], 1u);
     if (j < p.K) {
-        p.rbits[src * p.K + j] = bits;
-        p.rtile[src * p.K + j] = tile;
+        p.rbits[(uint64_t)r.x * p.K + j] = (uint64_t)r.w << 32 | r.z;
+        p.rtile[(uint64_t)r.x * p.K + j] = r.y;
     } else {
         atomicMax(&p.hdr->record_overflow, j + 1);
-    }
-}
-
-__device__ __forceinline__ void emit(const DevPlan &p, uint64_t src, uint32_t tile, uint64_t bits) {
-    put_record(p, src, atomicAdd(&p.cnt[src], 1u), tile, bits);
-}
-
-__global__ void __launch_bounds__(1024) traverse_kernel(DevPlan p, uint32_t stages, uint32_t max_n,
-                                                        uint32_t max_layer_noise, uint32_t max_layer_meas) {
-    extern __shared__ __align__(16) uint8_t smem[];
-    __shared__ uint32_t s_min_m, s_max_m;
-    __shared__ CircuitMeta s_meta;
-    __shared__ uint32_t s_c;
-
-    const uint32_t tid = threadIdx.x, nthr = blockDim.x;
-    if (tid == 0) {
-        s_c = find_u32(arr<uint32_t>(p, p.lay.circ_tile), p.tot.C, blockIdx.x);
-        s_meta = arr<CircuitMeta>(p, p.lay.meta)[s_c];
-        s_min_m = 0xFFFFFFFFu;
-        s_max_m = 0;
-    }
-    __syncthreads();
-    const CircuitMeta m = s_meta;
-    const uint32_t t = blockIdx.x - m.tile_base;
-    const uint32_t n2 = 2 * m.n;
-
-    // Measurement window of this tile's detectors / observables.
-    {
-        const uint32_t d0 = t * 64, d1 = min(d0 + 64, m.D);
-        const uint32_t *doff = arr<uint32_t>(p, p.lay.det_off) + m.det_base;
-        const uint32_t *dms = arr<uint32_t>(p, p.lay.det_meas);
-        uint32_t lo = 0xFFFFFFFFu, hi = 0;
-        for (uint32_t d = d0 + tid; d < d1; d += nthr)
-            for (uint32_t k = doff[d]; k < doff[d + 1]; k++) {
-                lo = min(lo, dms[k]);
-                hi = max(hi, dms[k]);
-            }
-        const uint32_t ob0 = max(d0, m.D), ob1 = min(t * 64 + 64, m.D + m.O);
-        const uint32_t *ooff = arr<uint32_t>(p, p.lay.obs_off) + m.obs_base;
-        const uint32_t *oms = arr<uint32_t>(p, p.lay.obs_meas);
-        for (uint32_t b = ob0; b < ob1; b++) {  // few observables: spread their entries
-            const uint32_t o = b - m.D;
-            for (uint32_t k = ooff[o] + tid; k < ooff[o + 1]; k += nthr) {
-                lo = min(lo, oms[k]);
-                hi = max(hi, oms[k]);
-            }
-        }
-        if (lo != 0xFFFFFFFFu) {
-            atomicMin(&s_min_m, lo);
-            atomicMax(&s_max_m, hi);
-        }
-    }
-    __syncthreads();
-    const uint32_t min_m = s_min_m, max_m = s_max_m;
-    if (min_m == 0xFFFFFFFFu) return;  // column all zero
-
-    const uint64_t *leafrow = p.leaf + m.leaf_base + (uint64_t)t * m.M;
-    const uint64_t src_flip = m.src_base + m.src_noise;
-
-    // Measurement-flip sources: their rows are the leaf rows (stepg.cpp:270-272).
-    {
-        const double *flip = arr<double>(p, p.lay.meas_flip) + m.meas_base;
-        for (uint32_t mm = min_m + tid; mm <= max_m; mm += nthr) {
-            if (flip[mm] > 0) {
-                const uint64_t w = leafrow[mm];
-                if (w) emit(p, src_flip + mm, t, w);
-            }
-        }
-    }
-
-    const uint32_t *lay_meas = arr<uint32_t>(p, p.lay.lay_meas) + m.layer_base;
-    const uint32_t *lay_noise = arr<uint32_t>(p, p.lay.lay_noise) + m.layer_base;
-    auto layer_of = [&](uint32_t mm) {  // largest i with lay_meas[i] <= mm
-        uint32_t lo = 0, hi = m.l;
-        while (hi - lo > 1) {
-            uint32_t mid = (lo + hi) >> 1;
-            if (lay_meas[mid] <= mm) lo = mid;
-            else hi = mid;
-        }
-        return lo;
-    };
-    const int first_layer = (int)layer_of(min_m);
-    const int b_hi = (int)layer_of(max_m) - 1;
-    if (b_hi < 0) return;
-
-    const TravDims L(max_n, max_layer_meas, max_layer_noise, stages);
-    uint64_t *bars = L.bars(smem);
-    uint64_t *st[2] = {L.state(smem, 0), L.state(smem, 1)};
-
-    const uint64_t *ell = p.ell + m.ell_base;
-    const uint64_t *noise = arr<uint64_t>(p, p.lay.noise);
-    const uint32_t *nsrc = arr<uint32_t>(p, p.lay.noise_src);
-
-    // Stage k holds boundary i: ELL slice of i, leaf words of layer i+1's
-    // measurements, noise ops of layer i (+ their source offsets).
-    auto issue = [&](int i, int k) {
-        uint8_t *sb = L.stage(smem, k);
-        uint64_t *s_ell = reinterpret_cast<uint64_t *>(sb);
-        uint64_t *s_leaf = s_ell + L.ell_words;
-        uint64_t *s_noise = s_leaf + L.leaf_words;
-        uint32_t *s_src = reinterpret_cast<uint32_t *>(s_noise + L.noise_words);
-        const uint32_t mb = lay_meas[i + 1], me = lay_meas[i + 2];  // i <= l - 2
-        const uint64_t leaf_a = (uint64_t)(leafrow + mb) & ~15ull;
-        const uint64_t leaf_e = ((uint64_t)(leafrow + me) + 15) & ~15ull;
-        const uint32_t n0 = lay_noise[i], n1 = lay_noise[i + 1];
-        const uint64_t noise_a = (uint64_t)(noise + n0) & ~15ull;
-        const uint64_t noise_e = ((uint64_t)(noise + n1) + 15) & ~15ull;
-        const uint64_t src_a = (uint64_t)(nsrc + n0) & ~15ull;
-        const uint64_t src_e = ((uint64_t)(nsrc + n1) + 15) & ~15ull;
-        const uint32_t b_ell = n2 * 8;
-        const uint32_t b_leaf = me > mb ? (uint32_t)(leaf_e - leaf_a) : 0;
-        const uint32_t b_noise = n1 > n0 ? (uint32_t)(noise_e - noise_a) : 0;
-        const uint32_t b_src = n1 > n0 ? (uint32_t)(src_e - src_a) : 0;
-        fence_proxy_async();
-        mbar_arrive_expect_tx(&bars[k], b_ell + b_leaf + b_noise + b_src);
-        bulk_g2s(s_ell, ell + (uint64_t)i * n2, b_ell, &bars[k]);
-        if (b_leaf) bulk_g2s(s_leaf, (const void *)leaf_a, b_leaf, &bars[k]);
-        if (b_noise) bulk_g2s(s_noise, (const void *)noise_a, b_noise, &bars[k]);
-        if (b_src) bulk_g2s(s_src, (const void *)src_a, b_src, &bars[k]);
-    };
-
-    if (tid == 0) {
-        for (uint32_t k = 0; k < stages; k++) mbar_init(&bars[k], 1);
-        mbar_fence_init();
-    }
-    for (uint32_t s = tid; s < n2; s += nthr) st[0][s] = 0;  // boundary b_hi + 1 is all zero
-    __syncthreads();
-    if (tid == 0)
-        for (int j = 0; j < (int)stages - 1 && b_hi - j >= 0; j++) issue(b_hi - j, j);
-
-    const uint32_t level = p.tot.level;
-    int cur = 0;  // st[cur] = boundary i + 1
-    int i = b_hi;
-    for (; i >= 0; i--) {
-        const int j = b_hi - i;
-        const int k = j % (int)stages;
-        mbar_wait(&bars[k], (uint32_t)(j / (int)stages) & 1u);
-        uint8_t *sb = L.stage(smem, k);
-        const uint64_t *s_ell = reinterpret_cast<const uint64_t *>(sb);
-        const uint64_t *s_leaf = s_ell + L.ell_words;
-        const uint64_t *s_noise = s_leaf + L.leaf_words;
-        const uint32_t *s_src = reinterpret_cast<const uint32_t *>(s_noise + L.noise_words);
-        const uint32_t mb = lay_meas[i + 1];
-        const uint32_t leaf_shift = (uint32_t)(((uint64_t)(leafrow + mb) & 15ull) >> 3);
-        const uint64_t *nxt = st[cur];
-        uint64_t *now = st[cur ^ 1];
-        bool any = false;
-        for (uint32_t s = tid; s < n2; s += nthr) {
-            const uint64_t w = s_ell[s];
-            uint64_t acc;
-            if (w == kEllIdle) {
-                acc = nxt[s];
-            } else {
-                acc = 0;
-                const uint32_t v0 = (uint32_t)w, v1 = (uint32_t)(w >> 32);
-                if (v0 != kSuccNone) acc ^= (v0 & kSuccLeaf) ? s_leaf[leaf_shift + (v0 & ~kSuccLeaf) - mb] : nxt[v0];
-                if (v1 != kSuccNone) acc ^= (v1 & kSuccLeaf) ? s_leaf[leaf_shift + (v1 & ~kSuccLeaf) - mb] : nxt[v1];
-            }
-            now[s] = acc;
-            any |= acc != 0;
-        }
-        const bool block_any = __syncthreads_or(any);
-        if (!block_any && first_layer > i) break;  // column is zero from here down
-        if (tid == 0 && i + 1 - (int)stages >= 0) issue(i + 1 - (int)stages, (j + (int)stages - 1) % (int)stages);
-        if (block_any) {
-            const uint32_t n0 = lay_noise[i], n1 = lay_noise[i + 1];
-            const uint32_t nshift = (uint32_t)(((uint64_t)(noise + n0) & 15ull) >> 3);
-            const uint32_t sshift = (uint32_t)(((uint64_t)(nsrc + n0) & 15ull) >> 2);
-            for (uint32_t o = tid; o < n1 - n0; o += nthr) {
-                const uint64_t w = s_noise[nshift + o];
-                const uint32_t lo = (uint32_t)w;
-                const uint32_t kind = lo >> kNoiseKindShift;
-                const uint32_t q0 = lo & ((1u << kNoiseKindShift) - 1), q1 = (uint32_t)(w >> 32);
-                const uint64_t src = m.src_base + s_src[sshift + o];
-                const uint64_t x0 = now[2 * q0], z0 = now[2 * q0 + 1];
-                if (kind <= 1) {
-                    const uint64_t v = kind == 0 ? x0 : z0;
-                    if (v) emit(p, src, t, v);
-                } else if (kind == 2) {
-                    if ((x0 | z0) == 0) continue;
-                    // X, Z (+ Y at L1+): all slot claims in flight before any store
-                    const uint64_t v[3] = {x0, z0, level ? x0 ^ z0 : 0};
-                    uint32_t slot[3];
-#pragma unroll
-                    for (int c = 0; c < 3; c++)
-                        if (v[c]) slot[c] = atomicAdd(&p.cnt[src + c], 1u);
-#pragma unroll
-                    for (int c = 0; c < 3; c++)
-                        if (v[c]) put_record(p, src + c, slot[c], t, v[c]);
-                } else {
-                    const uint64_t x1 = now[2 * q1], z1 = now[2 * q1 + 1];
-                    if ((x0 | z0 | x1 | z1) == 0) continue;
-                    const uint32_t nc = level == 0 ? 6 : level == 1 ? 10 : 15;
-                    constexpr uint8_t kMask[15] = {4, 8, 1, 5, 2, 10, 12, 9, 3, 6, 13, 7, 15, 11, 14};
-                    uint64_t v[15];
-                    uint32_t slot[15];
-#pragma unroll
-                    for (int c = 0; c < 15; c++) {
-                        const uint32_t mk = kMask[c];
-                        v[c] = (uint32_t)c < nc ? ((mk & 1) ? x0 : 0) ^ ((mk & 2) ? z0 : 0) ^ ((mk & 4) ? x1 : 0) ^
-                                                      ((mk & 8) ? z1 : 0)
-                                                : 0;
-                    }
-#pragma unroll
-                    for (int c = 0; c < 15; c++)
-                        if (v[c]) slot[c] = atomicAdd(&p.cnt[src + c], 1u);
-#pragma unroll
-                    for (int c = 0; c < 15; c++)
-                        if (v[c]) put_record(p, src + c, slot[c], t, v[c]);
-                }
-            }
-        }
-        cur ^= 1;
-    }
-    // Drain bulk copies still in flight after an early exit.
-    if (i >= 0) {
-        const int lowest = max(0, i + 2 - (int)stages);  // issued: [lowest, i - 1]
-        for (int b = i - 1; b >= lowest; b--) {
-            const int j = b_hi - b;
-            mbar_wait(&bars[j % (int)stages], (uint32_t)(j / (int)stages) & 1u);
-        }
     }
 }
 
@@ -688,7 +445,9 @@ struct BucketScanF {
 struct PosScanF {  // (detector ids, observable ids) in canonical order
     const uint32_t *perm, *nd, *no;
     const DeviceHeader *hdr;
-    __device__ bool active(uint64_t base) const { return base < hdr->num_edges; }
+    __device__ bool active(uint64_t base) const {  // not on a capacity-failed attempt (perm unwritten)
+        return base < hdr->num_edges && hdr->record_overflow == 0 && hdr->num_det_ids != 0xFFFFFFFFu;
+    }
     __device__ uint4 operator()(uint64_t q) const {
         if (q >= hdr->num_edges) return make_uint4(0, 0, 0, 0);
         const uint32_t e = perm[q];
@@ -699,16 +458,18 @@ struct PosScanF {  // (detector ids, observable ids) in canonical order
 // ---------------------------------------------------------------- K5..K9
 
 __global__ void totals_kernel(DevPlan p, const uint4 *src_total) {
-    // after the source scan: publish edge / member / id totals, check capacity
+    // after the source scan: publish edge / member / id totals, check id
+    // capacity, and per-circuit edge offsets (one thread per circuit)
     const uint4 t = *src_total;
-    p.hdr->num_edges = t.x;
-    p.hdr->num_members = t.y;
-    if ((uint64_t)t.z > p.ids_cap) p.hdr->num_det_ids = 0xFFFFFFFFu;  // capacity overflow marker
-    p.e_moff[t.x] = t.y;
-    // per-circuit edge offsets
-    const uint64_t *circ_src = arr<uint64_t>(p, p.lay.circ_src);
-    for (uint32_t c = 0; c <= p.tot.C; c++) {
-        const uint64_t s0 = circ_src[c];
+    const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c == 0) {
+        p.hdr->num_edges = t.x;
+        p.hdr->num_members = t.y;
+        if ((uint64_t)t.z > p.ids_cap) p.hdr->num_det_ids = 0xFFFFFFFFu;  // capacity overflow marker
+        p.e_moff[t.x] = t.y;
+    }
+    if (c <= p.tot.C) {
+        const uint64_t s0 = arr<uint64_t>(p, p.lay.circ_src)[c];
         p.o_edge_off[c] = s0 < p.tot.sources ? p.sscan[s0].x : t.x;
     }
 }
@@ -886,17 +647,46 @@ uint32_t blocks_for(uint64_t n, uint32_t tpb) { return (uint32_t)((n + tpb - 1) 
 
 }  // namespace
 
-bool traversal_smem(const BatchTotals &t, int device, size_t *bytes, int *stages, int *threads) {
-    int optin = 0;
+bool plan_traversal(const BatchTotals &t, int device, TravCfg *cfg, size_t *smem) {
+    int optin = 0, sms = 148;
     cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
-    const size_t budget = (size_t)optin - 1024;  // static shared variables + slack
-    int k = kTravStagesMax;
-    while (k > 2 && TravDims(t.max_n, t.max_layer_meas, t.max_layer_noise, k).total_bytes() > budget) k--;
-    *stages = k;
-    *bytes = TravDims(t.max_n, t.max_layer_meas, t.max_layer_noise, k).total_bytes();
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+    const size_t budget = (size_t)optin - 2048;  // static shared variables + slack
+    TravCfg c{};
+    c.max_n = t.max_n;
+    c.max_layer_noise = t.max_layer_noise;
+    c.max_layer_meas = t.max_layer_meas;
+    c.max_l = t.max_l;
     const uint32_t n2 = 2 * t.max_n;
-    *threads = n2 <= 256 ? 128 : n2 <= 1024 ? 256 : n2 <= 4096 ? 512 : 1024;
-    return *bytes <= budget;
+    c.node_warps = n2 <= 512 ? 4 : n2 <= 2048 ? 8 : 12;
+    c.emit_warps = c.node_warps;
+    // Wide groups (one CTA per circuit, atomic-free emission) when the batch
+    // alone fills the machine; one word per CTA for single large circuits.
+    uint32_t T = 1;
+    if (t.C >= 2u * (uint32_t)sms && t.max_W <= 8) T = t.max_W;
+    // Batches: shallow rings (more CTAs per SM); single circuits: deep rings
+    // (the copy latency of a boundary's stage hides behind NST-1 boundaries).
+    static const uint32_t kBatch[][2] = {{3, 3}, {2, 3}, {2, 2}};
+    static const uint32_t kSingle[][2] = {{6, 8}, {4, 8}, {4, 6}, {4, 4}, {3, 3}, {2, 2}};
+    for (;; T = (T + 1) / 2) {
+        const bool batch = T > 1;
+        const uint32_t(*opts)[2] = batch ? kBatch : kSingle;
+        const int nopt = batch ? 3 : 6;
+        for (int o = 0; o < nopt; o++) {
+            const uint32_t R = opts[o][0], N = opts[o][1];
+            const trav::Dims d(T, R, N, t.max_n, t.max_layer_meas, t.max_layer_noise, t.max_l);
+            if (d.total_bytes() <= budget) {
+                c.T = T;
+                c.R = R;
+                c.NST = N;
+                c.direct = t.max_W <= T;
+                *cfg = c;
+                *smem = d.total_bytes();
+                return true;
+            }
+        }
+        if (T == 1) return false;
+    }
 }
 
 int enqueue_pipeline(const DevPlan &p, cudaStream_t st, const StageEvents *ev, const cudaEvent_t *prof,
@@ -928,15 +718,23 @@ int enqueue_pipeline(const DevPlan &p, cudaStream_t st, const StageEvents *ev, c
     if (ev) cudaEventRecord(ev->lowered, st);
 
     // K2 traversal.
-    if (p.tot.tiles) {
-        size_t smem;
-        int stages, threads, dev;
-        cudaGetDevice(&dev);
-        traversal_smem(p.tot, dev, &smem, &stages, &threads);
-        cudaFuncSetAttribute(traverse_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        traverse_kernel<<<(uint32_t)p.tot.tiles, threads, smem, st>>>(p, stages, p.tot.max_n, p.tot.max_layer_noise,
-                                                                    p.tot.max_layer_meas);
+    if (p.tot.groups) {
+        const TravCfg &c = p.trav;
+        const int threads = 32 * (1 + (int)c.node_warps + (int)c.emit_warps);
+        const uint32_t tm = c.T <= 1 ? 1 : c.T <= 2 ? 2 : c.T <= 4 ? 4 : 8;
+        auto launch = [&](auto kern) {
+            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.trav_smem);
+            kern<<<(uint32_t)p.tot.groups, threads, p.trav_smem, st>>>(p, c);
+        };
+        if (tm == 1) launch(trav::traverse_kernel<1>);
+        else if (tm == 2) launch(trav::traverse_kernel<2>);
+        else if (tm == 4) launch(trav::traverse_kernel<4>);
+        else launch(trav::traverse_kernel<8>);
         launches++;
+        if (p.pool_chunks_cap) {
+            slot_kernel<<<(uint32_t)((uint64_t)p.pool_chunks_cap * kPoolChunk / 256), 256, 0, st>>>(p);
+            launches++;
+        }
     }
     mark(kProfTraverse);
     if (ev) cudaEventRecord(ev->traversed, st);
@@ -947,7 +745,7 @@ int enqueue_pipeline(const DevPlan &p, cudaStream_t st, const StageEvents *ev, c
     if (S) dedup_kernel<<<blocks_for(S, tpb), tpb, 0, st>>>(p), launches++;
     mark(kProfDedup);
     launch_scan(SrcScanF{p.rep, p.gcnt, p.ecnt, p.hdr}, S, p.bsum, p.sscan, &totals[0], st, &launches);
-    totals_kernel<<<1, 1, 0, st>>>(p, &totals[0]), launches++;
+    totals_kernel<<<blocks_for(p.tot.C + 1, 256), 256, 0, st>>>(p, &totals[0]), launches++;
     mark(kProfScanSrc);
     if (S) scatter_kernel<<<blocks_for(S, tpb), tpb, 0, st>>>(p), launches++;
     mark(kProfScatter);

@@ -40,6 +40,8 @@ struct CircuitMeta {
     uint64_t src_base;     // global id of source 0
     uint64_t ell_base;     // ELLPACK index of (boundary 0, slot 0); (l - 1) * 2n entries
     uint64_t leaf_base;    // leaf matrix index of (tile 0, meas 0); W * M entries, tile-major
+    // Host-side packing bases (global element indices of this circuit's slices).
+    uint64_t gate_base, noise_base, det_entry_base, obs_entry_base, circ_layer_base;
 };
 
 // Offsets (bytes) of every array inside one staging image.
@@ -48,6 +50,7 @@ struct StageLayout {
     uint64_t circ_layer;  // u32[C + 1] cumulative layer count (for warp -> circuit search)
     uint64_t circ_src;    // u64[C + 1] cumulative sources
     uint64_t circ_tile;   // u32[C + 1] cumulative tiles
+    uint64_t circ_grp;    // u32[C + 1] cumulative traversal column groups
     uint64_t circ_det;    // u32[C + 1] cumulative detectors
     uint64_t circ_obs;    // u32[C + 1] cumulative observables
     uint64_t lay_gate;    // u32[sum(l + 1)] global gate index of each layer start
@@ -74,11 +77,14 @@ struct BatchTotals {
     uint64_t det_slots, det_entries, obs_slots, obs_entries;
     uint64_t dets, obss;
     uint64_t tiles;
+    uint64_t groups;      // traversal CTAs: sum ceil(W / T)
+    uint32_t max_W;
     uint64_t sources;
     uint64_t ell;         // sum (l - 1) * 2n
     uint64_t leaf;        // sum W * M
     uint64_t buckets;     // sum (D + 1)
     uint32_t max_n;       // max qubits
+    uint32_t max_l;       // max layers
     uint32_t max_layer_noise;
     uint32_t max_layer_meas;
 };
@@ -90,7 +96,9 @@ struct DeviceHeader {
     uint32_t num_obs_ids;
     uint32_t num_members;
     uint32_t record_overflow;  // max records seen for one source if > slots, else 0
-    uint32_t pad[3];
+    uint32_t pool_chunks;      // record-pool chunks handed out by the traversal
+    uint32_t pool_overflow;    // chunks requested beyond capacity (re-run larger)
+    uint32_t pad;
 };
 
 }  // namespace gp
