@@ -28,6 +28,17 @@ using gp::DevPlan;
 using gp::DeviceHeader;
 using gp::StageLayout;
 
+// Per-circuit counts of pass 1 (independent across circuits).
+struct CircCount {
+    int err;  // 0 ok, 1 index space, 2 detector leaf, 3 observable leaf, 4 too wide
+    uint32_t src_noise, max_noise, max_meas;
+    uint64_t gates, noise, det_entries, obs_entries;
+    std::vector<double> probs;  // distinct noise probabilities (<= kLocalProbs, else many)
+    std::vector<uint32_t> pidx; // global table index of each local probability
+    bool many;
+};
+constexpr size_t kLocalProbs = 64;
+
 struct gp_ctx {
     int device = 0;
     cudaStream_t stream = nullptr;
@@ -53,6 +64,8 @@ struct gp_ctx {
 
     std::vector<CircuitMeta> metas;
     std::vector<uint32_t> out_ndet, out_nobs;
+    std::vector<double> prob_table;
+    std::vector<CircCount> circ_counts;
 
     // Last successful device plan (for gp_replay) and profiling state.
     bool has_plan = false;
@@ -110,12 +123,7 @@ void parallel_for(size_t n, F f) {
     for (auto &th : pool) th.join();
 }
 
-// Per-circuit counts of pass 1 (independent across circuits).
-struct CircCount {
-    int err;  // 0 ok, 1 index space, 2 detector leaf, 3 observable leaf, 4 too wide
-    uint32_t src_noise, max_noise, max_meas;
-    uint64_t gates, noise, det_entries, obs_entries;
-};
+
 
 // Pass 1: validation (the reference's exceptions, in the reference's order;
 // for a batch, the first failing circuit), device-encoding limits, totals and
@@ -148,7 +156,7 @@ gp_status plan_batch(gp_ctx *ctx, const gp_circuit_view *cs, size_t C, uint8_t l
                     k.err = 3;
                     return;
                 }
-        if (v.num_qubits >= (1u << 29) || v.num_measurements >= 0x7FFFFFFFu) {
+        if (v.num_qubits >= (1u << gp::kNoiseQubitBits) || v.num_measurements >= 0x7FFFFFFFu) {
             k.err = 4;
             return;
         }
@@ -156,7 +164,17 @@ gp_status plan_batch(gp_ctx *ctx, const gp_circuit_view *cs, size_t C, uint8_t l
         for (uint32_t i = 0; i < v.num_layers; i++) {
             const uint32_t n0 = v.noise_offsets[i], n1 = v.noise_offsets[i + 1];
             k.max_noise = std::max(k.max_noise, n1 - n0);
-            for (uint32_t o = n0; o < n1; o++) src += components(v.noise_kind[o], level);
+            for (uint32_t o = n0; o < n1; o++) {
+                src += components(v.noise_kind[o], level);
+                if (k.many) continue;
+                const double pr = v.noise_prob[o];
+                bool seen = false;
+                for (double q : k.probs) seen |= std::memcmp(&q, &pr, 8) == 0;
+                if (!seen) {
+                    if (k.probs.size() == kLocalProbs) k.many = true;
+                    else k.probs.push_back(pr);
+                }
+            }
             uint32_t meas = 0;
             for (uint32_t g = v.gate_offsets[i]; g < v.gate_offsets[i + 1]; g++)
                 meas += v.gate_kind[g] == GP_GATE_M || v.gate_kind[g] == GP_GATE_MR;
@@ -168,15 +186,50 @@ gp_status plan_batch(gp_ctx *ctx, const gp_circuit_view *cs, size_t C, uint8_t l
         k.det_entries = v.det_offsets[v.num_detectors] - v.det_offsets[0];
         k.obs_entries = v.obs_offsets[v.num_observables] - v.obs_offsets[0];
     });
+    // Batch probability table (bit-exact keys); wide mode if it would not fit.
+    {
+        std::vector<uint64_t> keys;
+        bool many = false;
+        for (const CircCount &k : cc) {
+            many |= k.many;
+            for (double q : k.probs) {
+                uint64_t b;
+                std::memcpy(&b, &q, 8);
+                keys.push_back(b);
+            }
+        }
+        std::sort(keys.begin(), keys.end());
+        keys.erase(std::unique(keys.begin(), keys.end()), keys.end());
+        t.wide_prob = many || keys.size() > gp::kNoisePidxMax;
+        ctx->prob_table.clear();
+        if (!t.wide_prob) {
+            for (uint64_t b : keys) {
+                double q;
+                std::memcpy(&q, &b, 8);
+                ctx->prob_table.push_back(q);
+            }
+            for (CircCount &k : cc) {
+                k.pidx.clear();
+                for (double q : k.probs) {
+                    uint64_t b;
+                    std::memcpy(&b, &q, 8);
+                    k.pidx.push_back((uint32_t)(std::lower_bound(keys.begin(), keys.end(), b) - keys.begin()));
+                }
+            }
+        }
+        t.prob_table_n = (uint32_t)ctx->prob_table.size();
+        ctx->circ_counts = std::move(cc);
+    }
+    std::vector<CircCount> &cc2 = ctx->circ_counts;
     static const char *kErr[] = {"", "circuit exceeds 32-bit node index space",
                                  "detector references a measurement without a leaf",
                                  "observable references a measurement without a leaf",
                                  "circuit too wide for the device encoding"};
     for (size_t c = 0; c < C; c++)
-        if (cc[c].err) return fail(ctx, cc[c].err == 4 ? GP_ERR_UNSUPPORTED : GP_ERR_INVALID_ARGUMENT, kErr[cc[c].err]);
+        if (cc2[c].err) return fail(ctx, cc2[c].err == 4 ? GP_ERR_UNSUPPORTED : GP_ERR_INVALID_ARGUMENT, kErr[cc2[c].err]);
     for (size_t c = 0; c < C; c++) {  // prefix sums (serial, O(C))
         const gp_circuit_view &v = cs[c];
-        const CircCount &k = cc[c];
+        const CircCount &k = cc2[c];
         CircuitMeta &m = metas[c];
         m.n = v.num_qubits;
         m.l = v.num_layers;
@@ -248,8 +301,9 @@ StageLayout stage_layout(const BatchTotals &t) {
     L.lay_meas = put(t.layer_slots * 4);
     L.gates = put(t.gates * 8);
     L.noise = put(t.noise * 8);
-    L.noise_prob = put(t.noise * 8);
-    L.noise_src = put(t.noise * 4);
+    L.noise_prob = put(t.wide_prob ? t.noise * 8 : 0);
+    L.prob_table = put((uint64_t)t.prob_table_n * 8);
+    L.lay_src = put(t.layer_slots * 4);
     L.meas_flip = put(t.meas * 8);
     L.det_off = put(t.det_slots * 4);
     L.det_meas = put(t.det_entries * 4);
@@ -263,8 +317,9 @@ StageLayout stage_layout(const BatchTotals &t) {
 // slices of every array are disjoint and located by its prefix bases).
 // Cumulative per-circuit tables (O(C), serial).
 void pack_tables(const BatchTotals &t, const std::vector<CircuitMeta> &metas, const StageLayout &L, uint32_t T,
-                 uint8_t *img) {
+                 const std::vector<double> &ptab, uint8_t *img) {
     auto at = [&](uint64_t off) { return img + off; };
+    if (!ptab.empty()) std::memcpy(at(L.prob_table), ptab.data(), ptab.size() * 8);
     std::memcpy(at(L.meta), metas.data(), t.C * sizeof(CircuitMeta));
     auto *circ_layer = (uint32_t *)at(L.circ_layer);
     auto *circ_src = (uint64_t *)at(L.circ_src);
@@ -295,7 +350,7 @@ void pack_tables(const BatchTotals &t, const std::vector<CircuitMeta> &metas, co
 
 // Per-circuit slices of every section for circuits [c0, c1), in parallel.
 void pack_circuits(const gp_circuit_view *cs, const BatchTotals &t, const std::vector<CircuitMeta> &metas,
-                   const StageLayout &L, uint8_t *img, size_t c0, size_t c1) {
+                   const std::vector<CircCount> &cc, const StageLayout &L, uint8_t *img, size_t c0, size_t c1) {
     auto at = [&](uint64_t off) { return img + off; };
     auto *lay_gate = (uint32_t *)at(L.lay_gate);
     auto *lay_noise = (uint32_t *)at(L.lay_noise);
@@ -303,7 +358,7 @@ void pack_circuits(const gp_circuit_view *cs, const BatchTotals &t, const std::v
     auto *gates = (uint64_t *)at(L.gates);
     auto *noise = (uint64_t *)at(L.noise);
     auto *nprob = (double *)at(L.noise_prob);
-    auto *nsrc = (uint32_t *)at(L.noise_src);
+    auto *lay_src = (uint32_t *)at(L.lay_src);
     auto *flip = (double *)at(L.meas_flip);
     auto *det_off = (uint32_t *)at(L.det_off);
     auto *det_meas = (uint32_t *)at(L.det_meas);
@@ -320,6 +375,7 @@ void pack_circuits(const gp_circuit_view *cs, const BatchTotals &t, const std::v
             lay_gate[m.layer_base + i] = (uint32_t)(g_at + v.gate_offsets[i] - g0);
             lay_noise[m.layer_base + i] = (uint32_t)(n_at + v.noise_offsets[i] - n0);
             lay_meas[m.layer_base + i] = meas;
+            lay_src[m.layer_base + i] = src;
             if (i == m.l) break;
             for (uint32_t g = v.gate_offsets[i]; g < v.gate_offsets[i + 1]; g++) {
                 const uint8_t k = v.gate_kind[g];
@@ -332,13 +388,24 @@ void pack_circuits(const gp_circuit_view *cs, const BatchTotals &t, const std::v
                 }
                 gates[g_at + g - g0] = (uint64_t)hi << 32 | (v.gate_q0[g] | (uint32_t)k << gp::kGateKindShift);
             }
+            const CircCount &k2 = cc[c];
             for (uint32_t o = v.noise_offsets[i]; o < v.noise_offsets[i + 1]; o++) {
                 const uint8_t k = v.noise_kind[o];
                 const uint64_t idx = n_at + o - n0;
-                noise[idx] = (uint64_t)(k == GP_NOISE_DEPOLARIZE2 ? v.noise_q1[o] : 0) << 32 |
-                             (v.noise_q0[o] | (uint32_t)k << gp::kNoiseKindShift);
-                nprob[idx] = v.noise_prob[o];
-                nsrc[idx] = src;
+                uint64_t pidx = 0;
+                const double pr = v.noise_prob[o];
+                if (t.wide_prob) {
+                    nprob[idx] = pr;
+                } else {
+                    for (size_t x = 0; x < k2.probs.size(); x++)
+                        if (std::memcmp(&k2.probs[x], &pr, 8) == 0) {
+                            pidx = k2.pidx[x];
+                            break;
+                        }
+                }
+                noise[idx] = (uint64_t)v.noise_q0[o] |
+                             (uint64_t)(k == GP_NOISE_DEPOLARIZE2 ? v.noise_q1[o] : 0) << gp::kNoiseQubitBits |
+                             (uint64_t)k << gp::kNoiseKindShift | pidx << gp::kNoisePidxShift;
                 src += components(k, (uint8_t)t.level);
             }
         }
@@ -379,6 +446,7 @@ size_t carve(gp_ctx *ctx, DevPlan &p, const BatchTotals &t, uint8_t *base, uint3
     p.ell = (uint64_t *)take(t.ell * 8);
     p.leaf = (uint64_t *)take(t.leaf * 8);
     p.prob = (double *)take(S * 8);
+    p.nsrc = (uint32_t *)take(t.noise * 4 + 16);
     p.cnt = (uint32_t *)take(S * 4 + 4);
     p.rbits = (uint64_t *)take(S * K * 8);
     p.rtile = (uint32_t *)take(S * K * 4);
@@ -503,7 +571,7 @@ gp_status run_batch(gp_ctx *ctx, const gp_circuit_view *cs, size_t count, uint8_
     for (size_t k = 0; k < nchunk; k++) {
         const size_t c0 = count * k / nchunk, c1 = count * (k + 1) / nchunk;
         if (c1 == c0) continue;
-        pack_circuits(cs, t, M, L, ctx->h_stage, c0, c1);
+        pack_circuits(cs, t, M, ctx->circ_counts, L, ctx->h_stage, c0, c1);
         const CircuitMeta &a = M[c0];
         const bool last = c1 == count;
         const CircuitMeta *b = last ? nullptr : &M[c1];
@@ -512,16 +580,17 @@ gp_status run_batch(gp_ctx *ctx, const gp_circuit_view *cs, size_t count, uint8_
         slice(L.lay_meas, 4, a.layer_base, last ? t.layer_slots : b->layer_base);
         slice(L.gates, 8, a.gate_base, last ? t.gates : b->gate_base);
         slice(L.noise, 8, a.noise_base, last ? t.noise : b->noise_base);
-        slice(L.noise_prob, 8, a.noise_base, last ? t.noise : b->noise_base);
-        slice(L.noise_src, 4, a.noise_base, last ? t.noise : b->noise_base);
+        if (t.wide_prob) slice(L.noise_prob, 8, a.noise_base, last ? t.noise : b->noise_base);
+        slice(L.lay_src, 4, a.layer_base, last ? t.layer_slots : b->layer_base);
         slice(L.meas_flip, 8, a.meas_base, last ? t.meas : b->meas_base);
         slice(L.det_off, 4, a.det_base, last ? t.det_slots : b->det_base);
         slice(L.det_meas, 4, a.det_entry_base, last ? t.det_entries : b->det_entry_base);
         slice(L.obs_off, 4, a.obs_base, last ? t.obs_slots : b->obs_base);
         slice(L.obs_meas, 4, a.obs_entry_base, last ? t.obs_entries : b->obs_entry_base);
     }
-    pack_tables(t, M, L, tcfg.T, ctx->h_stage);
+    pack_tables(t, M, L, tcfg.T, ctx->prob_table, ctx->h_stage);
     slice(0, 1, 0, L.lay_gate);  // meta + cumulative tables (the image's head)
+    slice(L.prob_table, 8, 0, t.prob_table_n);
     const uint64_t pack_ns = ns_since(t0);
     if (e != cudaSuccess) return cuda_fail(ctx, e, "upload");
     cudaEventRecord(ctx->ev_h2d, ctx->stream);

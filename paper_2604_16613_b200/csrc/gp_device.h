@@ -37,6 +37,7 @@ struct DevPlan {
 
     // Per source.
     double *prob;      // [S]
+    uint32_t *nsrc;    // [N] local source offset of each noise op's first component
     uint32_t *cnt;     // [S] sparse signature words emitted
     uint64_t *rbits;   // [S * K]
     uint32_t *rtile;   // [S * K]

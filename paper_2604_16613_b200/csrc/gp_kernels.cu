@@ -194,16 +194,33 @@ __global__ void lower_kernel(DevPlan p, uint32_t blocks_a) {
                     break;
             }
         }
+        // Noise ops: component counts -> warp scan -> source offsets (from the
+        // layer's base) and per-component probabilities.
         const uint64_t *noise = arr<uint64_t>(p, p.lay.noise);
         const double *nprob = arr<double>(p, p.lay.noise_prob);
-        const uint32_t *nsrc = arr<uint32_t>(p, p.lay.noise_src);
-        for (uint32_t o = lay_noise[li] + lane; o < lay_noise[li + 1]; o += 32) {
-            const uint32_t kind = (uint32_t)noise[o] >> kNoiseKindShift;
-            const double pr = nprob[o];
-            const double pe = kind == 2 ? __ddiv_rn(pr, 3.0) : kind == 3 ? __ddiv_rn(pr, 15.0) : pr;
-            const uint32_t k = noise_components(kind, p.tot.level);
-            double *dst = p.prob + m.src_base + nsrc[o];
-            for (uint32_t j = 0; j < k; j++) dst[j] = pe;
+        const double *ptab = arr<double>(p, p.lay.prob_table);
+        uint32_t base = arr<uint32_t>(p, p.lay.lay_src)[li];
+        for (uint32_t o0 = lay_noise[li]; o0 < lay_noise[li + 1]; o0 += 32) {
+            const uint32_t o = o0 + lane;
+            const bool act = o < lay_noise[li + 1];
+            const uint64_t w = act ? noise[o] : 0;
+            const uint32_t kind = noise_kind(w);
+            const uint32_t k = act ? noise_components(kind, p.tot.level) : 0;
+            uint32_t incl = k;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const uint32_t x = __shfl_up_sync(0xffffffffu, incl, d);
+                if (lane >= (uint32_t)d) incl += x;
+            }
+            if (act) {
+                const uint32_t off = base + incl - k;
+                p.nsrc[o] = off;
+                const double pr = p.tot.wide_prob ? nprob[o] : ptab[noise_pidx(w)];
+                const double pe = kind == 2 ? __ddiv_rn(pr, 3.0) : kind == 3 ? __ddiv_rn(pr, 15.0) : pr;
+                double *dst = p.prob + m.src_base + off;
+                for (uint32_t j = 0; j < k; j++) dst[j] = pe;
+            }
+            base += __shfl_sync(0xffffffffu, incl, 31);
         }
         return;
     }

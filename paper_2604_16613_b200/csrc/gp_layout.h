@@ -8,6 +8,10 @@
 // unless marked "local".
 #pragma once
 #include <stdint.h>
+#if !defined(__CUDACC__) && !defined(__host__)
+#define __host__
+#define __device__
+#endif
 
 namespace gp {
 
@@ -23,9 +27,19 @@ constexpr uint64_t kEllIdle = 0;                 // whole word 0: idle qubit, X-
 constexpr uint64_t kEllDead = 0xFFFFFFFFFFFFFFFFull;  // R / Z into M: no successor
 
 // Gate word: lo = q0 | kind << 29, hi = q1 (CX) or local measurement index.
-// Noise word: lo = q0 | kind << 30, hi = q1.
 constexpr uint32_t kGateKindShift = 29;
-constexpr uint32_t kNoiseKindShift = 30;
+// Noise word (8 bytes per op): q0 [0,24) | q1 [24,48) | kind [48,50) |
+// probability index [50,64) into the batch's probability table (or, in
+// wide-probability mode, the op's own fp64 in noise_prob).
+constexpr uint32_t kNoiseQubitBits = 24;
+constexpr uint64_t kNoiseQubitMask = (1ull << kNoiseQubitBits) - 1;
+constexpr uint32_t kNoiseKindShift = 48;
+constexpr uint32_t kNoisePidxShift = 50;
+constexpr uint32_t kNoisePidxMax = (1u << 14) - 1;  // table entries
+__host__ __device__ inline uint32_t noise_q0(uint64_t w) { return (uint32_t)(w & kNoiseQubitMask); }
+__host__ __device__ inline uint32_t noise_q1(uint64_t w) { return (uint32_t)(w >> kNoiseQubitBits & kNoiseQubitMask); }
+__host__ __device__ inline uint32_t noise_kind(uint64_t w) { return (uint32_t)(w >> kNoiseKindShift & 3); }
+__host__ __device__ inline uint32_t noise_pidx(uint64_t w) { return (uint32_t)(w >> kNoisePidxShift); }
 
 struct CircuitMeta {
     uint32_t n, l, M, D, O, W;
@@ -57,9 +71,10 @@ struct StageLayout {
     uint64_t lay_noise;   // u32[sum(l + 1)] global noise index
     uint64_t lay_meas;    // u32[sum(l + 1)] local measurement index
     uint64_t gates;       // u64[G]
-    uint64_t noise;       // u64[N]
-    uint64_t noise_prob;  // f64[N]
-    uint64_t noise_src;   // u32[N] local source offset of the op's first component
+    uint64_t noise;       // u64[N] noise words
+    uint64_t noise_prob;  // f64[N] (wide-probability mode only, else empty)
+    uint64_t prob_table;  // f64[P] distinct noise probabilities of the batch
+    uint64_t lay_src;     // u32[sum(l + 1)] local source offset of each layer's first op
     uint64_t meas_flip;   // f64[sum M]
     uint64_t det_off;     // u32[sum(D + 1)] global index into det_meas
     uint64_t det_meas;    // u32[] local measurement ids
@@ -87,6 +102,8 @@ struct BatchTotals {
     uint32_t max_l;       // max layers
     uint32_t max_layer_noise;
     uint32_t max_layer_meas;
+    uint32_t wide_prob;   // 1: per-op fp64 probabilities (table would exceed 14 bits)
+    uint32_t prob_table_n;
 };
 
 // Header written by the device at the end of a compile (read back first).

@@ -296,7 +296,7 @@ __global__ void __launch_bounds__(800, 1) traverse_kernel(DevPlan p, TravCfg cfg
 
     const uint64_t *ell = p.ell + m.ell_base;
     const uint64_t *noise = arr<uint64_t>(p, p.lay.noise);
-    const uint32_t *nsrc = arr<uint32_t>(p, p.lay.noise_src);
+    const uint32_t *nsrc = p.nsrc;
 
     if (warp == 0) {
         // ------------------------------------------------ producer (one lane)
@@ -427,9 +427,8 @@ __global__ void __launch_bounds__(800, 1) traverse_kernel(DevPlan p, TravCfg cfg
                 const uint32_t o = ob + lane;
                 const bool act = o < nops;
                 uint64_t wd = act ? s_noise[o] : 0;
-                const uint32_t lo = (uint32_t)wd;
-                const uint32_t kind = act ? lo >> kNoiseKindShift : 0;
-                const uint32_t q0 = lo & ((1u << kNoiseKindShift) - 1), q1 = (uint32_t)(wd >> 32);
+                const uint32_t kind = act ? noise_kind(wd) : 0;
+                const uint32_t q0 = noise_q0(wd), q1 = noise_q1(wd);
                 const uint64_t src = m.src_base + (act ? s_src[o] : 0);
                 if constexpr (TM == 1) {
                     if (!direct) {

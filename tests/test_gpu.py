@@ -276,3 +276,18 @@ def test_cpp_dropin_shim(tmp_path):
     dump_flat(bad, tmp_path / "bad.txt")
     out = subprocess.run([str(exe), str(tmp_path / "bad.txt"), "0"], capture_output=True, text=True, check=True)
     assert out.stdout == "invalid_argument: detector references a measurement without a leaf\n"
+
+
+def test_many_distinct_probabilities_use_wide_mode(compiler, port):
+    """> 64 distinct noise probabilities in a circuit: per-op fp64 upload path
+    (the probability table would not be exact otherwise); results unchanged."""
+    import random
+    rng = random.Random(5)
+    g = gp.gen_surface(5, 3, 1e-3).to_circuit()
+    g.noise_prob = np.array([rng.uniform(1e-4, 3e-3) for _ in g.noise_prob])
+    for level in (0, 2):
+        assert compiler.compile(g, level).hyperedges() == port.compile(g, level)[0]
+    small = gp.gen_surface(3, 2, 1e-3).to_circuit()
+    batch = compiler.compile_batch([g, small], 1)
+    assert batch[0].hyperedges() == port.compile(g, 1)[0]
+    assert batch[1].hyperedges() == port.compile(small, 1)[0]
