@@ -116,6 +116,34 @@ class Clocks:
                 "reasons": reasons, "samples": len(rows)}
 
 
+def shard(rank: int, world: int, per_rank: int) -> range:
+    """Branch ids owned by a rank (weak scaling: every rank owns per_rank)."""
+    return range(rank * per_rank, (rank + 1) * per_rank)
+
+
+def gather_flat(dist, arrays: dict, device: str):
+    """Gathers variable-length flat DEM arrays (per-rank tables) to every rank
+    with two all_gathers per array (sizes, then padded payloads): the final
+    exchange step of SURVEY.md 8e. Returns {name: [per-rank np.ndarray]}."""
+    import numpy as np
+    import torch
+    out = {}
+    for name, a in arrays.items():
+        a = np.ascontiguousarray(a)
+        as_i64 = a.dtype in (np.uint32, np.uint64, np.int32)
+        t = torch.from_numpy(a.astype(np.int64) if as_i64 else a.astype(np.float64)).to(device)
+        n = torch.tensor([t.numel()], dtype=torch.int64, device=device)
+        sizes = [torch.zeros_like(n) for _ in range(dist.ws)]
+        dist.td.all_gather(sizes, n)
+        mx = int(max(int(x.item()) for x in sizes))
+        pad = torch.zeros(mx, dtype=t.dtype, device=device)
+        pad[:t.numel()] = t
+        parts = [torch.zeros_like(pad) for _ in range(dist.ws)]
+        dist.td.all_gather(parts, pad)
+        out[name] = [parts[r][:int(sizes[r].item())].cpu().numpy().astype(a.dtype) for r in range(dist.ws)]
+    return out
+
+
 def build_branches(first: int, count: int):
     import paper_2604_16613_b200 as gp
     return [gp.gen_bb72_branch(first + b) for b in range(count)]
@@ -230,7 +258,7 @@ def run_gpu(args, dist):
     compiler = gp.Compiler(device)
     B = args.branches
     t_gen = time.time()
-    circuits = build_branches(rank * B, B)
+    circuits = build_branches(shard(rank, ws, B).start, B)
     views = views_of(circuits)
     gen_s = time.time() - t_gen
 
@@ -272,6 +300,22 @@ def run_gpu(args, dist):
     e2e_s = dist.max(t1 - t0)
     e2e_value = total_edges * args.steps / e2e_s
 
+    # --- optional final gather of per-rank DEM tables over NCCL -------------
+    gather = None
+    if ws > 1:
+        from paper_2604_16613_b200 import _native as N
+        E_ = int(out.num_edges)
+        doff_ = N.copy_u64(out.det_offsets, E_ + 1)
+        arrays = {"edge_offsets": N.copy_u64(out.edge_offsets, len(circuits) + 1), "det_offsets": doff_,
+                  "det_ids": N.copy_u32(out.det_ids, int(doff_[-1])), "probs": N.copy_f64(out.probs, E_)}
+        dist.barrier()
+        g0 = time.perf_counter()
+        got = gather_flat(dist, arrays, f"cuda:{device}")
+        dist.barrier()
+        gather = {"ms": dist.max(time.perf_counter() - g0) * 1e3,
+                  "bytes": int(sum(sum(x.nbytes for x in v) for v in got.values())),
+                  "edges": int(sum(len(x) for x in got["probs"]))}
+
     # --- roofline of the dominant kernel ------------------------------------
     from paper_2604_16613_b200 import _native as N
     E = int(out.num_edges)
@@ -312,6 +356,7 @@ def run_gpu(args, dist):
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "ms_per_step": e2e_s / args.steps * 1e3, "breakdown": e2e_parts},
         "gpu_launches": launches_per_step * args.steps,
+        "gather": gather,
         "roofline": roofline,
         "clocks": clk,
     }
