@@ -38,7 +38,7 @@ def _stale() -> bool:
     if not LIB.exists():
         return True
     t = LIB.stat().st_mtime
-    deps = [CSRC / s for s in CU_SOURCES + CPP_SOURCES + HEADERS]
+    deps = [CSRC / s for s in CU_SOURCES + CPP_SOURCES + HEADERS] + list(CSRC.glob("*.cuh"))
     deps += list((ROOT / "include").rglob("*.h*"))
     return any(p.stat().st_mtime > t for p in deps if p.exists())
 

@@ -13,6 +13,7 @@
 #include <thread>
 #include <charconv>
 #include <chrono>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <string>
@@ -73,6 +74,7 @@ struct gp_ctx {
     cudaEvent_t prof[gp::kProfCount] = {};
     uint64_t prof_ns[gp::kProfCount] = {};
     uint8_t *d_flush = nullptr;
+    uint64_t *d_dbg = nullptr;  // experiments only (option 99, bit 2)
 };
 
 namespace {
@@ -271,8 +273,8 @@ gp_status plan_batch(gp_ctx *ctx, const gp_circuit_view *cs, size_t C, uint8_t l
         t.obss += m.O;
         t.tiles += m.W;
         t.sources += k.src_noise + m.M;
-        t.ell += m.l ? (uint64_t)(m.l - 1) * 2 * m.n : 0;
-        t.leaf += (uint64_t)m.W * m.M;
+        t.ell += m.l ? (uint64_t)(m.l - 1) * gp::ell_stride(m.n) : 0;
+        t.leaf += (uint64_t)m.W * gp::leaf_stride(m.M);
         t.buckets += (uint64_t)m.D + 1;
     }
     if (t.sources >= 0xFFFFFFFFull || t.tiles >= 0xFFFFFFFFull || t.gates >= 0xFFFFFFFFull ||
@@ -432,7 +434,7 @@ struct WsPlan {
 };
 
 size_t carve(gp_ctx *ctx, DevPlan &p, const BatchTotals &t, uint8_t *base, uint32_t K, uint64_t ids_cap,
-             uint64_t pool_chunks) {
+             uint64_t pool_chunks, uint64_t slabs) {
     const uint64_t S = t.sources;
     uint64_t cap = 1024;
     while (cap < S + S / 2 + 16) cap <<= 1;
@@ -443,7 +445,7 @@ size_t carve(gp_ctx *ctx, DevPlan &p, const BatchTotals &t, uint8_t *base, uint3
         o = (size_t)align16(o + bytes + 16);
         return base ? base + at : nullptr;
     };
-    p.ell = (uint64_t *)take(t.ell * 8);
+    p.ell = (uint32_t *)take(t.ell * 4);
     p.leaf = (uint64_t *)take(t.leaf * 8);
     p.prob = (double *)take(S * 8);
     p.nsrc = (uint32_t *)take(t.noise * 4 + 16);
@@ -453,6 +455,10 @@ size_t carve(gp_ctx *ctx, DevPlan &p, const BatchTotals &t, uint8_t *base, uint3
     p.K = K;
     p.pool = (uint4 *)take(pool_chunks * gp::kPoolChunk * 16);
     p.pool_chunks_cap = (uint32_t)pool_chunks;
+    p.slab_words = (2 * t.max_n + 1) & ~1u;
+    p.slab_stride = slabs ? t.max_l : 0;
+    p.slab = (uint64_t *)take(slabs * p.slab_words * 8);
+    p.slab_hdr = (uint4 *)take(slabs * 16);
     p.rep = (uint32_t *)take(S * 4);
     p.gcnt = (uint32_t *)take(S * 4 + 4);
     p.ecnt = (uint2 *)take(S * 8);
@@ -599,9 +605,11 @@ gp_status run_batch(gp_ctx *ctx, const gp_circuit_view *cs, size_t count, uint8_
     uint32_t K = tcfg.direct ? std::max<uint32_t>(ctx->record_slots, tcfg.T) : ctx->record_slots;
     // Multi-CTA circuits (one word per CTA) emit through the record pool.
     uint64_t pool = 0;
-    if (!tcfg.direct)
+    if (!tcfg.direct && !tcfg.split)
         pool = std::max<uint64_t>(ctx->pool_hint,
                                   (2 * t.sources) / gp::kPoolChunk + t.groups * tcfg.emit_warps + 16);
+    // Split traversal: walker CTA g owns max_l slabs (one per boundary it may walk).
+    const uint64_t slabs = tcfg.split ? t.groups * t.max_l : 0;
     uint64_t ids_cap = std::max<uint64_t>(ctx->ids_hint, 3 * t.sources + 1024);
     DevPlan p{};
     int launches = 0;
@@ -613,9 +621,14 @@ gp_status run_batch(gp_ctx *ctx, const gp_circuit_view *cs, size_t count, uint8_
         p.trav = tcfg;
         p.trav.debug = ctx->trav_debug;
         p.trav_smem = tsmem;
-        const size_t need = carve(ctx, p, t, nullptr, K, ids_cap, pool);
+        const size_t need = carve(ctx, p, t, nullptr, K, ids_cap, pool, slabs);
         if ((st = ensure_device(ctx, &ctx->d_ws, &ctx->d_ws_cap, need)) != GP_OK) return st;
-        carve(ctx, p, t, ctx->d_ws, K, ids_cap, pool);
+        carve(ctx, p, t, ctx->d_ws, K, ids_cap, pool, slabs);
+        if (ctx->trav_debug & 4) {  // experiments: per-step walk timestamps of every CTA
+            if (!ctx->d_dbg) cudaMalloc(&ctx->d_dbg, (size_t)8192 * 512 * 4 * 8);
+            cudaMemsetAsync(ctx->d_dbg, 0, (size_t)8192 * 512 * 4 * 8, ctx->stream);
+            p.dbg = t.groups <= 8192 ? ctx->d_dbg : nullptr;
+        }
         launches += gp::enqueue_pipeline(p, ctx->stream, &ctx->stage_ev, nullptr, &e);
         if (e != cudaSuccess) return cuda_fail(ctx, e, "kernel launch");
         e = cudaMemcpyAsync(ctx->h_hdr, p.hdr, sizeof(DeviceHeader), cudaMemcpyDeviceToHost, ctx->stream);
@@ -644,6 +657,16 @@ gp_status run_batch(gp_ctx *ctx, const gp_circuit_view *cs, size_t count, uint8_
     }
     ctx->last_plan = p;
     ctx->has_plan = true;
+    if (p.dbg) {
+        const char *path = std::getenv("GP_DEBUG_DUMP");
+        std::vector<uint64_t> h((size_t)t.groups * 512 * 4);
+        cudaMemcpy(h.data(), p.dbg, h.size() * 8, cudaMemcpyDeviceToHost);
+        if (path)
+            if (FILE *f = std::fopen(path, "wb")) {
+                std::fwrite(h.data(), 8, h.size(), f);
+                std::fclose(f);
+            }
+    }
     const uint64_t E = hdr.num_edges, nd = hdr.num_det_ids, no = hdr.num_obs_ids;
     size_t o = 0;
     auto take = [&](size_t bytes) {
@@ -831,7 +854,7 @@ gp_status gp_replay(gp_ctx *ctx, uint32_t iterations, int flush_l2, gp_stats *st
         for (int k = 1; k < gp::kProfCount; k++)
             ctx->prof_ns[k] += (uint64_t)(elapsed_ms(ctx->prof[k - 1], ctx->prof[k]) * 1e6);
         total += (uint64_t)(elapsed_ms(ctx->prof[0], ctx->prof[gp::kProfCount - 1]) * 1e6);
-        trav += (uint64_t)(elapsed_ms(ctx->prof[gp::kProfLower], ctx->prof[gp::kProfTraverse]) * 1e6);
+        trav += (uint64_t)(elapsed_ms(ctx->prof[gp::kProfLower], ctx->prof[gp::kProfEmit]) * 1e6);
     }
     if (stats) {
         *stats = gp_stats{};

@@ -18,6 +18,9 @@ struct TravCfg {
     uint32_t node_warps, emit_warps;
     uint32_t max_n, max_layer_noise, max_layer_meas, max_l;
     uint32_t direct;     // every circuit fits one group: atomic-free emission
+    uint32_t split;      // walk_kernel + emit_kernel (one word per CTA) instead of traverse_kernel
+    uint32_t walk_threads, walk_npt;  // walk CTA size; base nodes per node thread (0: generic)
+    uint32_t G;          // boundaries per staged group (walk_kernel)
     uint32_t debug;      // experiments only: bit0 skip emission work, bit1 skip node work
 };
 
@@ -32,7 +35,7 @@ struct DevPlan {
     size_t trav_smem;
 
     // STEPG IR built on device.
-    uint64_t *ell;   // [tot.ell] base-slot ELLPACK
+    uint32_t *ell;   // [tot.ell] base-slot ELLPACK (node words, gp_layout.h)
     uint64_t *leaf;  // [tot.leaf] leaf rows, tile-major per circuit (Eq. 3)
 
     // Per source.
@@ -46,6 +49,12 @@ struct DevPlan {
     // bits) records in per-warp chunks; slot_kernel files them per source.
     uint4 *pool;          // [pool_chunks_cap * kPoolChunk] {src, word, bits lo, bits hi}
     uint32_t pool_chunks_cap;
+    // Split traversal: walker CTA g owns slabs [g * slab_stride, (g + 1) *
+    // slab_stride), one per walked boundary (2n u64 words), each with a
+    // header {circuit, word, boundary, state}.
+    uint64_t *slab;
+    uint4 *slab_hdr;
+    uint32_t slab_stride, slab_words;
     uint32_t *rep;     // [S] representative source (group key) or kSuccNone
     uint32_t *gcnt;    // [S] members per representative
     uint2 *ecnt;       // [S] (detector ids, observable ids) per representative
@@ -78,6 +87,7 @@ struct DevPlan {
     double *o_prob;                   // [S]
     uint64_t *o_edge_off;             // [C + 1]
     DeviceHeader *hdr;
+    uint64_t *dbg;  // experiments only (TravCfg.debug bit 2): per-step walk timestamps
 };
 
 struct StageEvents {
@@ -91,6 +101,7 @@ enum ProfStage {
     kProfMemset,
     kProfLower,
     kProfTraverse,
+    kProfEmit,
     kProfDedup,
     kProfScanSrc,
     kProfScatter,
@@ -102,7 +113,7 @@ enum ProfStage {
     kProfGather,
     kProfCount
 };
-constexpr const char *kProfNames[kProfCount] = {"start",   "memset",     "lower",          "traverse", "dedup",
+constexpr const char *kProfNames[kProfCount] = {"start",   "memset",     "lower",          "traverse", "emit", "dedup",
                                                 "scan_src", "scatter",   "finalize",       "scan_bucket",
                                                 "bucket_scatter", "rank", "scan_pos",      "gather"};
 

@@ -14,6 +14,9 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <algorithm>
+#include <cstdlib>
+
 #include "gp_device.h"
 
 namespace gp {
@@ -165,32 +168,32 @@ __global__ void lower_kernel(DevPlan p, uint32_t blocks_a) {
             const uint32_t q = lo & ((1u << kGateKindShift) - 1), kind = lo >> kGateKindShift;
             if (kind == 3 || kind == 4) p.prob[src_flip + hi] = flip[m.meas_base + hi];
             if (i == 0) continue;  // no boundary before layer 0
-            uint64_t *e = p.ell + m.ell_base + (uint64_t)(i - 1) * (2 * m.n);
+            uint32_t *e = p.ell + m.ell_base + (uint64_t)(i - 1) * ell_stride(m.n);
             const uint32_t x = 2 * q, z = 2 * q + 1;
             switch (kind) {
                 case 0:  // H: X <-> Z
-                    e[x] = (uint64_t)kSuccNone << 32 | z;
-                    e[z] = (uint64_t)kSuccNone << 32 | x;
+                    e[x] = kSuccNotSelf | kSuccOther | z;
+                    e[z] = kSuccNotSelf | kSuccOther | x;
                     break;
-                case 1: {  // CX q -> hi: X_c -> {X_c, X_t}, Z_c -> Z_c, X_t -> X_t, Z_t -> {Z_c, Z_t}
+                case 1: {  // CX q -> hi: X_c -> {X_c, X_t}, Z_c -> Z_c, X_t -> X_t, Z_t -> {Z_t, Z_c}
                     const uint32_t xt = 2 * hi, zt = 2 * hi + 1;
-                    e[x] = (uint64_t)xt << 32 | x;
-                    e[z] = (uint64_t)kSuccNone << 32 | z;
-                    e[xt] = (uint64_t)kSuccNone << 32 | xt;
-                    e[zt] = (uint64_t)zt << 32 | z;
+                    e[x] = kSuccOther | xt;
+                    e[z] = kEllIdle;
+                    e[xt] = kEllIdle;
+                    e[zt] = kSuccOther | z;
                     break;
                 }
                 case 2:  // R
-                    e[x] = kEllDead;
-                    e[z] = kEllDead;
+                    e[x] = kSuccNone;
+                    e[z] = kSuccNone;
                     break;
                 case 3:  // M: X -> {leaf, X}, Z -> none
-                    e[x] = (uint64_t)x << 32 | (kSuccLeaf | hi);
-                    e[z] = kEllDead;
+                    e[x] = kSuccOther | kSuccLeaf | hi;
+                    e[z] = kSuccNone;
                     break;
                 default:  // MR: X -> {leaf}, Z -> none
-                    e[x] = (uint64_t)kSuccNone << 32 | (kSuccLeaf | hi);
-                    e[z] = kEllDead;
+                    e[x] = kSuccNotSelf | kSuccOther | kSuccLeaf | hi;
+                    e[z] = kSuccNone;
                     break;
             }
         }
@@ -232,7 +235,7 @@ __global__ void lower_kernel(DevPlan p, uint32_t blocks_a) {
         const uint32_t d = (uint32_t)t - arr<uint32_t>(p, p.lay.circ_det)[c];
         const uint32_t *off = arr<uint32_t>(p, p.lay.det_off) + m.det_base;
         const uint32_t *ms = arr<uint32_t>(p, p.lay.det_meas);
-        uint64_t *row = p.leaf + m.leaf_base + (uint64_t)(d >> 6) * m.M;
+        uint64_t *row = p.leaf + m.leaf_base + (uint64_t)(d >> 6) * leaf_stride(m.M);
         for (uint32_t k = off[d]; k < off[d + 1]; k++)
             atomicXor((unsigned long long *)&row[ms[k]], 1ull << (d & 63));
     } else if (t < p.tot.dets + p.tot.obss) {
@@ -243,7 +246,7 @@ __global__ void lower_kernel(DevPlan p, uint32_t blocks_a) {
         const uint32_t b = m.D + o;
         const uint32_t *off = arr<uint32_t>(p, p.lay.obs_off) + m.obs_base;
         const uint32_t *ms = arr<uint32_t>(p, p.lay.obs_meas);
-        uint64_t *row = p.leaf + m.leaf_base + (uint64_t)(b >> 6) * m.M;
+        uint64_t *row = p.leaf + m.leaf_base + (uint64_t)(b >> 6) * leaf_stride(m.M);
         for (uint32_t k = off[o]; k < off[o + 1]; k++)
             atomicXor((unsigned long long *)&row[ms[k]], 1ull << (b & 63));
     }
@@ -252,6 +255,7 @@ __global__ void lower_kernel(DevPlan p, uint32_t blocks_a) {
 // ---------------------------------------------------------------- K2 traversal
 }  // namespace
 #include "gp_traverse.cuh"
+#include "gp_walk.cuh"
 namespace {
 
 // Files the traversal's pooled records into per-source slots: the returning
@@ -662,6 +666,32 @@ void launch_scan(F f, uint64_t n, uint4 *bsum, uint4 *out, uint4 *total, cudaStr
 
 uint32_t blocks_for(uint64_t n, uint32_t tpb) { return (uint32_t)((n + tpb - 1) / tpb); }
 
+constexpr uint32_t kWalkNpl = 4;  // target nodes per walk thread (issue-bound: more warps)
+
+template <int WPC, class F>
+void walk_dispatch_npl(uint32_t npl, F &&launch) {
+    switch (npl) {
+        case 2: launch(walk::walk_kernel<WPC, 2>); break;
+        case 4: launch(walk::walk_kernel<WPC, 4>); break;
+        case 8: launch(walk::walk_kernel<WPC, 8>); break;
+        case 16: if constexpr (WPC <= 16) { launch(walk::walk_kernel<WPC, 16>); break; } [[fallthrough]];
+        default: launch(walk::walk_kernel<WPC, 0>); break;
+    }
+}
+
+template <class F>
+void walk_dispatch(uint32_t wpc, uint32_t npl, F &&launch) {
+    switch (wpc) {
+        case 1: walk_dispatch_npl<1>(npl, launch); break;
+        case 2: walk_dispatch_npl<2>(npl, launch); break;
+        case 4: walk_dispatch_npl<4>(npl, launch); break;
+        case 8: walk_dispatch_npl<8>(npl, launch); break;
+        case 16: walk_dispatch_npl<16>(npl, launch); break;
+        default: walk_dispatch_npl<32>(npl, launch); break;
+    }
+}
+constexpr uint32_t kEmitBlocks = 148 * 8;
+
 }  // namespace
 
 bool plan_traversal(const BatchTotals &t, int device, TravCfg *cfg, size_t *smem) {
@@ -685,6 +715,34 @@ bool plan_traversal(const BatchTotals &t, int device, TravCfg *cfg, size_t *smem
     // (the copy latency of a boundary's stage hides behind NST-1 boundaries).
     static const uint32_t kBatch[][2] = {{3, 3}, {2, 3}, {2, 2}};
     static const uint32_t kSingle[][2] = {{6, 8}, {4, 8}, {4, 6}, {4, 4}, {3, 3}, {2, 2}};
+    if (T == 1) {  // split traversal: walk_kernel + emit_kernel
+        c.T = 1;
+        c.direct = t.max_W <= 1;
+        c.split = 1;
+        // Threads per column (a power-of-two number of warps) and unrolled
+        // nodes per thread: the fewest warps with <= kWalkNpl nodes each (one
+        // warp needs no CTA barrier at all); GP_WALK_WPC overrides (tuning).
+        uint32_t wpc = 1;
+        while (wpc < 32 && n2 > wpc * 32 * kWalkNpl) wpc *= 2;
+        if (const char *o = std::getenv("GP_WALK_WPC")) wpc = std::max(1, std::min(32, std::atoi(o)));
+        c.walk_threads = 32 * wpc;
+        const uint32_t npl = (n2 + c.walk_threads - 1) / c.walk_threads;
+        c.walk_npt = npl <= 2 ? 2 : npl <= 4 ? 4 : npl <= 8 ? 8 : npl <= 16 ? 16 : 0;
+        // Deepest staging that fits: groups of G boundaries, NST groups in flight.
+        static const uint32_t kOpts[][2] = {{3, 8}, {2, 8}, {3, 4}, {2, 4}, {2, 2}, {2, 1}};
+        for (const auto &o : kOpts) {
+            const walk::WalkDims d(o[0], o[1], t.max_n, t.max_layer_meas, t.max_l);
+            if (d.total_bytes() <= budget) {
+                c.NST = o[0];
+                c.G = o[1];
+                c.R = 2;
+                *cfg = c;
+                *smem = d.total_bytes();
+                return true;
+            }
+        }
+        return false;
+    }
     for (;; T = (T + 1) / 2) {
         const bool batch = T > 1;
         const uint32_t(*opts)[2] = batch ? kBatch : kSingle;
@@ -715,7 +773,7 @@ int enqueue_pipeline(const DevPlan &p, cudaStream_t st, const StageEvents *ev, c
     mark(kProfStart);
     const uint64_t S = p.tot.sources;
     // Zero / sentinel fills.
-    if (p.tot.ell) cudaMemsetAsync(p.ell, 0, p.tot.ell * 8, st);
+    if (p.tot.ell) cudaMemsetAsync(p.ell, 0, p.tot.ell * 4, st);
     if (p.tot.leaf) cudaMemsetAsync(p.leaf, 0, p.tot.leaf * 8, st);
     cudaMemsetAsync(p.cnt, 0, S * 4 + 4, st);
     cudaMemsetAsync(p.gcnt, 0, S * 4 + 4, st);
@@ -735,7 +793,16 @@ int enqueue_pipeline(const DevPlan &p, cudaStream_t st, const StageEvents *ev, c
     if (ev) cudaEventRecord(ev->lowered, st);
 
     // K2 traversal.
-    if (p.tot.groups) {
+    if (p.tot.groups && p.trav.split) {
+        auto launch = [&](auto kern) {
+            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.trav_smem);
+            kern<<<(uint32_t)p.tot.groups, p.trav.walk_threads, p.trav_smem, st>>>(p, p.trav);
+        };
+        walk_dispatch(p.trav.walk_threads / 32, p.trav.walk_npt, launch);
+        mark(kProfTraverse);
+        walk::emit_kernel<<<kEmitBlocks, 256, 0, st>>>(p);
+        launches += 2;
+    } else if (p.tot.groups) {
         const TravCfg &c = p.trav;
         const int threads = 32 * (1 + (int)c.node_warps + (int)c.emit_warps);
         const uint32_t tm = c.T <= 1 ? 1 : c.T <= 2 ? 2 : c.T <= 4 ? 4 : 8;
@@ -753,7 +820,8 @@ int enqueue_pipeline(const DevPlan &p, cudaStream_t st, const StageEvents *ev, c
             launches++;
         }
     }
-    mark(kProfTraverse);
+    if (!p.trav.split) mark(kProfTraverse);
+    mark(kProfEmit);
     if (ev) cudaEventRecord(ev->traversed, st);
 
     // K3..K9 reduce.

@@ -15,16 +15,29 @@
 
 namespace gp {
 
-// Successor encoding of the base-slot STEPG ELLPACK (one u64 per base node,
-// lo = first successor, hi = second; the reference's packing, stepg.hpp:85-91).
+// Successor encoding of the base-slot STEPG ELLPACK: one u32 per base node.
+// Every node of the reference's STEPG has at most two successors through the
+// next layer (stepg.cpp:196-234), and one of them, when there are two, is the
+// node's own slot at the next boundary (CX: X_c -> {X_c, X_t}, Z_t -> {Z_t,
+// Z_c}; M: X -> {leaf, X}). So a node word holds a "self" flag and at most one
+// "other" successor -- a base slot at the next boundary or a leaf:
+//   bit 31  NOT self (the word 0 is the idle node: X -> X, Z -> Z)
+//   bit 30  has other
+//   bit 29  other is a leaf (local measurement index) rather than a base slot
+//   bits 0-28 the other successor's index
 // Only the 2n base slots are materialised: every correlated slot of the
 // reference (Y, XZ, ZX, XY, YX, YY, YZ, ZY; stepg.cpp:236-254) is the XOR of
 // same-boundary base rows, so sources are expanded onto base rows instead
 // (bit-identical; pinned by test_eec.cpp:84-99 and by our oracle parity).
-constexpr uint32_t kSuccNone = 0xFFFFFFFFu;      // kNoSuccessor (stepg.hpp:52)
-constexpr uint32_t kSuccLeaf = 0x80000000u;      // | local measurement index
-constexpr uint64_t kEllIdle = 0;                 // whole word 0: idle qubit, X->X / Z->Z
-constexpr uint64_t kEllDead = 0xFFFFFFFFFFFFFFFFull;  // R / Z into M: no successor
+constexpr uint32_t kSuccNotSelf = 1u << 31;
+constexpr uint32_t kSuccOther = 1u << 30;
+constexpr uint32_t kSuccLeaf = 1u << 29;
+constexpr uint32_t kSuccIdx = kSuccLeaf - 1;
+constexpr uint32_t kSuccNone = kSuccNotSelf;  // R / Z into M: no successor
+constexpr uint32_t kEllIdle = 0;
+// ELLPACK rows (one boundary) are padded to a multiple of 4 words so every
+// row is a 16-byte-aligned bulk-copy unit.
+__host__ __device__ inline uint32_t ell_stride(uint32_t n) { return (2 * n + 3) & ~3u; }
 
 // Gate word: lo = q0 | kind << 29, hi = q1 (CX) or local measurement index.
 constexpr uint32_t kGateKindShift = 29;
@@ -52,11 +65,17 @@ struct CircuitMeta {
     uint32_t bucket_base;  // canonical-order buckets (D + 1 per circuit)
     uint32_t max_layer_noise;  // max noise ops in one layer
     uint64_t src_base;     // global id of source 0
-    uint64_t ell_base;     // ELLPACK index of (boundary 0, slot 0); (l - 1) * 2n entries
+    uint64_t ell_base;     // ELLPACK index of (boundary 0, slot 0); (l - 1) * ell_stride(n) entries
     uint64_t leaf_base;    // leaf matrix index of (tile 0, meas 0); W * M entries, tile-major
     // Host-side packing bases (global element indices of this circuit's slices).
     uint64_t gate_base, noise_base, det_entry_base, obs_entry_base, circ_layer_base;
 };
+
+// Leaf rows (one per 64-bit detector word, tile-major) are padded to an even
+// length so every row starts 16-byte aligned: a layer's leaf words staged by
+// a 16-byte-granular bulk copy then start at local measurement (mb & ~1), and
+// the ELLPACK stores leaf successors relative to that start (lower_kernel).
+__host__ __device__ inline uint32_t leaf_stride(uint32_t M) { return (M + 1) & ~1u; }
 
 // Offsets (bytes) of every array inside one staging image.
 struct StageLayout {
@@ -95,7 +114,7 @@ struct BatchTotals {
     uint64_t groups;      // traversal CTAs: sum ceil(W / T)
     uint32_t max_W;
     uint64_t sources;
-    uint64_t ell;         // sum (l - 1) * 2n
+    uint64_t ell;         // sum (l - 1) * ell_stride(n)
     uint64_t leaf;        // sum W * M
     uint64_t buckets;     // sum (D + 1)
     uint32_t max_n;       // max qubits

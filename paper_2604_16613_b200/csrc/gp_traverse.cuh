@@ -49,14 +49,14 @@ struct Dims {
           R(r),
           NST(nst),
           n2(2 * max_n),
-          ell_w(2 * max_n),
+          ell_w(ell_stride(max_n)),
           leaf_w((max_meas + 3) & ~1u),
           noise_w((max_noise + 3) & ~1u),
           src_w((max_noise + 9) & ~3u),
           lay_w((max_l + 4) & ~3u) {}
     __host__ __device__ size_t ring_bytes() const { return (size_t)R * T * n2 * 8; }
     __host__ __device__ size_t stage_bytes() const {
-        return sizeof(StageHdr) + ((size_t)ell_w + (size_t)T * leaf_w + noise_w) * 8 + (size_t)src_w * 4;
+        return sizeof(StageHdr) + (size_t)ell_w * 4 + ((size_t)T * leaf_w + noise_w) * 8 + (size_t)src_w * 4;
     }
     __host__ __device__ size_t total_bytes() const {
         return ring_bytes() + NST * stage_bytes() + (2 * NST + 2 * R) * 8 + (size_t)2 * lay_w * 4 + 64;
@@ -66,10 +66,12 @@ struct Dims {
     }
     __device__ uint8_t *stage(uint8_t *base, uint32_t k) const { return base + ring_bytes() + (size_t)k * stage_bytes(); }
     __device__ StageHdr *hdr(uint8_t *base, uint32_t k) const { return reinterpret_cast<StageHdr *>(stage(base, k)); }
-    __device__ uint64_t *ell(uint8_t *base, uint32_t k) const {
-        return reinterpret_cast<uint64_t *>(stage(base, k) + sizeof(StageHdr));
+    __device__ uint32_t *ell(uint8_t *base, uint32_t k) const {
+        return reinterpret_cast<uint32_t *>(stage(base, k) + sizeof(StageHdr));
     }
-    __device__ uint64_t *leaf(uint8_t *base, uint32_t k) const { return ell(base, k) + ell_w; }
+    __device__ uint64_t *leaf(uint8_t *base, uint32_t k) const {
+        return reinterpret_cast<uint64_t *>(ell(base, k) + ell_w);
+    }
     __device__ uint64_t *noise(uint8_t *base, uint32_t k) const { return leaf(base, k) + (size_t)T * leaf_w; }
     __device__ uint32_t *src(uint8_t *base, uint32_t k) const {
         return reinterpret_cast<uint32_t *>(noise(base, k) + noise_w);
@@ -294,7 +296,8 @@ __global__ void __launch_bounds__(800, 1) traverse_kernel(DevPlan p, TravCfg cfg
     }
     __syncthreads();
 
-    const uint64_t *ell = p.ell + m.ell_base;
+    const uint32_t *ell = p.ell + m.ell_base;
+    const uint32_t estride = ell_stride(m.n);
     const uint64_t *noise = arr<uint64_t>(p, p.lay.noise);
     const uint32_t *nsrc = p.nsrc;
 
@@ -323,11 +326,11 @@ __global__ void __launch_bounds__(800, 1) traverse_kernel(DevPlan p, TravCfg cfg
                 h->n1 = n1;
                 h->noise_shift = (uint32_t)(((uint64_t)(noise + n0) & 15ull) >> 3);
                 h->src_shift = (uint32_t)(((uint64_t)(nsrc + n0) & 15ull) >> 2);
-                uint32_t bytes = n2 * 8;
+                uint32_t bytes = estride * 4;
                 uint32_t leaf_b[8] = {};
                 uint64_t leaf_a[8] = {};
                 for (uint32_t w = 0; w < tw; w++) {
-                    const uint64_t *row = leaf + (uint64_t)(t0 + w) * m.M;
+                    const uint64_t *row = leaf + (uint64_t)(t0 + w) * leaf_stride(m.M);
                     leaf_a[w] = (uint64_t)(row + mb) & ~15ull;
                     h->leaf_shift[w] = (uint32_t)(((uint64_t)(row + mb) & 15ull) >> 3);
                     leaf_b[w] = me > mb ? (uint32_t)((((uint64_t)(row + me) + 15) & ~15ull) - leaf_a[w]) : 0;
@@ -337,7 +340,7 @@ __global__ void __launch_bounds__(800, 1) traverse_kernel(DevPlan p, TravCfg cfg
                 bytes += nb + sb;
                 fence_proxy_async();
                 mbar_arrive_expect_tx(&stage_full[k], bytes);
-                bulk_g2s(L.ell(smem, k), ell + (uint64_t)b * n2, n2 * 8, &stage_full[k]);
+                bulk_g2s(L.ell(smem, k), ell + (uint64_t)b * estride, estride * 4, &stage_full[k]);
                 for (uint32_t w = 0; w < tw; w++)
                     if (leaf_b[w]) bulk_g2s(L.leaf(smem, k) + (size_t)w * L.leaf_w, (const void *)leaf_a[w], leaf_b[w],
                                             &stage_full[k]);
@@ -357,31 +360,22 @@ __global__ void __launch_bounds__(800, 1) traverse_kernel(DevPlan p, TravCfg cfg
             if (j >= (int)L.R) mbar_wait(&state_empty[r], (uint32_t)(j / (int)L.R - 1) & 1u);
             mbar_wait(&stage_full[k], (uint32_t)(j / (int)L.NST) & 1u);
             const StageHdr *h = L.hdr(smem, k);
-            const uint64_t *s_ell = L.ell(smem, k);
+            const uint32_t *s_ell = L.ell(smem, k);
             const uint64_t *s_leaf = L.leaf(smem, k);
             const uint64_t *nxt = L.slot(smem, rp);
             uint64_t *now = L.slot(smem, r);
-            const uint32_t mb = h->mb;
-            uint32_t lsh[TM];
-#pragma unroll
-            for (int w = 0; w < TM; w++) lsh[w] = (uint32_t)w < tw ? h->leaf_shift[w] : 0;
+            const uint32_t mb_al = h->mb & ~1u;  // leaf rows are 16-byte aligned: the slice starts there
             bool any = false;
             for (uint32_t s = tn; s < ((cfg.debug & 2) ? 0 : n2); s += node_threads) {
-                const uint64_t e = s_ell[s];
-                const uint32_t v0 = (uint32_t)e, v1 = (uint32_t)(e >> 32);
+                const uint32_t e = s_ell[s];
+                const uint32_t idx = e & kSuccIdx;
 #pragma unroll
                 for (int w = 0; w < TM; w++) {
                     if ((uint32_t)w >= tw) break;
                     const uint64_t *nw = nxt + (size_t)w * n2;
-                    const uint64_t *lw = s_leaf + (size_t)w * L.leaf_w + lsh[w] - mb;
-                    uint64_t acc;
-                    if (e == kEllIdle) {
-                        acc = nw[s];
-                    } else {
-                        acc = 0;
-                        if (v0 != kSuccNone) acc ^= (v0 & kSuccLeaf) ? lw[v0 & ~kSuccLeaf] : nw[v0];
-                        if (v1 != kSuccNone) acc ^= (v1 & kSuccLeaf) ? lw[v1 & ~kSuccLeaf] : nw[v1];
-                    }
+                    const uint64_t *lw = s_leaf + (size_t)w * L.leaf_w - mb_al;
+                    uint64_t acc = (e & kSuccNotSelf) ? 0 : nw[s];
+                    if (e & kSuccOther) acc ^= (e & kSuccLeaf) ? lw[idx] : nw[idx];
                     now[(size_t)w * n2 + s] = acc;
                     any |= acc != 0;
                 }
@@ -406,7 +400,7 @@ __global__ void __launch_bounds__(800, 1) traverse_kernel(DevPlan p, TravCfg cfg
                 if (!(flip[mm] > 0)) continue;
                 uint64_t v[TM];
 #pragma unroll
-                for (int w = 0; w < TM; w++) v[w] = (uint32_t)w < tw ? leaf[(uint64_t)(t0 + w) * m.M + mm] : 0;
+                for (int w = 0; w < TM; w++) v[w] = (uint32_t)w < tw ? leaf[(uint64_t)(t0 + w) * leaf_stride(m.M) + mm] : 0;
                 emit_source<TM>(p, src_flip + mm, t0, tw, v, direct);
             }
         }
