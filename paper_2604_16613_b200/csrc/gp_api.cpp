@@ -22,23 +22,13 @@
 #include "../../include/greenpeas.h"
 #include "gp_device.h"
 #include "gp_layout.h"
+#include "gp_pack.h"
 
 using gp::BatchTotals;
 using gp::CircuitMeta;
 using gp::DevPlan;
 using gp::DeviceHeader;
 using gp::StageLayout;
-
-// Per-circuit counts of pass 1 (independent across circuits).
-struct CircCount {
-    int err;  // 0 ok, 1 index space, 2 detector leaf, 3 observable leaf, 4 too wide
-    uint32_t src_noise, max_noise, max_meas;
-    uint64_t gates, noise, det_entries, obs_entries;
-    std::vector<double> probs;  // distinct noise probabilities (<= kLocalProbs, else many)
-    std::vector<uint32_t> pidx; // global table index of each local probability
-    bool many;
-};
-constexpr size_t kLocalProbs = 64;
 
 struct gp_ctx {
     int device = 0;
@@ -49,6 +39,7 @@ struct gp_ctx {
     uint32_t record_slots = 8;
     uint64_t ids_hint = 0;  // learned id capacity (grows on overflow)
     uint64_t pool_hint = 0; // learned record-pool chunks (grows on overflow)
+    uint64_t items_hint = 0; // learned reduce item capacity (grows on overflow)
 
     uint8_t *h_stage = nullptr;
     size_t h_stage_cap = 0;
@@ -63,10 +54,9 @@ struct gp_ctx {
     cudaEvent_t ev_start = nullptr, ev_h2d = nullptr, ev_end = nullptr;
     gp::StageEvents stage_ev{};
 
-    std::vector<CircuitMeta> metas;
+    gp::PackPlan pack;
+    std::unique_ptr<gp::HostPool> pool;  // created on the first large job
     std::vector<uint32_t> out_ndet, out_nobs;
-    std::vector<double> prob_table;
-    std::vector<CircCount> circ_counts;
 
     // Last successful device plan (for gp_replay) and profiling state.
     bool has_plan = false;
@@ -96,331 +86,11 @@ gp_status cuda_fail(gp_ctx *ctx, cudaError_t e, const char *what) {
     return fail(ctx, GP_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
 }
 
-uint32_t alpha_of(uint8_t level) { return level == 0 ? 2 : level == 1 ? 4 : 7; }  // stepg.cpp:23-33
 
 uint32_t components(uint8_t kind, uint8_t level) {  // stepg.cpp:66-103
     if (kind <= GP_NOISE_Z_ERROR) return 1;
     if (kind == GP_NOISE_DEPOLARIZE1) return level == 0 ? 2 : 3;
     return level == 0 ? 6 : level == 1 ? 10 : 15;
-}
-
-// Runs f(i) for i in [0, n) on up to hardware_concurrency host threads
-// (inline for small n: single-circuit latency pays no thread start-up).
-template <class F>
-void parallel_for(size_t n, F f) {
-    const size_t hw = std::max<unsigned>(1, std::thread::hardware_concurrency());
-    const size_t nt = std::min(hw, n / 32);
-    if (nt <= 1) {
-        for (size_t i = 0; i < n; i++) f(i);
-        return;
-    }
-    std::atomic<size_t> next{0};
-    auto work = [&] {
-        for (size_t i0; (i0 = next.fetch_add(16)) < n;)
-            for (size_t i = i0; i < std::min(n, i0 + 16); i++) f(i);
-    };
-    std::vector<std::thread> pool;
-    for (size_t t = 1; t < nt; t++) pool.emplace_back(work);
-    work();
-    for (auto &th : pool) th.join();
-}
-
-
-
-// Pass 1: validation (the reference's exceptions, in the reference's order;
-// for a batch, the first failing circuit), device-encoding limits, totals and
-// per-circuit metadata. Counting runs in parallel over circuits.
-gp_status plan_batch(gp_ctx *ctx, const gp_circuit_view *cs, size_t C, uint8_t level, BatchTotals &t,
-                     std::vector<CircuitMeta> &metas) {
-    t = BatchTotals{};
-    t.C = (uint32_t)C;
-    t.level = level;
-    metas.assign(C, CircuitMeta{});
-    std::vector<CircCount> cc(C);
-    parallel_for(C, [&](size_t c) {
-        const gp_circuit_view &v = cs[c];
-        CircCount &k = cc[c];
-        k = CircCount{};
-        const uint64_t rows = (uint64_t)v.num_layers * alpha_of(level) * v.num_qubits + v.num_measurements;
-        if (rows >= 0xFFFFFFFFull) {  // lower(), stepg.cpp:171-174
-            k.err = 1;
-            return;
-        }
-        for (uint32_t d = 0; d < v.num_detectors; d++)  // init_leaves, eec.cpp:42-49
-            for (uint32_t x = v.det_offsets[d]; x < v.det_offsets[d + 1]; x++)
-                if (v.det_meas[x] >= v.num_measurements) {
-                    k.err = 2;
-                    return;
-                }
-        for (uint32_t o = 0; o < v.num_observables; o++)  // eec.cpp:50-57
-            for (uint32_t x = v.obs_offsets[o]; x < v.obs_offsets[o + 1]; x++)
-                if (v.obs_meas[x] >= v.num_measurements) {
-                    k.err = 3;
-                    return;
-                }
-        if (v.num_qubits >= (1u << gp::kNoiseQubitBits) || v.num_measurements >= 0x7FFFFFFFu) {
-            k.err = 4;
-            return;
-        }
-        uint64_t src = 0;
-        for (uint32_t i = 0; i < v.num_layers; i++) {
-            const uint32_t n0 = v.noise_offsets[i], n1 = v.noise_offsets[i + 1];
-            k.max_noise = std::max(k.max_noise, n1 - n0);
-            for (uint32_t o = n0; o < n1; o++) {
-                src += components(v.noise_kind[o], level);
-                if (k.many) continue;
-                const double pr = v.noise_prob[o];
-                bool seen = false;
-                for (double q : k.probs) seen |= std::memcmp(&q, &pr, 8) == 0;
-                if (!seen) {
-                    if (k.probs.size() == kLocalProbs) k.many = true;
-                    else k.probs.push_back(pr);
-                }
-            }
-            uint32_t meas = 0;
-            for (uint32_t g = v.gate_offsets[i]; g < v.gate_offsets[i + 1]; g++)
-                meas += v.gate_kind[g] == GP_GATE_M || v.gate_kind[g] == GP_GATE_MR;
-            k.max_meas = std::max(k.max_meas, meas);
-        }
-        k.src_noise = (uint32_t)src;
-        k.gates = v.gate_offsets[v.num_layers] - v.gate_offsets[0];
-        k.noise = v.noise_offsets[v.num_layers] - v.noise_offsets[0];
-        k.det_entries = v.det_offsets[v.num_detectors] - v.det_offsets[0];
-        k.obs_entries = v.obs_offsets[v.num_observables] - v.obs_offsets[0];
-    });
-    // Batch probability table (bit-exact keys); wide mode if it would not fit.
-    {
-        std::vector<uint64_t> keys;
-        bool many = false;
-        for (const CircCount &k : cc) {
-            many |= k.many;
-            for (double q : k.probs) {
-                uint64_t b;
-                std::memcpy(&b, &q, 8);
-                keys.push_back(b);
-            }
-        }
-        std::sort(keys.begin(), keys.end());
-        keys.erase(std::unique(keys.begin(), keys.end()), keys.end());
-        t.wide_prob = many || keys.size() > gp::kNoisePidxMax;
-        ctx->prob_table.clear();
-        if (!t.wide_prob) {
-            for (uint64_t b : keys) {
-                double q;
-                std::memcpy(&q, &b, 8);
-                ctx->prob_table.push_back(q);
-            }
-            for (CircCount &k : cc) {
-                k.pidx.clear();
-                for (double q : k.probs) {
-                    uint64_t b;
-                    std::memcpy(&b, &q, 8);
-                    k.pidx.push_back((uint32_t)(std::lower_bound(keys.begin(), keys.end(), b) - keys.begin()));
-                }
-            }
-        }
-        t.prob_table_n = (uint32_t)ctx->prob_table.size();
-        ctx->circ_counts = std::move(cc);
-    }
-    std::vector<CircCount> &cc2 = ctx->circ_counts;
-    static const char *kErr[] = {"", "circuit exceeds 32-bit node index space",
-                                 "detector references a measurement without a leaf",
-                                 "observable references a measurement without a leaf",
-                                 "circuit too wide for the device encoding"};
-    for (size_t c = 0; c < C; c++)
-        if (cc2[c].err) return fail(ctx, cc2[c].err == 4 ? GP_ERR_UNSUPPORTED : GP_ERR_INVALID_ARGUMENT, kErr[cc2[c].err]);
-    for (size_t c = 0; c < C; c++) {  // prefix sums (serial, O(C))
-        const gp_circuit_view &v = cs[c];
-        const CircCount &k = cc2[c];
-        CircuitMeta &m = metas[c];
-        m.n = v.num_qubits;
-        m.l = v.num_layers;
-        m.M = v.num_measurements;
-        m.D = v.num_detectors;
-        m.O = v.num_observables;
-        m.W = (uint32_t)(((uint64_t)m.D + m.O + 63) / 64);
-        m.layer_base = (uint32_t)t.layer_slots;
-        m.meas_base = (uint32_t)t.meas;
-        m.det_base = (uint32_t)t.det_slots;
-        m.obs_base = (uint32_t)t.obs_slots;
-        m.tile_base = (uint32_t)t.tiles;
-        m.bucket_base = (uint32_t)t.buckets;
-        m.src_base = t.sources;
-        m.ell_base = t.ell;
-        m.leaf_base = t.leaf;
-        m.src_noise = k.src_noise;
-        m.max_layer_noise = k.max_noise;
-        m.gate_base = t.gates;
-        m.noise_base = t.noise;
-        m.det_entry_base = t.det_entries;
-        m.obs_entry_base = t.obs_entries;
-        m.circ_layer_base = t.layers;
-        t.max_layer_noise = std::max(t.max_layer_noise, k.max_noise);
-        t.max_layer_meas = std::max(t.max_layer_meas, k.max_meas);
-        t.max_n = std::max(t.max_n, m.n);
-        t.max_W = std::max(t.max_W, m.W);
-        t.max_l = std::max(t.max_l, m.l);
-        t.layers += m.l;
-        t.layer_slots += m.l + 1;
-        t.gates += k.gates;
-        t.noise += k.noise;
-        t.meas += m.M;
-        t.det_slots += m.D + 1;
-        t.det_entries += k.det_entries;
-        t.obs_slots += m.O + 1;
-        t.obs_entries += k.obs_entries;
-        t.dets += m.D;
-        t.obss += m.O;
-        t.tiles += m.W;
-        t.sources += k.src_noise + m.M;
-        t.ell += m.l ? (uint64_t)(m.l - 1) * gp::ell_stride(m.n) : 0;
-        t.leaf += (uint64_t)m.W * gp::leaf_stride(m.M);
-        t.buckets += (uint64_t)m.D + 1;
-    }
-    if (t.sources >= 0xFFFFFFFFull || t.tiles >= 0xFFFFFFFFull || t.gates >= 0xFFFFFFFFull ||
-        t.noise >= 0xFFFFFFFFull || t.meas >= 0xFFFFFFFFull || t.layer_slots >= 0xFFFFFFFFull)
-        return fail(ctx, GP_ERR_UNSUPPORTED, "batch exceeds 32-bit device indexing; split it");
-    return GP_OK;
-}
-
-StageLayout stage_layout(const BatchTotals &t) {
-    StageLayout L{};
-    uint64_t o = 0;
-    auto put = [&](uint64_t bytes) {
-        const uint64_t at = o;
-        o = align16(o + bytes + 16);  // +16: bulk copies may over-read one 16-byte unit
-        return at;
-    };
-    L.meta = put(t.C * sizeof(CircuitMeta));
-    L.circ_layer = put((t.C + 1) * 4);
-    L.circ_src = put((t.C + 1) * 8);
-    L.circ_tile = put((t.C + 1) * 4);
-    L.circ_grp = put((t.C + 1) * 4);
-    L.circ_det = put((t.C + 1) * 4);
-    L.circ_obs = put((t.C + 1) * 4);
-    L.lay_gate = put(t.layer_slots * 4);
-    L.lay_noise = put(t.layer_slots * 4);
-    L.lay_meas = put(t.layer_slots * 4);
-    L.gates = put(t.gates * 8);
-    L.noise = put(t.noise * 8);
-    L.noise_prob = put(t.wide_prob ? t.noise * 8 : 0);
-    L.prob_table = put((uint64_t)t.prob_table_n * 8);
-    L.lay_src = put(t.layer_slots * 4);
-    L.meas_flip = put(t.meas * 8);
-    L.det_off = put(t.det_slots * 4);
-    L.det_meas = put(t.det_entries * 4);
-    L.obs_off = put(t.obs_slots * 4);
-    L.obs_meas = put(t.obs_entries * 4);
-    L.total = o;
-    return L;
-}
-
-// Pass 2: write the staging image, in parallel over circuits (each circuit's
-// slices of every array are disjoint and located by its prefix bases).
-// Cumulative per-circuit tables (O(C), serial).
-void pack_tables(const BatchTotals &t, const std::vector<CircuitMeta> &metas, const StageLayout &L, uint32_t T,
-                 const std::vector<double> &ptab, uint8_t *img) {
-    auto at = [&](uint64_t off) { return img + off; };
-    if (!ptab.empty()) std::memcpy(at(L.prob_table), ptab.data(), ptab.size() * 8);
-    std::memcpy(at(L.meta), metas.data(), t.C * sizeof(CircuitMeta));
-    auto *circ_layer = (uint32_t *)at(L.circ_layer);
-    auto *circ_src = (uint64_t *)at(L.circ_src);
-    auto *circ_tile = (uint32_t *)at(L.circ_tile);
-    auto *circ_grp = (uint32_t *)at(L.circ_grp);
-    auto *circ_det = (uint32_t *)at(L.circ_det);
-    auto *circ_obs = (uint32_t *)at(L.circ_obs);
-    uint64_t grps = 0, dets = 0, obss = 0;
-    for (uint32_t c = 0; c < t.C; c++) {  // O(C) cumulative tables
-        const CircuitMeta &m = metas[c];
-        circ_layer[c] = (uint32_t)m.circ_layer_base;
-        circ_src[c] = m.src_base;
-        circ_tile[c] = m.tile_base;
-        circ_grp[c] = (uint32_t)grps;
-        circ_det[c] = (uint32_t)dets;
-        circ_obs[c] = (uint32_t)obss;
-        grps += (m.W + T - 1) / T;
-        dets += m.D;
-        obss += m.O;
-    }
-    circ_layer[t.C] = (uint32_t)t.layers;
-    circ_src[t.C] = t.sources;
-    circ_tile[t.C] = (uint32_t)t.tiles;
-    circ_grp[t.C] = (uint32_t)grps;
-    circ_det[t.C] = (uint32_t)dets;
-    circ_obs[t.C] = (uint32_t)obss;
-}
-
-// Per-circuit slices of every section for circuits [c0, c1), in parallel.
-void pack_circuits(const gp_circuit_view *cs, const BatchTotals &t, const std::vector<CircuitMeta> &metas,
-                   const std::vector<CircCount> &cc, const StageLayout &L, uint8_t *img, size_t c0, size_t c1) {
-    auto at = [&](uint64_t off) { return img + off; };
-    auto *lay_gate = (uint32_t *)at(L.lay_gate);
-    auto *lay_noise = (uint32_t *)at(L.lay_noise);
-    auto *lay_meas = (uint32_t *)at(L.lay_meas);
-    auto *gates = (uint64_t *)at(L.gates);
-    auto *noise = (uint64_t *)at(L.noise);
-    auto *nprob = (double *)at(L.noise_prob);
-    auto *lay_src = (uint32_t *)at(L.lay_src);
-    auto *flip = (double *)at(L.meas_flip);
-    auto *det_off = (uint32_t *)at(L.det_off);
-    auto *det_meas = (uint32_t *)at(L.det_meas);
-    auto *obs_off = (uint32_t *)at(L.obs_off);
-    auto *obs_meas = (uint32_t *)at(L.obs_meas);
-    parallel_for(c1 - c0, [&](size_t ci) {
-        const size_t c = c0 + ci;
-        const gp_circuit_view &v = cs[c];
-        const CircuitMeta &m = metas[c];
-        const uint64_t g_at = m.gate_base, n_at = m.noise_base;
-        const uint32_t g0 = v.gate_offsets[0], n0 = v.noise_offsets[0];
-        uint32_t src = 0, meas = 0;
-        for (uint32_t i = 0; i <= m.l; i++) {
-            lay_gate[m.layer_base + i] = (uint32_t)(g_at + v.gate_offsets[i] - g0);
-            lay_noise[m.layer_base + i] = (uint32_t)(n_at + v.noise_offsets[i] - n0);
-            lay_meas[m.layer_base + i] = meas;
-            lay_src[m.layer_base + i] = src;
-            if (i == m.l) break;
-            for (uint32_t g = v.gate_offsets[i]; g < v.gate_offsets[i + 1]; g++) {
-                const uint8_t k = v.gate_kind[g];
-                uint32_t hi = 0;
-                if (k == GP_GATE_CX) hi = v.gate_q1[g];
-                if (k == GP_GATE_M || k == GP_GATE_MR) {
-                    hi = (uint32_t)v.gate_meas[g];
-                    flip[m.meas_base + hi] = v.gate_flip[g];
-                    meas++;
-                }
-                gates[g_at + g - g0] = (uint64_t)hi << 32 | (v.gate_q0[g] | (uint32_t)k << gp::kGateKindShift);
-            }
-            const CircCount &k2 = cc[c];
-            for (uint32_t o = v.noise_offsets[i]; o < v.noise_offsets[i + 1]; o++) {
-                const uint8_t k = v.noise_kind[o];
-                const uint64_t idx = n_at + o - n0;
-                uint64_t pidx = 0;
-                const double pr = v.noise_prob[o];
-                if (t.wide_prob) {
-                    nprob[idx] = pr;
-                } else {
-                    for (size_t x = 0; x < k2.probs.size(); x++)
-                        if (std::memcmp(&k2.probs[x], &pr, 8) == 0) {
-                            pidx = k2.pidx[x];
-                            break;
-                        }
-                }
-                noise[idx] = (uint64_t)v.noise_q0[o] |
-                             (uint64_t)(k == GP_NOISE_DEPOLARIZE2 ? v.noise_q1[o] : 0) << gp::kNoiseQubitBits |
-                             (uint64_t)k << gp::kNoiseKindShift | pidx << gp::kNoisePidxShift;
-                src += components(k, (uint8_t)t.level);
-            }
-        }
-        const uint64_t de_at = m.det_entry_base, oe_at = m.obs_entry_base;
-        for (uint32_t d = 0; d <= m.D; d++)
-            det_off[m.det_base + d] = (uint32_t)(de_at + v.det_offsets[d] - v.det_offsets[0]);
-        const uint32_t nde = v.det_offsets[m.D] - v.det_offsets[0];
-        if (nde) std::memcpy(det_meas + de_at, v.det_meas + v.det_offsets[0], nde * 4);
-        for (uint32_t o = 0; o <= m.O; o++)
-            obs_off[m.obs_base + o] = (uint32_t)(oe_at + v.obs_offsets[o] - v.obs_offsets[0]);
-        const uint32_t noe = v.obs_offsets[m.O] - v.obs_offsets[0];
-        if (noe) std::memcpy(obs_meas + oe_at, v.obs_meas + v.obs_offsets[0], noe * 4);
-    });
 }
 
 // Device workspace carve-up for a batch (capacity-checked, grown on demand).
@@ -434,11 +104,9 @@ struct WsPlan {
 };
 
 size_t carve(gp_ctx *ctx, DevPlan &p, const BatchTotals &t, uint8_t *base, uint32_t K, uint64_t ids_cap,
-             uint64_t pool_chunks, uint64_t slabs) {
-    const uint64_t S = t.sources;
-    uint64_t cap = 1024;
-    while (cap < S + S / 2 + 16) cap <<= 1;
-    const uint64_t nb = std::max<uint64_t>(S, t.buckets + 1) / 2048 + 16;
+             uint64_t pool_chunks, uint64_t slabs, uint64_t items_cap) {
+    const uint64_t S = t.sources, NB = t.buckets;
+    const uint64_t nb = std::max<uint64_t>(S, NB + 1) / 2048 + 16;
     size_t o = 0;
     auto take = [&](size_t bytes) {
         const size_t at = o;
@@ -459,29 +127,22 @@ size_t carve(gp_ctx *ctx, DevPlan &p, const BatchTotals &t, uint8_t *base, uint3
     p.slab_stride = slabs ? t.max_l : 0;
     p.slab = (uint64_t *)take(slabs * p.slab_words * 8);
     p.slab_hdr = (uint4 *)take(slabs * 16);
-    p.rep = (uint32_t *)take(S * 4);
-    p.gcnt = (uint32_t *)take(S * 4 + 4);
-    p.ecnt = (uint2 *)take(S * 8);
-    p.sscan = (uint4 *)take(S * 16);
-    p.table = (uint64_t *)take(cap * 8);
-    p.table_mask = cap - 1;
+    p.s_bkt = (uint32_t *)take(S * 4);
+    p.s_pos = (uint32_t *)take(S * 4);
+    p.s_ndno = (uint32_t *)take(S * 4);
     p.force_collisions = ctx->force_collisions;
-    p.e_src = (uint32_t *)take(S * 4);
-    p.e_idoff = (uint32_t *)take(S * 4);
-    p.e_nd = (uint32_t *)take(S * 4);
-    p.e_no = (uint32_t *)take(S * 4);
-    p.e_moff = (uint32_t *)take(S * 4 + 4);
-    p.e_bucket = (uint32_t *)take(S * 4);
-    p.e_circ = (uint32_t *)take(S * 4);
-    p.blist = (uint32_t *)take(S * 4);
-    p.perm = (uint32_t *)take(S * 4);
-    p.e_prob = (double *)take(S * 8);
-    p.mprob = (double *)take(S * 8);
-    p.pscan = (uint4 *)take(S * 16 + 16);
-    p.tid = (uint32_t *)take(ids_cap * 4);
+    p.bcount = (uint32_t *)take(NB * 4 + 4);
+    p.boff = (uint4 *)take((NB + 1) * 16);
+    p.items = (DevPlan::ItemStub *)take(items_cap * sizeof(DevPlan::ItemStub));
+    p.items_cap = items_cap;
+    p.ecount = (uint32_t *)take(NB * 4);
+    p.eids = (uint2 *)take(NB * 8);
+    p.oscan = (uint4 *)take((NB + 1) * 16);
+    p.e_src = (uint32_t *)take(items_cap * 4);
+    p.e_ndno = (uint32_t *)take(items_cap * 4);
+    p.e_prob = (double *)take(items_cap * 8);
+    p.huge = (uint32_t *)take(NB * 4);
     p.ids_cap = ids_cap;
-    p.bcount = (uint32_t *)take(t.buckets * 4 + 4);
-    p.boff = (uint4 *)take((t.buckets + 1) * 16);
     p.bsum = (uint4 *)take(nb * 16);
     p.bsum_cap = nb;
     p.o_det_off = (uint64_t *)take(S * 8 + 8);
@@ -530,6 +191,15 @@ gp_status ensure_host(gp_ctx *ctx, uint8_t **buf, size_t *cap, size_t need) {
     return GP_OK;
 }
 
+// The reference's exception texts (stepg.cpp:172-174, eec.cpp:45,53).
+gp_status fail_pack(gp_ctx *ctx, int err) {
+    static const char *kErr[] = {"", "circuit exceeds 32-bit node index space",
+                                 "detector references a measurement without a leaf",
+                                 "observable references a measurement without a leaf",
+                                 "circuit too wide for the device encoding"};
+    return fail(ctx, err == gp::kPackTooWide ? GP_ERR_UNSUPPORTED : GP_ERR_INVALID_ARGUMENT, kErr[err]);
+}
+
 float elapsed_ms(cudaEvent_t a, cudaEvent_t b) {
     float ms = 0;
     if (cudaEventElapsedTime(&ms, a, b) != cudaSuccess) {
@@ -550,24 +220,33 @@ gp_status run_batch(gp_ctx *ctx, const gp_circuit_view *cs, size_t count, uint8_
     const auto t0 = clk::now();
     if (level > 2) return fail(ctx, GP_ERR_INVALID_ARGUMENT, "correlation level must be 0, 1 or 2");
     if (cudaSetDevice(ctx->device) != cudaSuccess) return fail(ctx, GP_ERR_CUDA, "cudaSetDevice failed");
-    BatchTotals t;
-    gp_status st = plan_batch(ctx, cs, count, level, t, ctx->metas);
-    if (st != GP_OK) return st;
-    gp::TravCfg tcfg;
-    size_t tsmem;
-    if (!gp::plan_traversal(t, ctx->device, &tcfg, &tsmem))
-        return fail(ctx, GP_ERR_UNSUPPORTED, "circuit too wide for on-chip traversal state (2n words)");
-    t.groups = 0;
-    for (const CircuitMeta &m : ctx->metas) t.groups += (m.W + tcfg.T - 1) / tcfg.T;
-    const StageLayout L = stage_layout(t);
+    gp_status st = GP_OK;
+    gp::PackPlan &pp = ctx->pack;
+    // Host pool for large jobs (single large circuits pack on every core too).
+    uint64_t ops = 0;
+    for (size_t c = 0; c < count; c++)
+        ops += (uint64_t)(cs[c].gate_offsets[cs[c].num_layers] - cs[c].gate_offsets[0]) +
+               (cs[c].noise_offsets[cs[c].num_layers] - cs[c].noise_offsets[0]);
+    if (!ctx->pool && ops >= (1u << 16))
+        ctx->pool = std::make_unique<gp::HostPool>(std::max(1u, std::thread::hardware_concurrency()) - 1);
+    gp::HostPool *hpool = ops >= (1u << 16) ? ctx->pool.get() : nullptr;
+    gp::pack_plan(hpool, cs, count, level, pp);
+    if (pp.err == gp::kPackIndexSpace || pp.err == gp::kPackTooWide) {
+        // Circuits before the first index-space failure may still hold leaf
+        // errors: the reference would have thrown on those first.
+        const int leaf_err = gp::validate_leaves(cs, 0, pp.err_circuit);
+        return fail_pack(ctx, leaf_err ? leaf_err : pp.err);
+    }
+    const StageLayout &L = pp.L;
     if ((st = ensure_host(ctx, &ctx->h_stage, &ctx->h_stage_cap, L.total)) != GP_OK) return st;
     if ((st = ensure_device(ctx, &ctx->d_img, &ctx->d_img_cap, L.total)) != GP_OK) return st;
 
     // Pack in circuit chunks; each chunk's slice of every section is copied
     // while the next chunk is packed (the image is circuit-major per section).
+    // One chunk (one copy of the whole image) for single circuits.
     cudaError_t e = cudaSuccess;
     cudaEventRecord(ctx->ev_start, ctx->stream);
-    const std::vector<CircuitMeta> &M = ctx->metas;
+    const std::vector<CircuitMeta> &M = pp.metas;
     const size_t nchunk = count >= 1024 ? 8 : count >= 256 ? 4 : 1;
     auto slice = [&](uint64_t off, uint64_t elem, uint64_t lo, uint64_t hi) {
         if (hi > lo && e == cudaSuccess)
@@ -577,26 +256,44 @@ gp_status run_batch(gp_ctx *ctx, const gp_circuit_view *cs, size_t count, uint8_
     for (size_t k = 0; k < nchunk; k++) {
         const size_t c0 = count * k / nchunk, c1 = count * (k + 1) / nchunk;
         if (c1 == c0) continue;
-        pack_circuits(cs, t, M, ctx->circ_counts, L, ctx->h_stage, c0, c1);
+        gp::pack_range(hpool, cs, pp, ctx->h_stage, c0, c1);
+        if (nchunk == 1) break;
         const CircuitMeta &a = M[c0];
         const bool last = c1 == count;
         const CircuitMeta *b = last ? nullptr : &M[c1];
-        slice(L.lay_gate, 4, a.layer_base, last ? t.layer_slots : b->layer_base);
-        slice(L.lay_noise, 4, a.layer_base, last ? t.layer_slots : b->layer_base);
-        slice(L.lay_meas, 4, a.layer_base, last ? t.layer_slots : b->layer_base);
-        slice(L.gates, 8, a.gate_base, last ? t.gates : b->gate_base);
-        slice(L.noise, 8, a.noise_base, last ? t.noise : b->noise_base);
-        if (t.wide_prob) slice(L.noise_prob, 8, a.noise_base, last ? t.noise : b->noise_base);
-        slice(L.lay_src, 4, a.layer_base, last ? t.layer_slots : b->layer_base);
-        slice(L.meas_flip, 8, a.meas_base, last ? t.meas : b->meas_base);
-        slice(L.det_off, 4, a.det_base, last ? t.det_slots : b->det_base);
-        slice(L.det_meas, 4, a.det_entry_base, last ? t.det_entries : b->det_entry_base);
-        slice(L.obs_off, 4, a.obs_base, last ? t.obs_slots : b->obs_base);
-        slice(L.obs_meas, 4, a.obs_entry_base, last ? t.obs_entries : b->obs_entry_base);
+        const BatchTotals &tt = pp.t;
+        slice(L.lay_gate, 4, a.layer_base, last ? tt.layer_slots : b->layer_base);
+        slice(L.lay_noise, 4, a.layer_base, last ? tt.layer_slots : b->layer_base);
+        slice(L.gates, 8, a.gate_base, last ? tt.gates : b->gate_base);
+        slice(L.noise, 8, a.noise_base, last ? tt.noise : b->noise_base);
+        if (tt.wide_prob) slice(L.noise_prob, 8, a.noise_base, last ? tt.noise : b->noise_base);
+        slice(L.meas_flip, 8, a.meas_base, last ? tt.meas : b->meas_base);
+        slice(L.det_off, 4, a.det_base, last ? tt.det_slots : b->det_base);
+        slice(L.det_meas, 4, a.det_entry_base, last ? tt.det_entries : b->det_entry_base);
+        slice(L.obs_off, 4, a.obs_base, last ? tt.obs_slots : b->obs_base);
+        slice(L.obs_meas, 4, a.obs_entry_base, last ? tt.obs_entries : b->obs_entry_base);
     }
-    pack_tables(t, M, L, tcfg.T, ctx->prob_table, ctx->h_stage);
-    slice(0, 1, 0, L.lay_gate);  // meta + cumulative tables (the image's head)
-    slice(L.prob_table, 8, 0, t.prob_table_n);
+    if (pp.err) return fail_pack(ctx, pp.err);
+    gp::pack_finish(pp, ctx->h_stage);
+    BatchTotals t = pp.t;
+    if (t.sources >= 0xFFFFFFFFull || t.tiles >= 0xFFFFFFFFull || t.gates >= 0xFFFFFFFFull ||
+        t.noise >= 0xFFFFFFFFull || t.meas >= 0xFFFFFFFFull || t.layer_slots >= 0xFFFFFFFFull)
+        return fail(ctx, GP_ERR_UNSUPPORTED, "batch exceeds 32-bit device indexing; split it");
+    gp::TravCfg tcfg;
+    size_t tsmem;
+    if (!gp::plan_traversal(t, ctx->device, &tcfg, &tsmem))
+        return fail(ctx, GP_ERR_UNSUPPORTED, "circuit too wide for on-chip traversal state (2n words)");
+    t.groups = 0;
+    for (const CircuitMeta &m : M) t.groups += (m.W + tcfg.T - 1) / tcfg.T;
+    gp::pack_head(pp, tcfg.T, ctx->h_stage);
+    if (nchunk == 1) {
+        slice(0, 1, 0, L.total);  // the whole image in one copy
+    } else {
+        slice(L.lay_meas, 4, 0, t.layer_slots);  // finished prefix tables
+        slice(L.lay_src, 4, 0, t.layer_slots);
+        slice(0, 1, 0, L.lay_gate);  // meta + cumulative tables (the image's head)
+        slice(L.prob_table, 8, 0, t.prob_table_n);
+    }
     const uint64_t pack_ns = ns_since(t0);
     if (e != cudaSuccess) return cuda_fail(ctx, e, "upload");
     cudaEventRecord(ctx->ev_h2d, ctx->stream);
@@ -611,6 +308,10 @@ gp_status run_batch(gp_ctx *ctx, const gp_circuit_view *cs, size_t count, uint8_
     // Split traversal: walker CTA g owns max_l slabs (one per boundary it may walk).
     const uint64_t slabs = tcfg.split ? t.groups * t.max_l : 0;
     uint64_t ids_cap = std::max<uint64_t>(ctx->ids_hint, 3 * t.sources + 1024);
+    // Items: one per nonempty signature. All sources fit for single circuits;
+    // large batches start from half (and learn the real count on overflow).
+    uint64_t items_cap = std::max<uint64_t>(ctx->items_hint,
+                                            t.sources <= (16u << 20) ? t.sources + 16 : t.sources / 2 + 16);
     DevPlan p{};
     int launches = 0;
     for (int attempt = 0;; attempt++) {
@@ -621,9 +322,9 @@ gp_status run_batch(gp_ctx *ctx, const gp_circuit_view *cs, size_t count, uint8_
         p.trav = tcfg;
         p.trav.debug = ctx->trav_debug;
         p.trav_smem = tsmem;
-        const size_t need = carve(ctx, p, t, nullptr, K, ids_cap, pool, slabs);
+        const size_t need = carve(ctx, p, t, nullptr, K, ids_cap, pool, slabs, items_cap);
         if ((st = ensure_device(ctx, &ctx->d_ws, &ctx->d_ws_cap, need)) != GP_OK) return st;
-        carve(ctx, p, t, ctx->d_ws, K, ids_cap, pool, slabs);
+        carve(ctx, p, t, ctx->d_ws, K, ids_cap, pool, slabs, items_cap);
         if (ctx->trav_debug & 4) {  // experiments: per-step walk timestamps of every CTA
             if (!ctx->d_dbg) cudaMalloc(&ctx->d_dbg, (size_t)8192 * 512 * 4 * 8);
             cudaMemsetAsync(ctx->d_dbg, 0, (size_t)8192 * 512 * 4 * 8, ctx->stream);
@@ -636,6 +337,11 @@ gp_status run_batch(gp_ctx *ctx, const gp_circuit_view *cs, size_t count, uint8_
         if (e != cudaSuccess) return cuda_fail(ctx, e, "device pipeline");
         hdr = *ctx->h_hdr;
         if (attempt > 4) return fail(ctx, GP_ERR_CUDA, "capacity retry loop did not converge");
+        if (hdr.items_overflow) {  // more nonempty signatures than items: use every source
+            items_cap = t.sources + 16;
+            ctx->items_hint = items_cap;
+            continue;
+        }
         if (hdr.pool_overflow) {  // the record pool was too small
             pool = 2 * std::max<uint64_t>(pool, hdr.pool_chunks);
             ctx->pool_hint = pool;

@@ -9,6 +9,7 @@ namespace gp {
 
 constexpr uint32_t kPoolChunk = 1024;  // records per pool chunk
 constexpr uint32_t kPoolInvalid = 0xFFFFFFFFu;
+constexpr uint32_t kHugeCtas = 148;  // CTAs sorting buckets too large for a warp
 
 // Traversal launch configuration (chosen by plan_traversal for a batch).
 struct TravCfg {
@@ -55,27 +56,24 @@ struct DevPlan {
     uint64_t *slab;
     uint4 *slab_hdr;
     uint32_t slab_stride, slab_words;
-    uint32_t *rep;     // [S] representative source (group key) or kSuccNone
-    uint32_t *gcnt;    // [S] members per representative
-    uint2 *ecnt;       // [S] (detector ids, observable ids) per representative
-    uint4 *sscan;      // [S] exclusive scan: (edge id, member offset, id offset)
-
-    // Hash table (open addressing, linear probing).
-    uint64_t *table;
-    uint64_t table_mask;
-    int force_collisions;
-
-    // Per edge (capacity S).
-    uint32_t *e_src, *e_idoff, *e_nd, *e_no, *e_moff, *e_bucket, *e_circ, *blist, *perm;
-    double *e_prob;
-    double *mprob;    // [S] member probabilities grouped by edge
-    uint4 *pscan;     // [S + 1]
-    uint32_t *tid;    // [ids_cap] unsorted-position id lists (bit ids)
-    uint64_t ids_cap;
-
-    // Canonical-order buckets.
-    uint32_t *bcount;  // [NB]
+    // Reduce (gp_reduce.cuh), per source: bucket, slot in the bucket, id counts.
+    uint32_t *s_bkt, *s_pos, *s_ndno;
+    int force_collisions;  // test hook: every sort key equal (exact compare decides)
+    // Per bucket (circuit, first detector): sources, slot offsets (scan),
+    // groups (edges) and their id counts, output offsets (scan).
+    uint32_t *bcount;  // [NB + 1]
     uint4 *boff;       // [NB + 1]
+    struct ItemStub { uint32_t w[14]; };  // red::Item (56 bytes), sources in bucket order
+    ItemStub *items;   // [items_cap]
+    uint64_t items_cap;
+    uint32_t *ecount;  // [NB]
+    uint2 *eids;       // [NB]
+    uint4 *oscan;      // [NB + 1]
+    // Per group (edge), at the bucket's slots: representative, probability, ids.
+    uint32_t *e_src, *e_ndno;
+    double *e_prob;
+    uint32_t *huge;    // [NB] buckets too large for a warp
+    uint64_t ids_cap;
 
     // Scan scratch.
     uint4 *bsum;       // [S / 2048 + 2]
@@ -102,20 +100,16 @@ enum ProfStage {
     kProfLower,
     kProfTraverse,
     kProfEmit,
-    kProfDedup,
-    kProfScanSrc,
-    kProfScatter,
-    kProfFinalize,
+    kProfKey,
     kProfScanBucket,
-    kProfBucketScatter,
-    kProfRank,
-    kProfScanPos,
-    kProfGather,
+    kProfScatter,
+    kProfBucket,
+    kProfScanOut,
+    kProfWrite,
     kProfCount
 };
-constexpr const char *kProfNames[kProfCount] = {"start",   "memset",     "lower",          "traverse", "emit", "dedup",
-                                                "scan_src", "scatter",   "finalize",       "scan_bucket",
-                                                "bucket_scatter", "rank", "scan_pos",      "gather"};
+constexpr const char *kProfNames[kProfCount] = {"start",  "memset",      "lower",   "traverse", "emit",    "key",
+                                                "scan_bucket", "scatter", "bucket",   "scan_out", "write"};
 
 // Enqueues the whole device pipeline on `stream`: lowering, traversal,
 // reduce, canonical order, output gather. Returns the number of kernel

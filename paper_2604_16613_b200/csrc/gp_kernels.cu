@@ -145,7 +145,7 @@ __device__ __forceinline__ void fence_proxy_async() {
 // Part B: one thread per detector / observable toggles its bit into the leaf
 // rows of its measurements (init_leaves, eec.cpp:40-58).
 
-__global__ void lower_kernel(DevPlan p, uint32_t blocks_a) {
+__global__ void lower_kernel(__grid_constant__ const DevPlan p, uint32_t blocks_a) {
     const uint32_t C = p.tot.C;
     const CircuitMeta *meta = arr<CircuitMeta>(p, p.lay.meta);
     if (blockIdx.x < blocks_a) {
@@ -260,7 +260,7 @@ namespace {
 
 // Files the traversal's pooled records into per-source slots: the returning
 // slot-claim atomics run here, throughput-bound, off the traversal's path.
-__global__ void slot_kernel(DevPlan p) {
+__global__ void slot_kernel(__grid_constant__ const DevPlan p) {
     const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const uint32_t used = min(p.hdr->pool_chunks, p.pool_chunks_cap);
     if (i >= (uint64_t)used * kPoolChunk) return;
@@ -273,84 +273,6 @@ __global__ void slot_kernel(DevPlan p) {
     } else {
         atomicMax(&p.hdr->record_overflow, j + 1);
     }
-}
-
-// ---------------------------------------------------------------- K3 dedup
-// Groups sources with identical sparse signatures (the exact-equality
-// grouping of reduce_packed, dem.cpp:73-91): an order-independent 64-bit key
-// over the (tile, word) records, open addressing with linear probing, and a
-// FULL record comparison before two sources are merged -- hash collisions
-// never merge distinct signatures (dem.cpp:73-78, test_dem.cpp:94-101).
-
-__device__ __forceinline__ bool same_signature(const DevPlan &p, uint64_t a, uint64_t b, uint32_t n) {
-    if (p.cnt[b] != n) return false;
-    for (uint32_t x = 0; x < n; x++) {
-        const uint32_t ta = p.rtile[a * p.K + x];
-        const uint64_t ba = p.rbits[a * p.K + x];
-        bool found = false;
-        for (uint32_t y = 0; y < n; y++)
-            if (p.rtile[b * p.K + y] == ta) {
-                found = p.rbits[b * p.K + y] == ba;
-                break;
-            }
-        if (!found) return false;
-    }
-    return true;
-}
-
-__global__ void dedup_kernel(DevPlan p) {
-    const uint64_t s = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (s >= p.tot.sources) return;
-    if (p.hdr->record_overflow) return;
-    const uint32_t n = p.cnt[s];
-    if (n == 0) {  // empty signature: dropped (dem.cpp:93)
-        p.rep[s] = kSuccNone;
-        return;
-    }
-    const uint64_t *circ_src = arr<uint64_t>(p, p.lay.circ_src);
-    const uint32_t c = find_u64(circ_src, p.tot.C, s);
-    const uint64_t lo_s = circ_src[c], hi_s = circ_src[c + 1];
-    const uint32_t D = arr<CircuitMeta>(p, p.lay.meta)[c].D;
-    uint64_t h = mix64(0x9e3779b97f4a7c15ull + c);
-    uint32_t nd = 0, no = 0;
-    for (uint32_t x = 0; x < n; x++) {
-        const uint32_t tile = p.rtile[s * p.K + x];
-        const uint64_t bits = p.rbits[s * p.K + x];
-        h ^= mix64(bits ^ mix64(0x632be59bd9b4e019ull + tile));
-        const uint32_t b0 = tile * 64;
-        uint64_t dm;
-        if (b0 + 64 <= D) dm = ~0ull;
-        else if (b0 >= D) dm = 0;
-        else dm = (1ull << (D - b0)) - 1;
-        nd += __popcll(bits & dm);
-        no += __popcll(bits & ~dm);
-    }
-    h = mix64(h);
-    if (p.force_collisions) h = 42;
-    const uint64_t mykey = (h & 0xFFFFFFFF00000000ull) | (uint32_t)s;
-    uint64_t idx = (h ^ (h >> 31)) & p.table_mask;
-    uint32_t rep = kSuccNone;
-    while (true) {
-        unsigned long long cur = p.table[idx];
-        if (cur == ~0ull) {
-            cur = atomicCAS((unsigned long long *)&p.table[idx], ~0ull, (unsigned long long)mykey);
-            if (cur == ~0ull) {
-                rep = (uint32_t)s;
-                break;
-            }
-        }
-        if ((cur >> 32) == (mykey >> 32)) {
-            const uint32_t r = (uint32_t)cur;
-            if (r >= lo_s && r < hi_s && same_signature(p, s, r, n)) {
-                rep = r;
-                break;
-            }
-        }
-        idx = (idx + 1) & p.table_mask;
-    }
-    p.rep[s] = rep;
-    if (rep == (uint32_t)s) p.ecnt[s] = make_uint2(nd, no);
-    atomicAdd(&p.gcnt[rep], 1u);
 }
 
 // ---------------------------------------------------------------- scans
@@ -445,211 +367,39 @@ __global__ void scan_apply_kernel(F f, uint64_t n, const uint4 *bsum, uint4 *out
     }
 }
 
-struct SrcScanF {  // (edges, members, ids) per representative source
-    const uint32_t *rep, *gcnt;
-    const uint2 *ecnt;
-    const DeviceHeader *hdr;
-    __device__ bool active(uint64_t) const { return hdr->record_overflow == 0; }
-    __device__ uint4 operator()(uint64_t s) const {
-        if (rep[s] != (uint32_t)s) return make_uint4(0, 0, 0, 0);
-        const uint2 e = ecnt[s];
-        return make_uint4(1, gcnt[s], e.x + e.y, 0);
-    }
-};
-
 struct BucketScanF {
     const uint32_t *bcount;
     __device__ bool active(uint64_t) const { return true; }
     __device__ uint4 operator()(uint64_t b) const { return make_uint4(bcount[b], 0, 0, 0); }
 };
 
-struct PosScanF {  // (detector ids, observable ids) in canonical order
-    const uint32_t *perm, *nd, *no;
-    const DeviceHeader *hdr;
-    __device__ bool active(uint64_t base) const {  // not on a capacity-failed attempt (perm unwritten)
-        return base < hdr->num_edges && hdr->record_overflow == 0 && hdr->num_det_ids != 0xFFFFFFFFu;
-    }
-    __device__ uint4 operator()(uint64_t q) const {
-        if (q >= hdr->num_edges) return make_uint4(0, 0, 0, 0);
-        const uint32_t e = perm[q];
-        return make_uint4(nd[e], no[e], 0, 0);
+struct OutScanF {  // (edges, detector ids, observable ids) per bucket, in canonical order
+    const uint32_t *ecount;
+    const uint2 *eids;
+    __device__ bool active(uint64_t) const { return true; }
+    __device__ uint4 operator()(uint64_t b) const {
+        const uint2 v = eids[b];
+        return make_uint4(ecount[b], v.x, v.y, 0);
     }
 };
 
-// ---------------------------------------------------------------- K5..K9
+// Zero fills of one compile in one launch (grid-stride over up to 8 ranges).
+struct ZeroRanges {
+    uint4 *ptr[8];
+    uint64_t n16[8];  // 16-byte units
+    int count;
+};
 
-__global__ void totals_kernel(DevPlan p, const uint4 *src_total) {
-    // after the source scan: publish edge / member / id totals, check id
-    // capacity, and per-circuit edge offsets (one thread per circuit)
-    const uint4 t = *src_total;
-    const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
-    if (c == 0) {
-        p.hdr->num_edges = t.x;
-        p.hdr->num_members = t.y;
-        if ((uint64_t)t.z > p.ids_cap) p.hdr->num_det_ids = 0xFFFFFFFFu;  // capacity overflow marker
-        p.e_moff[t.x] = t.y;
-    }
-    if (c <= p.tot.C) {
-        const uint64_t s0 = arr<uint64_t>(p, p.lay.circ_src)[c];
-        p.o_edge_off[c] = s0 < p.tot.sources ? p.sscan[s0].x : t.x;
-    }
+__global__ void zero_kernel(ZeroRanges z) {
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (int r = 0; r < z.count; r++)
+        for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < z.n16[r]; i += stride)
+            z.ptr[r][i] = make_uint4(0, 0, 0, 0);
 }
 
-__device__ __forceinline__ bool pipeline_failed(const DevPlan &p) {
-    return p.hdr->record_overflow != 0 || p.hdr->num_det_ids == 0xFFFFFFFFu;
-}
-
-// Scatter member probabilities next to their edge; record edge -> source.
-__global__ void scatter_kernel(DevPlan p) {
-    const uint64_t s = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (s >= p.tot.sources || pipeline_failed(p)) return;
-    const uint32_t r = p.rep[s];
-    if (r == kSuccNone) return;
-    const uint4 sc = p.sscan[r];
-    const uint32_t pos = sc.y + atomicSub(&p.gcnt[r], 1u) - 1;
-    p.mprob[pos] = p.prob[s];
-    if (r == (uint32_t)s) {
-        p.e_src[sc.x] = r;
-        p.e_idoff[sc.x] = sc.z;
-        p.e_moff[sc.x] = sc.y;
-        const uint2 e = p.ecnt[r];
-        p.e_nd[sc.x] = e.x;
-        p.e_no[sc.x] = e.y;
-    }
-}
-
-// Per edge: sorted ascending fold from 0 (dem.cpp:97-106), id list expansion
-// (bit b < D -> detector b, else observable b - D; dem.cpp:108-116), bucket
-// by first detector for the canonical sort.
-__global__ void finalize_kernel(DevPlan p) {
-    const uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (pipeline_failed(p) || e >= p.hdr->num_edges) return;
-    const uint32_t m0 = p.e_moff[e], m1 = p.e_moff[e + 1], nm = m1 - m0;
-    double *mp = p.mprob + m0;
-    double acc = 0;
-    if (nm <= 32) {
-        double v[32];
-        for (uint32_t a = 0; a < nm; a++) {
-            const double x = mp[a];
-            uint32_t b = a;
-            while (b > 0 && v[b - 1] > x) {
-                v[b] = v[b - 1];
-                b--;
-            }
-            v[b] = x;
-        }
-        for (uint32_t a = 0; a < nm; a++) acc = merge_prob(acc, v[a]);
-    } else {  // rare large groups: in-place insertion sort in global memory
-        for (uint32_t a = 1; a < nm; a++) {
-            const double x = mp[a];
-            uint32_t b = a;
-            while (b > 0 && mp[b - 1] > x) {
-                mp[b] = mp[b - 1];
-                b--;
-            }
-            mp[b] = x;
-        }
-        for (uint32_t a = 0; a < nm; a++) acc = merge_prob(acc, mp[a]);
-    }
-    p.e_prob[e] = acc;
-
-    // ids: records sorted by tile, bits ascending
-    const uint32_t r = p.e_src[e];
-    const uint32_t n = p.cnt[r];
-    uint32_t order[16];
-    uint32_t nn = 0;
-    const uint32_t K = p.K;
-    for (uint32_t x = 0; x < n && x < 16; x++) {
-        const uint32_t tx = p.rtile[(uint64_t)r * K + x];
-        uint32_t b = nn++;
-        while (b > 0 && p.rtile[(uint64_t)r * K + order[b - 1]] > tx) {
-            order[b] = order[b - 1];
-            b--;
-        }
-        order[b] = x;
-    }
-    uint32_t *out = p.tid + p.e_idoff[e];
-    uint32_t w = 0;
-    for (uint32_t x = 0; x < nn; x++) {
-        const uint32_t tile = p.rtile[(uint64_t)r * K + order[x]];
-        uint64_t bits = p.rbits[(uint64_t)r * K + order[x]];
-        while (bits) {
-            const uint32_t b = __ffsll((long long)bits) - 1;
-            bits &= bits - 1;
-            out[w++] = tile * 64 + b;
-        }
-    }
-    const uint32_t c = find_u64(arr<uint64_t>(p, p.lay.circ_src), p.tot.C, r);
-    const CircuitMeta m = arr<CircuitMeta>(p, p.lay.meta)[c];
-    p.e_circ[e] = c;
-    const uint32_t bkt = m.bucket_base + (p.e_nd[e] ? out[0] + 1 : 0);
-    p.e_bucket[e] = bkt;
-    atomicAdd(&p.bcount[bkt], 1u);
-}
-
-__global__ void bucket_scatter_kernel(DevPlan p) {
-    const uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (pipeline_failed(p) || e >= p.hdr->num_edges) return;
-    const uint32_t b = p.e_bucket[e];
-    const uint32_t pos = p.boff[b].x + atomicSub(&p.bcount[b], 1u) - 1;
-    p.blist[pos] = (uint32_t)e;
-}
-
-// Canonical order (dem.cpp:122-127): std::vector lexicographic compare on
-// detectors (a prefix sorts first), then on observables.
-__device__ __forceinline__ int cmp_ids(const uint32_t *a, uint32_t na, const uint32_t *b, uint32_t nb) {
-    const uint32_t k = min(na, nb);
-    for (uint32_t x = 0; x < k; x++)
-        if (a[x] != b[x]) return a[x] < b[x] ? -1 : 1;
-    return na < nb ? -1 : na > nb ? 1 : 0;
-}
-
-__device__ __forceinline__ bool edge_less(const DevPlan &p, uint32_t a, uint32_t b) {
-    const uint32_t *ia = p.tid + p.e_idoff[a], *ib = p.tid + p.e_idoff[b];
-    const uint32_t nda = p.e_nd[a], ndb = p.e_nd[b];
-    const int c = cmp_ids(ia, nda, ib, ndb);
-    if (c) return c < 0;
-    return cmp_ids(ia + nda, p.e_no[a], ib + ndb, p.e_no[b]) < 0;
-}
-
-// Rank sort inside each bucket (edges sharing circuit and first detector):
-// all keys are distinct, so ranks form a permutation.
-__global__ void rank_kernel(DevPlan p) {
-    const uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (pipeline_failed(p) || e >= p.hdr->num_edges) return;
-    const uint32_t b = p.e_bucket[e];
-    const uint32_t lo = p.boff[b].x, hi = p.boff[b + 1].x;
-    uint32_t rank = 0;
-    for (uint32_t k = lo; k < hi; k++) {
-        const uint32_t o = p.blist[k];
-        if (o != (uint32_t)e && edge_less(p, o, (uint32_t)e)) rank++;
-    }
-    p.perm[lo + rank] = (uint32_t)e;
-}
-
-__global__ void gather_kernel(DevPlan p, const uint4 *pos_total) {
-    const uint64_t q = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (pipeline_failed(p)) return;
-    const uint32_t E = p.hdr->num_edges;
-    if (q == 0) {
-        const uint4 t = *pos_total;
-        p.o_det_off[E] = t.x;
-        p.o_obs_off[E] = t.y;
-        p.hdr->num_det_ids = t.x;
-        p.hdr->num_obs_ids = t.y;
-    }
-    if (q >= E) return;
-    const uint32_t e = p.perm[q];
-    const uint4 o = p.pscan[q];
-    p.o_det_off[q] = o.x;
-    p.o_obs_off[q] = o.y;
-    p.o_prob[q] = p.e_prob[e];
-    const uint32_t *ids = p.tid + p.e_idoff[e];
-    const uint32_t nd = p.e_nd[e], no = p.e_no[e];
-    const uint32_t D = arr<CircuitMeta>(p, p.lay.meta)[p.e_circ[e]].D;
-    for (uint32_t x = 0; x < nd; x++) p.o_det[o.x + x] = ids[x];
-    for (uint32_t x = 0; x < no; x++) p.o_obs[o.y + x] = ids[nd + x] - D;
-}
+}  // namespace
+#include "gp_reduce.cuh"
+namespace {
 
 template <class F>
 void launch_scan(F f, uint64_t n, uint4 *bsum, uint4 *out, uint4 *total, cudaStream_t st, int *launches) {
@@ -771,15 +521,27 @@ int enqueue_pipeline(const DevPlan &p, cudaStream_t st, const StageEvents *ev, c
         if (prof) cudaEventRecord(prof[k], st);
     };
     mark(kProfStart);
-    const uint64_t S = p.tot.sources;
-    // Zero / sentinel fills.
-    if (p.tot.ell) cudaMemsetAsync(p.ell, 0, p.tot.ell * 4, st);
-    if (p.tot.leaf) cudaMemsetAsync(p.leaf, 0, p.tot.leaf * 8, st);
-    cudaMemsetAsync(p.cnt, 0, S * 4 + 4, st);
-    cudaMemsetAsync(p.gcnt, 0, S * 4 + 4, st);
-    cudaMemsetAsync(p.table, 0xFF, (p.table_mask + 1) * 8, st);
-    cudaMemsetAsync(p.bcount, 0, p.tot.buckets * 4 + 4, st);
-    cudaMemsetAsync(p.hdr, 0, sizeof(DeviceHeader), st);
+    const uint64_t S = p.tot.sources, NB = p.tot.buckets;
+    // Zero fills (one launch): ELLPACK (idle nodes are word 0), leaf rows,
+    // per-source record counts, bucket counts, the header.
+    {
+        ZeroRanges z{};
+        auto add = [&](void *ptr, uint64_t bytes) {
+            if (!bytes) return;
+            z.ptr[z.count] = (uint4 *)ptr;
+            z.n16[z.count] = (bytes + 15) / 16;
+            z.count++;
+        };
+        add(p.ell, p.tot.ell * 4);
+        add(p.leaf, p.tot.leaf * 8);
+        add(p.cnt, S * 4 + 4);
+        add(p.bcount, NB * 4 + 4);
+        add(p.hdr, sizeof(DeviceHeader));
+        uint64_t units = 0;
+        for (int r = 0; r < z.count; r++) units = std::max(units, z.n16[r]);
+        zero_kernel<<<(uint32_t)std::min<uint64_t>(blocks_for(units, 256), 148 * 8), 256, 0, st>>>(z);
+        launches++;
+    }
     mark(kProfMemset);
 
     // K1 lowering.
@@ -824,28 +586,39 @@ int enqueue_pipeline(const DevPlan &p, cudaStream_t st, const StageEvents *ev, c
     mark(kProfEmit);
     if (ev) cudaEventRecord(ev->traversed, st);
 
-    // K3..K9 reduce.
+    // K3 reduce (gp_reduce.cuh): bucket by (circuit, first detector) with a
+    // counting sort, sort + group + fold each bucket on chip, write in order.
     const uint32_t tpb = 256;
-    uint4 *totals = p.bsum + p.bsum_cap - 4;  // 3 scan totals live at the end of bsum
-    if (S) dedup_kernel<<<blocks_for(S, tpb), tpb, 0, st>>>(p), launches++;
-    mark(kProfDedup);
-    launch_scan(SrcScanF{p.rep, p.gcnt, p.ecnt, p.hdr}, S, p.bsum, p.sscan, &totals[0], st, &launches);
-    totals_kernel<<<blocks_for(p.tot.C + 1, 256), 256, 0, st>>>(p, &totals[0]), launches++;
-    mark(kProfScanSrc);
-    if (S) scatter_kernel<<<blocks_for(S, tpb), tpb, 0, st>>>(p), launches++;
-    mark(kProfScatter);
-    if (S) finalize_kernel<<<blocks_for(S, tpb), tpb, 0, st>>>(p), launches++;
-    mark(kProfFinalize);
-    launch_scan(BucketScanF{p.bcount}, p.tot.buckets + 1, p.bsum, p.boff, &totals[1], st, &launches);
+    uint4 *totals = p.bsum + p.bsum_cap - 4;  // scan totals live at the end of bsum
+    const uint32_t sgrid = (uint32_t)std::min<uint64_t>(std::max<uint64_t>(blocks_for(S, tpb), 1), 148 * 16);
+    red::key_kernel<<<sgrid, tpb, 0, st>>>(p), launches++;
+    mark(kProfKey);
+    launch_scan(BucketScanF{p.bcount}, NB + 1, p.bsum, p.boff, &totals[0], st, &launches);
     mark(kProfScanBucket);
-    if (S) bucket_scatter_kernel<<<blocks_for(S, tpb), tpb, 0, st>>>(p), launches++;
-    mark(kProfBucketScatter);
-    if (S) rank_kernel<<<blocks_for(S, tpb), tpb, 0, st>>>(p), launches++;
-    mark(kProfRank);
-    launch_scan(PosScanF{p.perm, p.e_nd, p.e_no, p.hdr}, S, p.bsum, p.pscan, &totals[2], st, &launches);
-    mark(kProfScanPos);
-    gather_kernel<<<blocks_for(S + 1, tpb), tpb, 0, st>>>(p, &totals[2]), launches++;
-    mark(kProfGather);
+    red::scatter_kernel<<<sgrid, tpb, 0, st>>>(p), launches++;
+    mark(kProfScatter);
+    {
+        const uint64_t ctas = (NB + red::kBucketThreads / 32 - 1) / (red::kBucketThreads / 32);
+        red::bucket_kernel<<<(uint32_t)std::min<uint64_t>(std::max<uint64_t>(ctas, 1), 148 * 32),
+                             red::kBucketThreads, 0, st>>>(p);
+        static bool attr = false;  // once per process (the device attribute is per function)
+        if (!attr) {
+            cudaFuncSetAttribute(red::huge_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)red::kHugeSmem);
+            attr = true;
+        }
+        red::huge_kernel<<<kHugeCtas, 256, red::kHugeSmem, st>>>(p);
+        launches += 2;
+    }
+    mark(kProfBucket);
+    launch_scan(OutScanF{p.ecount, p.eids}, NB, p.bsum, p.oscan, &totals[1], st, &launches);
+    mark(kProfScanOut);
+    {
+        const uint64_t threads = std::max<uint64_t>(NB * 32, p.tot.C + 1);
+        red::write_kernel<<<(uint32_t)std::min<uint64_t>(blocks_for(threads, tpb), 148 * 32), tpb, 0, st>>>(
+            p, &totals[1]);
+        launches++;
+    }
+    mark(kProfWrite);
     if (ev) cudaEventRecord(ev->reduced, st);
     *err = cudaGetLastError();
     return launches;

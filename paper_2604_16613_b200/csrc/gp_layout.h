@@ -86,6 +86,7 @@ struct StageLayout {
     uint64_t circ_grp;    // u32[C + 1] cumulative traversal column groups
     uint64_t circ_det;    // u32[C + 1] cumulative detectors
     uint64_t circ_obs;    // u32[C + 1] cumulative observables
+    uint64_t circ_bkt;    // u32[C + 1] cumulative reduce buckets (D + 1 per circuit)
     uint64_t lay_gate;    // u32[sum(l + 1)] global gate index of each layer start
     uint64_t lay_noise;   // u32[sum(l + 1)] global noise index
     uint64_t lay_meas;    // u32[sum(l + 1)] local measurement index
@@ -134,7 +135,9 @@ struct DeviceHeader {
     uint32_t record_overflow;  // max records seen for one source if > slots, else 0
     uint32_t pool_chunks;      // record-pool chunks handed out by the traversal
     uint32_t pool_overflow;    // chunks requested beyond capacity (re-run larger)
-    uint32_t pad;
+    uint32_t huge_count;       // buckets too large for shared memory
+    uint32_t items_overflow;   // nonempty signatures beyond the item capacity (re-run larger)
+    uint32_t pad[2];
 };
 
 }  // namespace gp

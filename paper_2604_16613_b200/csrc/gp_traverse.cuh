@@ -196,7 +196,7 @@ __device__ __forceinline__ void pool_close(const DevPlan &p, const PoolWriter &w
 }
 
 template <int TM>
-__global__ void __launch_bounds__(800, 1) traverse_kernel(DevPlan p, TravCfg cfg) {
+__global__ void __launch_bounds__(800, 1) traverse_kernel(__grid_constant__ const DevPlan p, TravCfg cfg) {
     extern __shared__ __align__(128) uint8_t smem[];
     __shared__ CircuitMeta s_meta;
     __shared__ uint32_t s_min_m, s_max_m;

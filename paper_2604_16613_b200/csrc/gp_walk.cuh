@@ -79,7 +79,7 @@ struct WalkDims {
 // keeps their previous-boundary values in registers, so only the "other"
 // successor is read from shared memory. NPL == 0: generic loop.
 template <int WPC, int NPL>
-__global__ void __launch_bounds__(32 * WPC) walk_kernel(DevPlan p, TravCfg cfg) {
+__global__ void __launch_bounds__(32 * WPC) walk_kernel(__grid_constant__ const DevPlan p, TravCfg cfg) {
     extern __shared__ __align__(128) uint8_t smem[];
     __shared__ CircuitMeta s_meta;
     __shared__ uint32_t s_min_m, s_max_m, s_grp, s_circ;
@@ -310,7 +310,7 @@ __device__ __forceinline__ void put_record(const DevPlan &p, uint64_t src, uint3
     }
 }
 
-__global__ void __launch_bounds__(256) emit_kernel(DevPlan p) {
+__global__ void __launch_bounds__(256) emit_kernel(__grid_constant__ const DevPlan p) {
     const uint64_t used = (uint64_t)p.tot.groups * p.slab_stride;
     const uint32_t level = p.tot.level;
     const CircuitMeta *meta = arr<CircuitMeta>(p, p.lay.meta);
