@@ -66,6 +66,13 @@ __device__ __forceinline__ uint4 add4(uint4 a, uint4 b) {
     return make_uint4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w);
 }
 
+// Signature records are slot-major -- slot j of source s at j * S + s -- so
+// the first record of consecutive sources is contiguous (most sources have
+// one or two records).
+__device__ __forceinline__ uint64_t rec_at(const DevPlan &p, uint64_t s, uint32_t j) {
+    return (uint64_t)j * p.tot.sources + s;
+}
+
 template <class T>
 __device__ __forceinline__ const T *arr(const DevPlan &p, uint64_t off) {
     return reinterpret_cast<const T *>(p.img + off);
@@ -268,8 +275,8 @@ __global__ void slot_kernel(__grid_constant__ const DevPlan p) {
     if (r.x == kPoolInvalid) return;
     const uint32_t j = atomicAdd(&p.cnt[r.x], 1u);
     if (j < p.K) {
-        p.rbits[(uint64_t)r.x * p.K + j] = (uint64_t)r.w << 32 | r.z;
-        p.rtile[(uint64_t)r.x * p.K + j] = r.y;
+        p.rbits[rec_at(p, r.x, j)] = (uint64_t)r.w << 32 | r.z;
+        p.rtile[rec_at(p, r.x, j)] = r.y;
     } else {
         atomicMax(&p.hdr->record_overflow, j + 1);
     }

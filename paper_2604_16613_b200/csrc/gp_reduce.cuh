@@ -29,7 +29,7 @@ namespace red {
 __device__ __forceinline__ uint32_t sig_order(const DevPlan &p, uint64_t s, uint32_t n, uint8_t *ord) {
     uint32_t tile[16];
     for (uint32_t x = 0; x < n; x++) {
-        const uint32_t t = p.rtile[s * p.K + x];
+        const uint32_t t = p.rtile[rec_at(p, s, x)];
         uint32_t b = x;
         while (b > 0 && tile[b - 1] > t) {
             tile[b] = tile[b - 1];
@@ -47,14 +47,16 @@ __device__ __forceinline__ uint32_t sig_order(const DevPlan &p, uint64_t s, uint
 struct SeqIt {
     const uint32_t *rtile;
     const uint64_t *rbits;
+    uint64_t stride;          // slot-major records: slot j at j * stride
     uint32_t n, D, r, phase;  // phase 0: detectors, 1: observables, 2: done
     uint64_t bits;
     uint32_t tile;
     uint8_t ord[16];
 
     __device__ void init(const DevPlan &pl, uint64_t src, uint32_t d) {
-        rtile = pl.rtile + src * pl.K;
-        rbits = pl.rbits + src * pl.K;
+        rtile = pl.rtile + src;
+        rbits = pl.rbits + src;
+        stride = pl.tot.sources;
         D = d;
         n = min(pl.cnt[src], 16u);
         sig_order(pl, src, n, ord);
@@ -74,8 +76,8 @@ struct SeqIt {
         bits = 0;
         while (r < n) {
             const uint32_t slot = ord[r];
-            tile = rtile[slot];
-            bits = rbits[slot] & mask(tile);
+            tile = rtile[slot * stride];
+            bits = rbits[slot * stride] & mask(tile);
             if (bits) return;
             r++;
         }
@@ -132,7 +134,96 @@ struct Item {
 static_assert(sizeof(Item) == sizeof(DevPlan::ItemStub), "DevPlan::ItemStub mirrors Item");
 __device__ __forceinline__ Item *items_of(const DevPlan &p) { return reinterpret_cast<Item *>(p.items); }
 
+// Word mask of the detector bits (ids < D) of word t.
+__device__ __forceinline__ uint64_t det_mask(uint32_t t, uint32_t D) {
+    const uint32_t b0 = t * 64;
+    return b0 + 64 <= D ? ~0ull : b0 >= D ? 0 : (1ull << (D - b0)) - 1;
+}
+
+// Item of a source with at most 4 records, all in registers: records sorted
+// by word with a compare-swap network, detector ids generated in order.
+__device__ __forceinline__ Item make_item_small(const DevPlan &p, uint32_t s, uint32_t n, uint32_t D,
+                                                uint32_t ndno) {
+    uint32_t t[4];
+    uint64_t w[4];
+#pragma unroll
+    for (int j = 0; j < 4; j++) {
+        t[j] = (uint32_t)j < n ? p.rtile[rec_at(p, s, j)] : 0xFFFFFFFFu;
+        w[j] = (uint32_t)j < n ? p.rbits[rec_at(p, s, j)] : 0;
+    }
+    auto cs = [&](int a, int b) {
+        const bool sw = t[a] > t[b];
+        const uint32_t ta = sw ? t[b] : t[a], tb = sw ? t[a] : t[b];
+        const uint64_t wa = sw ? w[b] : w[a], wb = sw ? w[a] : w[b];
+        t[a] = ta;
+        t[b] = tb;
+        w[a] = wa;
+        w[b] = wb;
+    };
+    cs(0, 1);
+    cs(2, 3);
+    cs(0, 2);
+    cs(1, 3);
+    cs(1, 2);
+    // detector ids in order: record r, its remaining detector bits
+    uint32_t r = 0;
+    uint64_t rem = w[0] & det_mask(t[0], D);
+    uint32_t tile = t[0];
+    auto next_det = [&]() -> uint32_t {  // id + 1, or 0 at the end
+        while (rem == 0 && r < 3) {
+            r++;
+            const uint32_t tt = r == 1 ? t[1] : r == 2 ? t[2] : t[3];
+            const uint64_t ww = r == 1 ? w[1] : r == 2 ? w[2] : w[3];
+            tile = tt;
+            rem = tt == 0xFFFFFFFFu ? 0 : ww & det_mask(tt, D);
+        }
+        if (rem == 0) return 0;
+        const uint32_t b = (uint32_t)__ffsll((long long)rem) - 1;
+        rem &= rem - 1;
+        return tile * 64 + b + 1;
+    };
+    Item it;
+    const uint32_t q0 = next_det();
+    bool sep = q0 == 0, fits = true;
+    uint32_t sl[16];
+#pragma unroll
+    for (int x = 0; x < 16; x++) {
+        uint32_t v = 0;
+        if (!sep) {
+            const uint32_t e = next_det();
+            if (e == 0) sep = true;
+            else {
+                v = e - q0;
+                if (v >= 0xFFFFu) fits = false;
+            }
+        }
+        sl[x] = v & 0xFFFF;
+    }
+    if (!sep) fits = false;
+    uint64_t obs = 0;
+#pragma unroll
+    for (int j = 0; j < 4; j++) {
+        if (t[j] == 0xFFFFFFFFu) continue;
+        uint64_t ob = w[j] & ~det_mask(t[j], D);
+        while (ob) {
+            const uint32_t o = t[j] * 64 + (uint32_t)__ffsll((long long)ob) - 1 - D;
+            ob &= ob - 1;
+            if (o < 64) obs |= 1ull << o;
+            else fits = false;
+        }
+    }
+#pragma unroll
+    for (int x = 0; x < 8; x++) it.k[x] = sl[2 * x] << 16 | sl[2 * x + 1];
+    it.obs = obs;
+    it.prob = p.prob[s];
+    it.src = s;
+    it.ndno = ndno | ((fits && !p.force_collisions) ? 1u << 31 : 0u);
+    return it;
+}
+
 __device__ __forceinline__ Item make_item(const DevPlan &p, uint32_t s, uint32_t D, uint32_t ndno) {
+    const uint32_t nrec = p.cnt[s];
+    if (nrec <= 4) return make_item_small(p, s, nrec, D, ndno);
     Item it;
     SeqIt q;
     q.init(p, s, D);
@@ -212,30 +303,52 @@ __device__ __forceinline__ bool item_less(const DevPlan &p, const Item &a, const
 // Per source with a nonempty signature (empty ones are dropped, dem.cpp:93):
 // bucket (circuit, first detector) with its slot claimed by a counting-sort
 // atomic, and the detector / observable id counts.
-__global__ void key_kernel(__grid_constant__ const DevPlan p) {
-    const uint64_t S = p.tot.sources;
-    const uint64_t *circ_src = arr<uint64_t>(p, p.lay.circ_src);
-    const CircuitMeta *meta = arr<CircuitMeta>(p, p.lay.meta);
-    for (uint64_t s = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; s < S; s += (uint64_t)gridDim.x * blockDim.x) {
-        const uint32_t n = p.cnt[s];
-        if (n == 0 || n > p.K) continue;  // n > K: capacity re-run (record_overflow)
+// Source loops of the reduce: each CTA takes one contiguous chunk of sources
+// (threads stride by blockDim: coalesced), and each thread caches the circuit
+// its sources belong to (a circuit spans thousands of sources).
+struct CircCache {
+    uint64_t lo = 1, hi = 0;
+    uint32_t D = 0, bucket_base = 0;
+    __device__ __forceinline__ void at(const DevPlan &p, uint64_t s) {
+        if (s >= lo && s < hi) return;
+        const uint64_t *circ_src = arr<uint64_t>(p, p.lay.circ_src);
         const uint32_t c = find_u64(circ_src, p.tot.C, s);
-        const CircuitMeta &m = meta[c];
+        lo = circ_src[c];
+        hi = circ_src[c + 1];
+        const CircuitMeta &m = arr<CircuitMeta>(p, p.lay.meta)[c];
+        D = m.D;
+        bucket_base = m.bucket_base;
+    }
+};
+
+template <class F>
+__device__ __forceinline__ void for_sources(const DevPlan &p, F &&f) {
+    const uint64_t S = p.tot.sources;
+    const uint64_t chunk = ((S + gridDim.x - 1) / gridDim.x + blockDim.x - 1) / blockDim.x * blockDim.x;
+    const uint64_t s0 = (uint64_t)blockIdx.x * chunk, s1 = min(S, s0 + chunk);
+    CircCache cc;
+    for (uint64_t s = s0 + threadIdx.x; s < s1; s += blockDim.x) f(s, cc);
+}
+
+__global__ void key_kernel(__grid_constant__ const DevPlan p) {
+    for_sources(p, [&](uint64_t s, CircCache &cc) {
+        const uint32_t n = p.cnt[s];
+        if (n == 0 || n > p.K) return;  // n > K: capacity re-run (record_overflow)
+        cc.at(p, s);
         uint32_t first = 0xFFFFFFFFu, nd = 0, no = 0;
         for (uint32_t x = 0; x < n; x++) {
-            const uint32_t t = p.rtile[s * p.K + x];
-            const uint64_t bits = p.rbits[s * p.K + x];
-            const uint32_t b0 = t * 64;
-            const uint64_t dm = b0 + 64 <= m.D ? ~0ull : b0 >= m.D ? 0 : (1ull << (m.D - b0)) - 1;
+            const uint32_t t = p.rtile[rec_at(p, s, x)];
+            const uint64_t bits = p.rbits[rec_at(p, s, x)];
+            const uint64_t dm = det_mask(t, cc.D);
             nd += __popcll(bits & dm);
             no += __popcll(bits & ~dm);
-            if (bits & dm) first = min(first, b0 + (uint32_t)__ffsll((long long)(bits & dm)) - 1);
+            if (bits & dm) first = min(first, t * 64 + (uint32_t)__ffsll((long long)(bits & dm)) - 1);
         }
-        const uint32_t bkt = m.bucket_base + (first == 0xFFFFFFFFu ? 0 : first + 1);
+        const uint32_t bkt = cc.bucket_base + (first == 0xFFFFFFFFu ? 0 : first + 1);
         p.s_bkt[s] = bkt;
         p.s_pos[s] = atomicAdd(&p.bcount[bkt], 1u);
         p.s_ndno[s] = nd | no << 16;
-    }
+    });
 }
 
 // R3: counting-sort scatter. Each source's sort item (key built from its
@@ -243,20 +356,17 @@ __global__ void key_kernel(__grid_constant__ const DevPlan p) {
 // bucket kernel reads every bucket as one contiguous run -- random gathers
 // (latency) become scattered stores (bandwidth).
 __global__ void scatter_kernel(__grid_constant__ const DevPlan p) {
-    const uint64_t S = p.tot.sources;
-    const uint64_t *circ_src = arr<uint64_t>(p, p.lay.circ_src);
-    const CircuitMeta *meta = arr<CircuitMeta>(p, p.lay.meta);
-    for (uint64_t s = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; s < S; s += (uint64_t)gridDim.x * blockDim.x) {
+    for_sources(p, [&](uint64_t s, CircCache &cc) {
         const uint32_t n = p.cnt[s];
-        if (n == 0 || n > p.K) continue;
+        if (n == 0 || n > p.K) return;
         const uint64_t at = (uint64_t)p.boff[p.s_bkt[s]].x + p.s_pos[s];
         if (at >= p.items_cap) {  // capacity re-run with the learned count
             atomicOr(&p.hdr->items_overflow, 1u);
-            continue;
+            return;
         }
-        const uint32_t c = find_u64(circ_src, p.tot.C, s);
-        items_of(p)[at] = make_item(p, (uint32_t)s, meta[c].D, p.s_ndno[s]);
-    }
+        cc.at(p, s);
+        items_of(p)[at] = make_item(p, (uint32_t)s, cc.D, p.s_ndno[s]);
+    });
 }
 
 __device__ __forceinline__ uint32_t bucket_circuit(const DevPlan &p, uint64_t b) {
@@ -794,8 +904,8 @@ __global__ void write_kernel(__grid_constant__ const DevPlan p, const uint4 *out
                 sig_order(p, r, n, ord);
                 uint32_t wd = d0, wo = o0;
                 for (uint32_t x = 0; x < n; x++) {
-                    const uint32_t t = p.rtile[(uint64_t)r * p.K + ord[x]];
-                    uint64_t bits = p.rbits[(uint64_t)r * p.K + ord[x]];
+                    const uint32_t t = p.rtile[rec_at(p, r, ord[x])];
+                    uint64_t bits = p.rbits[rec_at(p, r, ord[x])];
                     while (bits) {
                         const uint32_t id = t * 64 + (uint32_t)__ffsll((long long)bits) - 1;
                         bits &= bits - 1;

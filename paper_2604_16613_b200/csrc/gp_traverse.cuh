@@ -122,8 +122,8 @@ __device__ __forceinline__ void emit_source(const DevPlan &p, uint64_t src, uint
 #pragma unroll
     for (int w = 0; w < TM; w++)
         if ((uint32_t)w < tw && v[w]) {
-            p.rbits[src * p.K + j] = v[w];
-            p.rtile[src * p.K + j] = t0 + w;
+            p.rbits[rec_at(p, src, j)] = v[w];
+            p.rtile[rec_at(p, src, j)] = t0 + w;
             j++;
         }
 }

@@ -303,8 +303,8 @@ __global__ void __launch_bounds__(32 * WPC) walk_kernel(__grid_constant__ const 
 __device__ __forceinline__ void put_record(const DevPlan &p, uint64_t src, uint32_t word, uint64_t bits) {
     const uint32_t j = atomicAdd(&p.cnt[src], 1u);
     if (j < p.K) {
-        p.rbits[src * p.K + j] = bits;
-        p.rtile[src * p.K + j] = word;
+        p.rbits[rec_at(p, src, j)] = bits;
+        p.rtile[rec_at(p, src, j)] = word;
     } else {
         atomicMax(&p.hdr->record_overflow, j + 1);
     }
