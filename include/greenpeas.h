@@ -135,7 +135,10 @@ enum {
                                          reference's injectable HashFn test hook
                                          (dem.hpp:59, test_dem.cpp:94-101) */
     GP_OPT_RECORD_SLOTS = 2,          /* inline sparse-signature slots per source */
-    GP_OPT_SYNC_TIMING = 3            /* 1: event-time each stage into gp_stats */
+    GP_OPT_SYNC_TIMING = 3,           /* 1: event-time each stage into gp_stats */
+    GP_OPT_PIPELINE = 4               /* batches of >= 1024 circuits: -1 auto (default), 0 off,
+                                         1 on -- sub-batches overlap host packing, upload,
+                                         device work and download */
 };
 gp_status gp_ctx_set_option(gp_ctx *ctx, int option, int64_t value);
 

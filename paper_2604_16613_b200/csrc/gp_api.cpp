@@ -30,6 +30,11 @@ using gp::DevPlan;
 using gp::DeviceHeader;
 using gp::StageLayout;
 
+namespace gp {
+struct PipeState;
+void pipe_destroy(PipeState *ps);
+}  // namespace gp
+
 struct gp_ctx {
     int device = 0;
     cudaStream_t stream = nullptr;
@@ -65,6 +70,9 @@ struct gp_ctx {
     uint64_t prof_ns[gp::kProfCount] = {};
     uint8_t *d_flush = nullptr;
     uint64_t *d_dbg = nullptr;  // experiments only (option 99, bit 2)
+    uint64_t *d_bases = nullptr;  // [8] zero bases in / scratch bases out (unpipelined compiles)
+    int pipeline = -1;            // GP_OPT_PIPELINE: -1 auto, 0 off, 1 on
+    gp::PipeState *pipe = nullptr;
 };
 
 namespace {
@@ -103,8 +111,28 @@ struct WsPlan {
     };
 };
 
+// Output region of a compile (gp_device.h): global-offset DEM arrays plus
+// the final header copy.
+size_t carve_out(DevPlan &p, uint8_t *base, uint64_t e_cap, uint64_t ids_cap, uint64_t C) {
+    size_t o = 0;
+    auto take = [&](size_t bytes) {
+        const size_t at = o;
+        o = (size_t)align16(o + bytes + 16);
+        return base ? base + at : nullptr;
+    };
+    p.e_cap = e_cap;
+    p.o_det_off = (uint64_t *)take(e_cap * 8 + 8);
+    p.o_obs_off = (uint64_t *)take(e_cap * 8 + 8);
+    p.o_prob = (double *)take(e_cap * 8);
+    p.o_det = (uint32_t *)take(ids_cap * 4);
+    p.o_obs = (uint32_t *)take(ids_cap * 4);
+    p.o_edge_off = (uint64_t *)take((C + 1) * 8);
+    p.hdr_out = (DeviceHeader *)take(sizeof(DeviceHeader));
+    return o;
+}
+
 size_t carve(gp_ctx *ctx, DevPlan &p, const BatchTotals &t, uint8_t *base, uint32_t K, uint64_t ids_cap,
-             uint64_t pool_chunks, uint64_t slabs, uint64_t items_cap) {
+             uint64_t pool_chunks, uint64_t slabs, uint64_t items_cap, bool with_out) {
     const uint64_t S = t.sources, NB = t.buckets;
     const uint64_t nb = std::max<uint64_t>(S, NB + 1) / 2048 + 16;
     size_t o = 0;
@@ -145,13 +173,12 @@ size_t carve(gp_ctx *ctx, DevPlan &p, const BatchTotals &t, uint8_t *base, uint3
     p.ids_cap = ids_cap;
     p.bsum = (uint4 *)take(nb * 16);
     p.bsum_cap = nb;
-    p.o_det_off = (uint64_t *)take(S * 8 + 8);
-    p.o_obs_off = (uint64_t *)take(S * 8 + 8);
-    p.o_det = (uint32_t *)take(ids_cap * 4);
-    p.o_obs = (uint32_t *)take(ids_cap * 4);
-    p.o_prob = (double *)take(S * 8);
-    p.o_edge_off = (uint64_t *)take((t.C + 1) * 8);
     p.hdr = (DeviceHeader *)take(sizeof(DeviceHeader));
+    if (with_out) {  // the output region at the end of the workspace
+        const size_t bytes = carve_out(p, nullptr, items_cap, ids_cap, t.C);
+        uint8_t *ob = (uint8_t *)take(bytes);
+        carve_out(p, ob, items_cap, ids_cap, t.C);
+    }
     return o;
 }
 
@@ -322,9 +349,11 @@ gp_status run_batch(gp_ctx *ctx, const gp_circuit_view *cs, size_t count, uint8_
         p.trav = tcfg;
         p.trav.debug = ctx->trav_debug;
         p.trav_smem = tsmem;
-        const size_t need = carve(ctx, p, t, nullptr, K, ids_cap, pool, slabs, items_cap);
+        const size_t need = carve(ctx, p, t, nullptr, K, ids_cap, pool, slabs, items_cap, true);
         if ((st = ensure_device(ctx, &ctx->d_ws, &ctx->d_ws_cap, need)) != GP_OK) return st;
-        carve(ctx, p, t, ctx->d_ws, K, ids_cap, pool, slabs, items_cap);
+        carve(ctx, p, t, ctx->d_ws, K, ids_cap, pool, slabs, items_cap, true);
+        p.base_in = ctx->d_bases;
+        p.base_out = ctx->d_bases + 4;
         if (ctx->trav_debug & 4) {  // experiments: per-step walk timestamps of every CTA
             if (!ctx->d_dbg) cudaMalloc(&ctx->d_dbg, (size_t)8192 * 512 * 4 * 8);
             cudaMemsetAsync(ctx->d_dbg, 0, (size_t)8192 * 512 * 4 * 8, ctx->stream);
@@ -427,6 +456,295 @@ gp_status run_batch(gp_ctx *ctx, const gp_circuit_view *cs, size_t count, uint8_
 
 }  // namespace
 
+// ---------------------------------------------------------------- pipelined batches
+// A large batch is compiled as P sub-batches in a software pipeline: while
+// the GPU runs sub-batch k, the host packs k+1 (into the other pinned
+// staging lane) and a copy stream uploads it; each sub-batch's DEM is copied
+// by copy_out_kernel on a third stream straight into the mapped pinned batch
+// view at its global offsets (the device keeps the running offsets), so the
+// download overlaps later sub-batches too. Device capacities come from the
+// context's learned hints; any overflow re-runs the batch unpipelined (which
+// learns larger hints).
+
+namespace {
+struct PipeLane {
+    gp::PackPlan pp;
+    uint8_t *h_stage = nullptr, *d_img = nullptr, *d_out = nullptr;
+    size_t h_stage_cap = 0, d_img_cap = 0, d_out_cap = 0;
+    cudaEvent_t ev_in = nullptr, ev_done = nullptr, ev_out = nullptr;
+    bool used = false;
+};
+}  // namespace
+
+namespace gp {
+struct PipeState {
+    PipeLane lane[2];
+    cudaStream_t s_in = nullptr, s_out = nullptr;
+    uint8_t *h_map = nullptr;  // mapped pinned DEM arrays
+    size_t h_map_cap = 0;
+    uint8_t *h_misc = nullptr;  // mapped: bases [(kMaxSub + 1) * 4], status, headers [kMaxSub]
+    uint64_t e_hint = 0, ids_hint = 0;
+};
+void pipe_destroy(PipeState *ps) {
+    if (!ps) return;
+    for (PipeLane &l : ps->lane) {
+        if (l.h_stage) cudaFreeHost(l.h_stage);
+        if (l.d_img) cudaFree(l.d_img);
+        if (l.d_out) cudaFree(l.d_out);
+        for (cudaEvent_t e : {l.ev_in, l.ev_done, l.ev_out})
+            if (e) cudaEventDestroy(e);
+    }
+    if (ps->s_in) cudaStreamDestroy(ps->s_in);
+    if (ps->s_out) cudaStreamDestroy(ps->s_out);
+    if (ps->h_map) cudaFreeHost(ps->h_map);
+    if (ps->h_misc) cudaFreeHost(ps->h_misc);
+    delete ps;
+}
+}  // namespace gp
+
+namespace {
+
+constexpr size_t kMaxSub = 64, kSubCircuits = 512;
+
+gp_status ensure_host_plain(uint8_t **buf, size_t *cap, size_t need) {
+    if (*cap >= need) return GP_OK;
+    if (*buf) cudaFreeHost(*buf);
+    *buf = nullptr;
+    *cap = 0;
+    const size_t want = need + need / 4 + 4096;
+    if (cudaHostAlloc(buf, want, cudaHostAllocDefault) != cudaSuccess) {
+        cudaGetLastError();
+        return GP_ERR_OUT_OF_MEMORY;
+    }
+    *cap = want;
+    return GP_OK;
+}
+
+gp_status ensure_dev_plain(uint8_t **buf, size_t *cap, size_t need) {
+    if (*cap >= need) return GP_OK;
+    if (*buf) cudaFree(*buf);
+    *buf = nullptr;
+    *cap = 0;
+    const size_t want = need + need / 4;
+    if (cudaMalloc(buf, want) != cudaSuccess) {
+        cudaGetLastError();
+        return GP_ERR_OUT_OF_MEMORY;
+    }
+    *cap = want;
+    return GP_OK;
+}
+
+bool pipeline_wanted(gp_ctx *ctx, size_t count) {
+    if (ctx->pipeline == 0 || count < 2 * kSubCircuits) return false;
+    return ctx->pipe && ctx->pipe->e_hint;  // needs learned output sizes (one unpipelined run)
+}
+
+gp_status run_batch_pipelined(gp_ctx *ctx, const gp_circuit_view *cs, size_t count, uint8_t level, HostOut &ho,
+                              DeviceHeader &hdr, gp_stats *stats) {
+    const auto t0 = clk::now();
+    gp::PipeState &ps = *ctx->pipe;
+    gp_status st = GP_OK;
+    const size_t P = std::min(kMaxSub, std::max<size_t>(2, count / kSubCircuits));
+    // Mapped host arrays of the whole batch view, sized by the learned hints.
+    const uint64_t e_cap = ps.e_hint, ids_cap = ps.ids_hint, c_cap = count + 1;
+    size_t o = 0;
+    auto take = [&](size_t bytes) {
+        const size_t at = o;
+        o = (size_t)align16(o + bytes);
+        return at;
+    };
+    const size_t o_det_off = take(e_cap * 8), o_obs_off = take(e_cap * 8), o_prob = take(e_cap * 8),
+                 o_det = take(ids_cap * 4), o_obs = take(ids_cap * 4), o_edge = take(c_cap * 8);
+    if (ps.h_map_cap < o) {
+        if (ps.h_map) cudaFreeHost(ps.h_map);
+        ps.h_map = nullptr;
+        ps.h_map_cap = 0;
+        if (cudaHostAlloc(&ps.h_map, o + o / 4, cudaHostAllocMapped) != cudaSuccess) {
+            cudaGetLastError();
+            return fail(ctx, GP_ERR_OUT_OF_MEMORY, "mapped host allocation failed");
+        }
+        ps.h_map_cap = o + o / 4;
+    }
+    uint64_t *bases = reinterpret_cast<uint64_t *>(ps.h_misc);
+    uint32_t *status = reinterpret_cast<uint32_t *>(bases + (kMaxSub + 1) * 4);
+    DeviceHeader *hdrs = reinterpret_cast<DeviceHeader *>(ps.h_misc + ((kMaxSub + 1) * 4 * 8 + 64));
+    std::fill(bases, bases + 4, 0);
+    *status = 0;
+    gp::HostOutMap hm{};
+    hm.det_off = (uint64_t *)(ps.h_map + o_det_off);
+    hm.obs_off = (uint64_t *)(ps.h_map + o_obs_off);
+    hm.probs = (double *)(ps.h_map + o_prob);
+    hm.det_ids = (uint32_t *)(ps.h_map + o_det);
+    hm.obs_ids = (uint32_t *)(ps.h_map + o_obs);
+    hm.edge_off = (uint64_t *)(ps.h_map + o_edge);
+    hm.e_cap = e_cap;
+    hm.ids_cap = ids_cap;
+    hm.c_cap = c_cap;
+    hm.status = status;
+
+    gp::HostPool *hpool = ctx->pool.get();
+    uint64_t h2d_bytes = 0, sources = 0;
+    int launches = 0;
+    auto drain = [&] {
+        cudaStreamSynchronize(ps.s_in);
+        cudaStreamSynchronize(ctx->stream);
+        cudaStreamSynchronize(ps.s_out);
+    };
+    cudaEventRecord(ctx->ev_start, ctx->stream);
+    for (size_t k = 0; k < P; k++) {
+        PipeLane &ln = ps.lane[k & 1];
+        const size_t c0 = count * k / P, c1 = count * (k + 1) / P, n = c1 - c0;
+        if (ln.used) cudaEventSynchronize(ln.ev_in);  // staging of sub-batch k-2 uploaded
+        gp::PackPlan &pp = ln.pp;
+        gp::pack_plan(hpool, cs + c0, n, level, pp);
+        if (pp.err == gp::kPackIndexSpace || pp.err == gp::kPackTooWide) {
+            drain();
+            const int leaf_err = gp::validate_leaves(cs + c0, 0, pp.err_circuit);
+            return fail_pack(ctx, leaf_err ? leaf_err : pp.err);
+        }
+        if ((st = ensure_host_plain(&ln.h_stage, &ln.h_stage_cap, pp.L.total)) != GP_OK)
+            return drain(), fail(ctx, st, "pinned host allocation failed");
+        gp::pack_range(hpool, cs + c0, pp, ln.h_stage, 0, n);
+        if (pp.err) return drain(), fail_pack(ctx, pp.err);
+        gp::pack_finish(pp, ln.h_stage);
+        BatchTotals t = pp.t;
+        if (t.sources >= 0xFFFFFFFFull || t.tiles >= 0xFFFFFFFFull || t.gates >= 0xFFFFFFFFull ||
+            t.noise >= 0xFFFFFFFFull || t.meas >= 0xFFFFFFFFull || t.layer_slots >= 0xFFFFFFFFull)
+            return drain(), fail(ctx, GP_ERR_UNSUPPORTED, "batch exceeds 32-bit device indexing; split it");
+        gp::TravCfg tcfg;
+        size_t tsmem;
+        if (!gp::plan_traversal(t, ctx->device, &tcfg, &tsmem))
+            return drain(), fail(ctx, GP_ERR_UNSUPPORTED, "circuit too wide for on-chip traversal state (2n words)");
+        t.groups = 0;
+        for (const CircuitMeta &m : pp.metas) t.groups += (m.W + tcfg.T - 1) / tcfg.T;
+        gp::pack_head(pp, tcfg.T, ln.h_stage);
+        // Device capacities from the learned hints (scaled to the sub-batch).
+        const uint32_t K = tcfg.direct ? std::max<uint32_t>(ctx->record_slots, tcfg.T) : ctx->record_slots;
+        uint64_t pool = 0;
+        if (!tcfg.direct && !tcfg.split)
+            pool = (2 * t.sources) / gp::kPoolChunk + t.groups * tcfg.emit_warps + 16;
+        const uint64_t slabs = tcfg.split ? t.groups * t.max_l : 0;
+        const uint64_t sub_ids = std::max<uint64_t>(3 * t.sources + 1024, ids_cap / P * 2);
+        const uint64_t sub_items = t.sources + 16;
+        DevPlan p{};
+        p.lay = pp.L;
+        p.tot = t;
+        p.trav = tcfg;
+        p.trav_smem = tsmem;
+        const size_t need_ws = carve(ctx, p, t, nullptr, K, sub_ids, pool, slabs, sub_items, false);
+        const size_t need_out = carve_out(p, nullptr, sub_items, sub_ids, t.C);
+        if (need_ws > ctx->d_ws_cap) {  // the workspace serves every sub-batch in stream order
+            cudaStreamSynchronize(ctx->stream);
+            if ((st = ensure_device(ctx, &ctx->d_ws, &ctx->d_ws_cap, need_ws)) != GP_OK) return drain(), st;
+        }
+        if (ln.used && (need_out > ln.d_out_cap || pp.L.total > ln.d_img_cap)) {
+            cudaEventSynchronize(ln.ev_out);
+            cudaEventSynchronize(ln.ev_done);
+        }
+        if (ensure_dev_plain(&ln.d_out, &ln.d_out_cap, need_out) != GP_OK ||
+            ensure_dev_plain(&ln.d_img, &ln.d_img_cap, pp.L.total) != GP_OK)
+            return drain(), fail(ctx, GP_ERR_OUT_OF_MEMORY, "device allocation failed");
+        carve(ctx, p, t, ctx->d_ws, K, sub_ids, pool, slabs, sub_items, false);
+        carve_out(p, ln.d_out, sub_items, sub_ids, t.C);
+        p.img = ln.d_img;
+        p.base_in = bases + 4 * k;
+        p.base_out = bases + 4 * (k + 1);
+        // upload (copy stream) -> pipeline (compute stream) -> copy-out (third
+        // stream); the upload overwrites the lane's image only once sub-batch
+        // k-2's kernels are done reading it
+        if (ln.used) cudaStreamWaitEvent(ps.s_in, ln.ev_done, 0);
+        cudaError_t e = cudaMemcpyAsync(ln.d_img, ln.h_stage, pp.L.total, cudaMemcpyHostToDevice, ps.s_in);
+        cudaEventRecord(ln.ev_in, ps.s_in);
+        cudaStreamWaitEvent(ctx->stream, ln.ev_in, 0);
+        if (ln.used) cudaStreamWaitEvent(ctx->stream, ln.ev_out, 0);  // copy-out of k-2 read d_out
+        launches += gp::enqueue_pipeline(p, ctx->stream, nullptr, nullptr, &e);
+        cudaEventRecord(ln.ev_done, ctx->stream);
+        cudaStreamWaitEvent(ps.s_out, ln.ev_done, 0);
+        hm.hdr_copy = hdrs + k;
+        gp::enqueue_copy_out(p, hm, ps.s_out);
+        cudaEventRecord(ln.ev_out, ps.s_out);
+        launches++;
+        ln.used = true;
+        if (e != cudaSuccess) return drain(), cuda_fail(ctx, e, "pipelined launch");
+        h2d_bytes += pp.L.total;
+        sources += t.sources;
+    }
+    const uint64_t pack_ns = ns_since(t0);
+    cudaEventRecord(ctx->ev_h2d, ctx->stream);
+    drain();
+    cudaEventRecord(ctx->ev_end, ps.s_out);
+    cudaEventSynchronize(ctx->ev_end);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "pipelined batch");
+    if (*status) {  // capacity: let the unpipelined path learn larger hints
+        ps.e_hint = 0;
+        return GP_ERR_UNSUPPORTED;  // caller falls back
+    }
+    const uint64_t E = bases[4 * P], nd = bases[4 * P + 1], no = bases[4 * P + 2];
+    hdr = DeviceHeader{};
+    hdr.num_edges = (uint32_t)E;
+    hdr.num_det_ids = (uint32_t)nd;
+    hdr.num_obs_ids = (uint32_t)no;
+    ps.e_hint = std::max(ps.e_hint, E + E / 8 + 1024);
+    ps.ids_hint = std::max(ps.ids_hint, std::max(nd, no) + std::max(nd, no) / 8 + 1024);
+    ho.det_off = hm.det_off;
+    ho.obs_off = hm.obs_off;
+    ho.probs = hm.probs;
+    ho.det_ids = hm.det_ids;
+    ho.obs_ids = hm.obs_ids;
+    ho.edge_off = hm.edge_off;
+    if (stats) {
+        *stats = gp_stats{};
+        const double all = elapsed_ms(ctx->ev_start, ctx->ev_end);
+        stats->lower_ns = pack_ns;
+        stats->kernel_ns = (uint64_t)(all * 1e6);
+        stats->num_sources = sources;
+        stats->h2d_bytes = h2d_bytes;
+        stats->d2h_bytes = (E + 1) * 16 + E * 8 + (nd + no) * 4 + (count + 1) * 8;
+        stats->kernel_launches = (uint64_t)launches;
+        stats->total_ns = ns_since(t0);
+    }
+    return GP_OK;
+}
+
+gp_status run_batch_any(gp_ctx *ctx, const gp_circuit_view *cs, size_t count, uint8_t level, HostOut &ho,
+                        DeviceHeader &hdr, gp_stats *stats) {
+    if (level > 2) return fail(ctx, GP_ERR_INVALID_ARGUMENT, "correlation level must be 0, 1 or 2");
+    if (cudaSetDevice(ctx->device) != cudaSuccess) return fail(ctx, GP_ERR_CUDA, "cudaSetDevice failed");
+    if (pipeline_wanted(ctx, count)) {
+        const gp_status st = run_batch_pipelined(ctx, cs, count, level, ho, hdr, stats);
+        if (st != GP_ERR_UNSUPPORTED || !ctx->err.empty()) return st;
+        ctx->err.clear();  // capacity miss: learn with the unpipelined path
+    }
+    const gp_status st = run_batch(ctx, cs, count, level, ho, hdr, stats);
+    if (st == GP_OK && ctx->pipeline != 0 && count >= 2 * kSubCircuits) {  // learn the pipeline's output sizes
+        if (!ctx->pipe) {
+            ctx->pipe = new gp::PipeState();
+            gp::PipeState &ps = *ctx->pipe;
+            cudaStreamCreateWithFlags(&ps.s_in, cudaStreamNonBlocking);
+            cudaStreamCreateWithFlags(&ps.s_out, cudaStreamNonBlocking);
+            for (PipeLane &l : ps.lane) {
+                cudaEventCreateWithFlags(&l.ev_in, cudaEventDisableTiming);
+                cudaEventCreateWithFlags(&l.ev_done, cudaEventDisableTiming);
+                cudaEventCreateWithFlags(&l.ev_out, cudaEventDisableTiming);
+            }
+            if (cudaHostAlloc(&ps.h_misc, (kMaxSub + 1) * 4 * 8 + 64 + kMaxSub * sizeof(DeviceHeader),
+                              cudaHostAllocMapped) != cudaSuccess) {
+                cudaGetLastError();
+                ps.h_misc = nullptr;
+            }
+        }
+        if (ctx->pipe->h_misc) {
+            const uint64_t E = hdr.num_edges, m = std::max(hdr.num_det_ids, hdr.num_obs_ids);
+            ctx->pipe->e_hint = std::max(ctx->pipe->e_hint, E + E / 8 + 1024);
+            ctx->pipe->ids_hint = std::max(ctx->pipe->ids_hint, m + m / 8 + 1024);
+        }
+    }
+    return st;
+}
+
+}  // namespace
+
 extern "C" {
 
 gp_status gp_ctx_create(int device, gp_ctx **out) {
@@ -451,6 +769,11 @@ gp_status gp_ctx_create(int device, gp_ctx **out) {
     cudaEventCreate(&ctx->stage_ev.lowered);
     cudaEventCreate(&ctx->stage_ev.traversed);
     cudaEventCreate(&ctx->stage_ev.reduced);
+    if (cudaMalloc(&ctx->d_bases, 8 * sizeof(uint64_t)) != cudaSuccess ||
+        cudaMemset(ctx->d_bases, 0, 8 * sizeof(uint64_t)) != cudaSuccess) {
+        delete ctx;
+        return GP_ERR_CUDA;
+    }
     *out = ctx;
     return GP_OK;
 }
@@ -465,6 +788,8 @@ void gp_ctx_destroy(gp_ctx *ctx) {
     if (ctx->d_img) cudaFree(ctx->d_img);
     if (ctx->d_ws) cudaFree(ctx->d_ws);
     if (ctx->d_flush) cudaFree(ctx->d_flush);
+    if (ctx->d_bases) cudaFree(ctx->d_bases);
+    gp::pipe_destroy(ctx->pipe);
     for (cudaEvent_t ev : ctx->prof)
         if (ev) cudaEventDestroy(ev);
     for (cudaEvent_t ev : {ctx->ev_start, ctx->ev_h2d, ctx->ev_end, ctx->stage_ev.lowered, ctx->stage_ev.traversed,
@@ -487,6 +812,10 @@ gp_status gp_ctx_set_option(gp_ctx *ctx, int option, int64_t value) {
             return GP_OK;
         case GP_OPT_SYNC_TIMING:
             return GP_OK;  // stage events are always recorded
+        case GP_OPT_PIPELINE:
+            if (value < -1 || value > 1) return fail(ctx, GP_ERR_INVALID_ARGUMENT, "pipeline must be -1, 0 or 1");
+            ctx->pipeline = (int)value;
+            return GP_OK;
         case 99:  // traversal experiments (not part of the ABI contract)
             ctx->trav_debug = (uint32_t)value;
             return GP_OK;
@@ -517,7 +846,7 @@ gp_status gp_compile_batch(gp_ctx *ctx, const gp_circuit_view *circuits, size_t 
     ctx->err.clear();
     HostOut ho{};
     DeviceHeader hdr{};
-    gp_status st = run_batch(ctx, circuits, count, level, ho, hdr, stats);
+    gp_status st = run_batch_any(ctx, circuits, count, level, ho, hdr, stats);
     if (st != GP_OK) return st;
     ctx->out_ndet.resize(count);
     ctx->out_nobs.resize(count);

@@ -79,11 +79,19 @@ struct DevPlan {
     uint4 *bsum;       // [S / 2048 + 2]
     uint64_t bsum_cap;
 
-    // Outputs (device), copied to pinned host after the header.
-    uint64_t *o_det_off, *o_obs_off;  // [S + 1]
-    uint32_t *o_det, *o_obs;          // [ids_cap]
-    double *o_prob;                   // [S]
-    uint64_t *o_edge_off;             // [C + 1]
+    // Outputs (device; the "output region"), copied to pinned host after the
+    // header, or by copy_out_kernel straight into mapped host memory.
+    // Offsets are global: this compile's edges / ids / circuits start at
+    // base_in[0..3] of the whole batch (a pipelined batch is compiled in
+    // sub-batches); write_kernel publishes base_out = base_in + totals.
+    uint64_t *o_det_off, *o_obs_off;  // [E_cap + 1] (values global)
+    uint32_t *o_det, *o_obs;          // [ids_cap] (local positions)
+    double *o_prob;                   // [E_cap]
+    uint64_t *o_edge_off;             // [C + 1] (values global)
+    uint64_t e_cap;                   // output edge capacity
+    const uint64_t *base_in;          // [4] edges, detector ids, observable ids, circuits before this compile
+    uint64_t *base_out;               // [4] the same after it
+    DeviceHeader *hdr_out;            // final header, copied into the output region
     DeviceHeader *hdr;
     uint64_t *dbg;  // experiments only (TravCfg.debug bit 2): per-step walk timestamps
 };
@@ -110,6 +118,22 @@ enum ProfStage {
 };
 constexpr const char *kProfNames[kProfCount] = {"start",  "memset",      "lower",   "traverse", "emit",    "key",
                                                 "scan_bucket", "scatter", "bucket",   "scan_out", "write"};
+
+// Mapped pinned host arrays of a batch DEM (gp_dem_batch_view) that
+// copy_out_kernel fills at the compile's global positions; capacities are
+// checked and an overflow is flagged in *status (the host re-runs larger).
+struct HostOutMap {
+    uint64_t *det_off, *obs_off, *edge_off;
+    double *probs;
+    uint32_t *det_ids, *obs_ids;
+    uint64_t e_cap, ids_cap, c_cap;
+    uint32_t *status;      // bit0 capacity overflow, bit1 a device capacity re-run is needed
+    DeviceHeader *hdr_copy;  // this compile's final header (mapped)
+};
+
+// Enqueues copy_out_kernel on `stream` (after the pipeline that produced p's
+// output region).
+void enqueue_copy_out(const DevPlan &p, const HostOutMap &h, cudaStream_t stream);
 
 // Enqueues the whole device pipeline on `stream`: lowering, traversal,
 // reduce, canonical order, output gather. Returns the number of kernel

@@ -850,24 +850,32 @@ __global__ void write_kernel(__grid_constant__ const DevPlan p, const uint4 *out
     const uint32_t lane = threadIdx.x & 31;
     const uint64_t warps = (uint64_t)gridDim.x * (blockDim.x >> 5);
     const CircuitMeta *meta = arr<CircuitMeta>(p, p.lay.meta);
+    const uint4 tot = *out_total;
+    const uint64_t bE = p.base_in[0], bD = p.base_in[1], bO = p.base_in[2];
+    const bool fits = (uint64_t)tot.y <= p.ids_cap && (uint64_t)tot.z <= p.ids_cap && (uint64_t)tot.x <= p.e_cap;
     if (blockIdx.x == 0 && threadIdx.x == 0) {
-        const uint4 t = *out_total;
-        if ((uint64_t)t.y > p.ids_cap || (uint64_t)t.z > p.ids_cap) {
-            p.hdr->num_det_ids = 0xFFFFFFFFu;  // capacity overflow marker: re-run larger
+        DeviceHeader h = *p.hdr;
+        if (!fits) {
+            h.num_det_ids = 0xFFFFFFFFu;  // capacity overflow marker: re-run larger
         } else {
-            p.hdr->num_edges = t.x;
-            p.hdr->num_det_ids = t.y;
-            p.hdr->num_obs_ids = t.z;
-            p.o_det_off[t.x] = t.y;
-            p.o_obs_off[t.x] = t.z;
+            h.num_edges = tot.x;
+            h.num_det_ids = tot.y;
+            h.num_obs_ids = tot.z;
+            p.o_det_off[tot.x] = bD + tot.y;
+            p.o_obs_off[tot.x] = bO + tot.z;
         }
+        *p.hdr = h;
+        *p.hdr_out = h;
+        p.base_out[0] = bE + tot.x;
+        p.base_out[1] = bD + tot.y;
+        p.base_out[2] = bO + tot.z;
+        p.base_out[3] = p.base_in[3] + p.tot.C;
     }
+    if (!fits || p.hdr->items_overflow) return;
     {  // per-circuit edge offsets (the bucket scan at each circuit's first bucket)
         const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-        if (t <= p.tot.C) p.o_edge_off[t] = t < p.tot.C ? p.oscan[meta[t].bucket_base].x : out_total->x;
+        if (t <= p.tot.C) p.o_edge_off[t] = bE + (t < p.tot.C ? p.oscan[meta[t].bucket_base].x : tot.x);
     }
-    const uint4 tot = *out_total;
-    if ((uint64_t)tot.y > p.ids_cap || (uint64_t)tot.z > p.ids_cap || p.hdr->items_overflow) return;
     for (uint64_t b = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; b < NB; b += warps) {
         const uint32_t ne = p.ecount[b];
         if (ne == 0) continue;
@@ -895,8 +903,8 @@ __global__ void write_kernel(__grid_constant__ const DevPlan p, const uint4 *out
             if (k < ne) {
                 const uint64_t e = (uint64_t)o.x + k;
                 const uint32_t d0 = o.y + dcar + di - nd, o0 = o.z + ocar + oi - no;
-                p.o_det_off[e] = d0;
-                p.o_obs_off[e] = o0;
+                p.o_det_off[e] = bD + d0;
+                p.o_obs_off[e] = bO + o0;
                 p.o_prob[e] = p.e_prob[base + k];
                 const uint32_t r = p.e_src[base + k];
                 uint8_t ord[16];
@@ -918,6 +926,34 @@ __global__ void write_kernel(__grid_constant__ const DevPlan p, const uint4 *out
             ocar += __shfl_sync(0xffffffffu, oi, 31);
         }
     }
+}
+
+// Copies one compile's output region into mapped host memory at its global
+// positions (the DEM of a pipelined sub-batch lands in the batch view while
+// later sub-batches compute). Sizes come from the device header: no host
+// round trip. Coalesced 8- / 4-byte stores over PCIe.
+__global__ void copy_out_kernel(__grid_constant__ const DevPlan p, HostOutMap h) {
+    const DeviceHeader hd = *p.hdr_out;
+    if (blockIdx.x == 0 && threadIdx.x == 0) *h.hdr_copy = hd;
+    if (hd.num_det_ids == 0xFFFFFFFFu || hd.items_overflow || hd.record_overflow || hd.pool_overflow) {
+        if (blockIdx.x == 0 && threadIdx.x == 0) atomicOr(h.status, 2u);
+        return;
+    }
+    const uint64_t bE = p.base_in[0], bD = p.base_in[1], bO = p.base_in[2], bC = p.base_in[3];
+    const uint64_t E = hd.num_edges, nd = hd.num_det_ids, no = hd.num_obs_ids, C = p.tot.C;
+    if (bE + E + 1 > h.e_cap || bD + nd > h.ids_cap || bO + no > h.ids_cap || bC + C + 1 > h.c_cap) {
+        if (blockIdx.x == 0 && threadIdx.x == 0) atomicOr(h.status, 1u);
+        return;
+    }
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x, t0 = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    for (uint64_t i = t0; i <= E; i += stride) {
+        h.det_off[bE + i] = p.o_det_off[i];
+        h.obs_off[bE + i] = p.o_obs_off[i];
+        if (i < E) h.probs[bE + i] = p.o_prob[i];
+    }
+    for (uint64_t i = t0; i < nd; i += stride) h.det_ids[bD + i] = p.o_det[i];
+    for (uint64_t i = t0; i < no; i += stride) h.obs_ids[bO + i] = p.o_obs[i];
+    for (uint64_t i = t0; i <= C; i += stride) h.edge_off[bC + i] = p.o_edge_off[i];
 }
 
 }  // namespace red

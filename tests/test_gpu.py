@@ -291,3 +291,17 @@ def test_many_distinct_probabilities_use_wide_mode(compiler, port):
     batch = compiler.compile_batch([g, small], 1)
     assert batch[0].hyperedges() == port.compile(g, 1)[0]
     assert batch[1].hyperedges() == port.compile(small, 1)[0]
+
+
+def test_pipelined_batch_matches_unpipelined():
+    """GP_OPT_PIPELINE: a batch compiled as overlapped sub-batches (host
+    packing || upload || device work || download) is bit-identical to the
+    one-pass batch, including the global offsets of the flat batch view."""
+    gens = [gp.gen_bb72_branch(b, rounds=3) for b in range(1100)]
+    comp = gp.Compiler(0)
+    comp.set_option(4, 0)
+    want = [d.hyperedges() for d in comp.compile_batch(gens, 0)]
+    comp.set_option(4, -1)
+    for _ in range(2):  # the first call learns output sizes, the second is pipelined
+        got = [d.hyperedges() for d in comp.compile_batch(gens, 0)]
+        assert got == want
