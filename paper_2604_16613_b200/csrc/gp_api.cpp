@@ -477,8 +477,9 @@ struct PipeLane {
 }  // namespace
 
 namespace gp {
+constexpr size_t kLanes = 3;  // sub-batches in flight (staging, image and output buffers)
 struct PipeState {
-    PipeLane lane[2];
+    PipeLane lane[kLanes];
     cudaStream_t s_in = nullptr, s_out = nullptr;
     uint8_t *h_map = nullptr;  // mapped pinned DEM arrays
     size_t h_map_cap = 0;
@@ -544,7 +545,8 @@ gp_status run_batch_pipelined(gp_ctx *ctx, const gp_circuit_view *cs, size_t cou
     const auto t0 = clk::now();
     gp::PipeState &ps = *ctx->pipe;
     gp_status st = GP_OK;
-    const size_t P = std::min(kMaxSub, std::max<size_t>(2, count / kSubCircuits));
+    static const size_t sub = std::getenv("GP_PIPE_SUB") ? (size_t)std::atoi(std::getenv("GP_PIPE_SUB")) : kSubCircuits;
+    const size_t P = std::min(kMaxSub, std::max<size_t>(2, count / sub));
     // Mapped host arrays of the whole batch view, sized by the learned hints.
     const uint64_t e_cap = ps.e_hint, ids_cap = ps.ids_hint, c_cap = count + 1;
     size_t o = 0;
@@ -570,7 +572,12 @@ gp_status run_batch_pipelined(gp_ctx *ctx, const gp_circuit_view *cs, size_t cou
     DeviceHeader *hdrs = reinterpret_cast<DeviceHeader *>(ps.h_misc + ((kMaxSub + 1) * 4 * 8 + 64));
     std::fill(bases, bases + 4, 0);
     *status = 0;
-    gp::HostOutMap hm{};
+    struct {
+        uint64_t *det_off, *obs_off, *edge_off;
+        double *probs;
+        uint32_t *det_ids, *obs_ids;
+        uint64_t e_cap, ids_cap, c_cap;
+    } hm{};
     hm.det_off = (uint64_t *)(ps.h_map + o_det_off);
     hm.obs_off = (uint64_t *)(ps.h_map + o_obs_off);
     hm.probs = (double *)(ps.h_map + o_prob);
@@ -580,7 +587,6 @@ gp_status run_batch_pipelined(gp_ctx *ctx, const gp_circuit_view *cs, size_t cou
     hm.e_cap = e_cap;
     hm.ids_cap = ids_cap;
     hm.c_cap = c_cap;
-    hm.status = status;
 
     gp::HostPool *hpool = ctx->pool.get();
     uint64_t h2d_bytes = 0, sources = 0;
@@ -590,11 +596,47 @@ gp_status run_batch_pipelined(gp_ctx *ctx, const gp_circuit_view *cs, size_t cou
         cudaStreamSynchronize(ctx->stream);
         cudaStreamSynchronize(ps.s_out);
     };
+    // Download of sub-batch j by the copy engine: sizes and global offsets
+    // are in mapped memory (written by its write_kernel) once it is done.
+    DevPlan plans[gp::kLanes];
+    std::vector<uint8_t> downloaded(P, 0);
+    auto download = [&](size_t j) {
+        PipeLane &l = ps.lane[j % gp::kLanes];
+        const DevPlan &pj = plans[j % gp::kLanes];
+        cudaEventSynchronize(l.ev_done);
+        const DeviceHeader &h = hdrs[j];
+        downloaded[j] = 1;
+        if (h.num_det_ids == 0xFFFFFFFFu || h.items_overflow || h.record_overflow || h.pool_overflow) {
+            *status |= 2;
+        } else {
+            const uint64_t bE = bases[4 * j], bD = bases[4 * j + 1], bO = bases[4 * j + 2], bC = bases[4 * j + 3];
+            const uint64_t E = h.num_edges, nd = h.num_det_ids, no = h.num_obs_ids, C = pj.tot.C;
+            if (bE + E + 1 > hm.e_cap || bD + nd > hm.ids_cap || bO + no > hm.ids_cap || bC + C + 1 > hm.c_cap) {
+                *status |= 1;
+            } else {
+                cudaMemcpyAsync(hm.det_off + bE, pj.o_det_off, (E + 1) * 8, cudaMemcpyDeviceToHost, ps.s_out);
+                cudaMemcpyAsync(hm.obs_off + bE, pj.o_obs_off, (E + 1) * 8, cudaMemcpyDeviceToHost, ps.s_out);
+                if (E) cudaMemcpyAsync(hm.probs + bE, pj.o_prob, E * 8, cudaMemcpyDeviceToHost, ps.s_out);
+                if (nd) cudaMemcpyAsync(hm.det_ids + bD, pj.o_det, nd * 4, cudaMemcpyDeviceToHost, ps.s_out);
+                if (no) cudaMemcpyAsync(hm.obs_ids + bO, pj.o_obs, no * 4, cudaMemcpyDeviceToHost, ps.s_out);
+                cudaMemcpyAsync(hm.edge_off + bC, pj.o_edge_off, (C + 1) * 8, cudaMemcpyDeviceToHost, ps.s_out);
+            }
+        }
+        cudaEventRecord(l.ev_out, ps.s_out);
+    };
     cudaEventRecord(ctx->ev_start, ctx->stream);
+    // GP_PIPE_TRACE=1: per sub-batch host pack time and device event times (stderr)
+    static const bool trace = std::getenv("GP_PIPE_TRACE") != nullptr;
+    std::vector<cudaEvent_t> tev;
+    std::vector<double> tpack;
     for (size_t k = 0; k < P; k++) {
-        PipeLane &ln = ps.lane[k & 1];
+        PipeLane &ln = ps.lane[k % gp::kLanes];
+        for (size_t j = k >= gp::kLanes ? k - gp::kLanes + 1 : 0; j < k; j++)  // finished ones: download now
+            if (!downloaded[j] && cudaEventQuery(ps.lane[j % gp::kLanes].ev_done) == cudaSuccess) download(j);
+        if (k >= gp::kLanes && !downloaded[k - gp::kLanes]) download(k - gp::kLanes);  // before the lane is reused
+        const auto tp0 = clk::now();
         const size_t c0 = count * k / P, c1 = count * (k + 1) / P, n = c1 - c0;
-        if (ln.used) cudaEventSynchronize(ln.ev_in);  // staging of sub-batch k-2 uploaded
+        if (ln.used) cudaEventSynchronize(ln.ev_in);  // the lane's previous staging was uploaded
         gp::PackPlan &pp = ln.pp;
         gp::pack_plan(hpool, cs + c0, n, level, pp);
         if (pp.err == gp::kPackIndexSpace || pp.err == gp::kPackTooWide) {
@@ -626,7 +668,8 @@ gp_status run_batch_pipelined(gp_ctx *ctx, const gp_circuit_view *cs, size_t cou
         const uint64_t slabs = tcfg.split ? t.groups * t.max_l : 0;
         const uint64_t sub_ids = std::max<uint64_t>(3 * t.sources + 1024, ids_cap / P * 2);
         const uint64_t sub_items = t.sources + 16;
-        DevPlan p{};
+        DevPlan &p = plans[k % gp::kLanes];
+        p = DevPlan{};
         p.lay = pp.L;
         p.tot = t;
         p.trav = tcfg;
@@ -649,26 +692,32 @@ gp_status run_batch_pipelined(gp_ctx *ctx, const gp_circuit_view *cs, size_t cou
         p.img = ln.d_img;
         p.base_in = bases + 4 * k;
         p.base_out = bases + 4 * (k + 1);
-        // upload (copy stream) -> pipeline (compute stream) -> copy-out (third
-        // stream); the upload overwrites the lane's image only once sub-batch
-        // k-2's kernels are done reading it
+        p.hdr_out = hdrs + k;  // mapped: the host reads it for the download
+        // upload (copy stream) -> pipeline (compute stream) -> download (third
+        // stream); the upload overwrites the lane's image only once the lane's
+        // previous kernels are done reading it
         if (ln.used) cudaStreamWaitEvent(ps.s_in, ln.ev_done, 0);
         cudaError_t e = cudaMemcpyAsync(ln.d_img, ln.h_stage, pp.L.total, cudaMemcpyHostToDevice, ps.s_in);
         cudaEventRecord(ln.ev_in, ps.s_in);
         cudaStreamWaitEvent(ctx->stream, ln.ev_in, 0);
-        if (ln.used) cudaStreamWaitEvent(ctx->stream, ln.ev_out, 0);  // copy-out of k-2 read d_out
+        if (ln.used) cudaStreamWaitEvent(ctx->stream, ln.ev_out, 0);  // the lane's download read d_out
+        if (trace) {
+            tpack.push_back(ns_since(tp0) / 1e3);
+            for (int x = 0; x < 3; x++) tev.push_back(nullptr), cudaEventCreate(&tev.back());
+            cudaEventRecord(tev[tev.size() - 3], ps.s_in);
+        }
         launches += gp::enqueue_pipeline(p, ctx->stream, nullptr, nullptr, &e);
+        if (trace) cudaEventRecord(tev[tev.size() - 2], ctx->stream);
         cudaEventRecord(ln.ev_done, ctx->stream);
-        cudaStreamWaitEvent(ps.s_out, ln.ev_done, 0);
-        hm.hdr_copy = hdrs + k;
-        gp::enqueue_copy_out(p, hm, ps.s_out);
-        cudaEventRecord(ln.ev_out, ps.s_out);
-        launches++;
         ln.used = true;
         if (e != cudaSuccess) return drain(), cuda_fail(ctx, e, "pipelined launch");
         h2d_bytes += pp.L.total;
         sources += t.sources;
     }
+    for (size_t j = 0; j < P; j++)
+        if (!downloaded[j]) download(j);
+    if (trace)
+        for (size_t k = 0; k < P; k++) cudaEventRecord(tev[3 * k + 2], ps.s_out);
     const uint64_t pack_ns = ns_since(t0);
     cudaEventRecord(ctx->ev_h2d, ctx->stream);
     drain();
@@ -676,6 +725,14 @@ gp_status run_batch_pipelined(gp_ctx *ctx, const gp_circuit_view *cs, size_t cou
     cudaEventSynchronize(ctx->ev_end);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(ctx, e, "pipelined batch");
+    if (trace) {
+        for (size_t k = 0; k < tpack.size(); k++) {
+            std::fprintf(stderr, "sub %zu pack %.0f us  upload done %.0f  kernels done %.0f  copy-out done %.0f (us from start)\n", k,
+                         tpack[k], elapsed_ms(ctx->ev_start, tev[3 * k]) * 1e3, elapsed_ms(ctx->ev_start, tev[3 * k + 1]) * 1e3,
+                         elapsed_ms(ctx->ev_start, tev[3 * k + 2]) * 1e3);
+        }
+        for (cudaEvent_t ev : tev) cudaEventDestroy(ev);
+    }
     if (*status) {  // capacity: let the unpipelined path learn larger hints
         ps.e_hint = 0;
         return GP_ERR_UNSUPPORTED;  // caller falls back

@@ -79,8 +79,8 @@ struct DevPlan {
     uint4 *bsum;       // [S / 2048 + 2]
     uint64_t bsum_cap;
 
-    // Outputs (device; the "output region"), copied to pinned host after the
-    // header, or by copy_out_kernel straight into mapped host memory.
+    // Outputs (device; the "output region"), copied to pinned host memory
+    // after the header.
     // Offsets are global: this compile's edges / ids / circuits start at
     // base_in[0..3] of the whole batch (a pipelined batch is compiled in
     // sub-batches); write_kernel publishes base_out = base_in + totals.
@@ -91,7 +91,7 @@ struct DevPlan {
     uint64_t e_cap;                   // output edge capacity
     const uint64_t *base_in;          // [4] edges, detector ids, observable ids, circuits before this compile
     uint64_t *base_out;               // [4] the same after it
-    DeviceHeader *hdr_out;            // final header, copied into the output region
+    DeviceHeader *hdr_out;            // final header copy (output region, or mapped host memory)
     DeviceHeader *hdr;
     uint64_t *dbg;  // experiments only (TravCfg.debug bit 2): per-step walk timestamps
 };
@@ -118,22 +118,6 @@ enum ProfStage {
 };
 constexpr const char *kProfNames[kProfCount] = {"start",  "memset",      "lower",   "traverse", "emit",    "key",
                                                 "scan_bucket", "scatter", "bucket",   "scan_out", "write"};
-
-// Mapped pinned host arrays of a batch DEM (gp_dem_batch_view) that
-// copy_out_kernel fills at the compile's global positions; capacities are
-// checked and an overflow is flagged in *status (the host re-runs larger).
-struct HostOutMap {
-    uint64_t *det_off, *obs_off, *edge_off;
-    double *probs;
-    uint32_t *det_ids, *obs_ids;
-    uint64_t e_cap, ids_cap, c_cap;
-    uint32_t *status;      // bit0 capacity overflow, bit1 a device capacity re-run is needed
-    DeviceHeader *hdr_copy;  // this compile's final header (mapped)
-};
-
-// Enqueues copy_out_kernel on `stream` (after the pipeline that produced p's
-// output region).
-void enqueue_copy_out(const DevPlan &p, const HostOutMap &h, cudaStream_t stream);
 
 // Enqueues the whole device pipeline on `stream`: lowering, traversal,
 // reduce, canonical order, output gather. Returns the number of kernel

@@ -521,10 +521,6 @@ bool plan_traversal(const BatchTotals &t, int device, TravCfg *cfg, size_t *smem
     }
 }
 
-void enqueue_copy_out(const DevPlan &p, const HostOutMap &h, cudaStream_t st) {
-    red::copy_out_kernel<<<64, 256, 0, st>>>(p, h);
-}
-
 int enqueue_pipeline(const DevPlan &p, cudaStream_t st, const StageEvents *ev, const cudaEvent_t *prof,
                      cudaError_t *err) {
     int launches = 0;

@@ -928,32 +928,4 @@ __global__ void write_kernel(__grid_constant__ const DevPlan p, const uint4 *out
     }
 }
 
-// Copies one compile's output region into mapped host memory at its global
-// positions (the DEM of a pipelined sub-batch lands in the batch view while
-// later sub-batches compute). Sizes come from the device header: no host
-// round trip. Coalesced 8- / 4-byte stores over PCIe.
-__global__ void copy_out_kernel(__grid_constant__ const DevPlan p, HostOutMap h) {
-    const DeviceHeader hd = *p.hdr_out;
-    if (blockIdx.x == 0 && threadIdx.x == 0) *h.hdr_copy = hd;
-    if (hd.num_det_ids == 0xFFFFFFFFu || hd.items_overflow || hd.record_overflow || hd.pool_overflow) {
-        if (blockIdx.x == 0 && threadIdx.x == 0) atomicOr(h.status, 2u);
-        return;
-    }
-    const uint64_t bE = p.base_in[0], bD = p.base_in[1], bO = p.base_in[2], bC = p.base_in[3];
-    const uint64_t E = hd.num_edges, nd = hd.num_det_ids, no = hd.num_obs_ids, C = p.tot.C;
-    if (bE + E + 1 > h.e_cap || bD + nd > h.ids_cap || bO + no > h.ids_cap || bC + C + 1 > h.c_cap) {
-        if (blockIdx.x == 0 && threadIdx.x == 0) atomicOr(h.status, 1u);
-        return;
-    }
-    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x, t0 = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    for (uint64_t i = t0; i <= E; i += stride) {
-        h.det_off[bE + i] = p.o_det_off[i];
-        h.obs_off[bE + i] = p.o_obs_off[i];
-        if (i < E) h.probs[bE + i] = p.o_prob[i];
-    }
-    for (uint64_t i = t0; i < nd; i += stride) h.det_ids[bD + i] = p.o_det[i];
-    for (uint64_t i = t0; i < no; i += stride) h.obs_ids[bO + i] = p.o_obs[i];
-    for (uint64_t i = t0; i <= C; i += stride) h.edge_off[bC + i] = p.o_edge_off[i];
-}
-
 }  // namespace red
