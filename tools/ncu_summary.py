@@ -18,6 +18,7 @@ def launches(path):
 
 
 METRICS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+           "dram__throughput.avg.pct_of_peak_sustained_elapsed", "l1tex__t_sector_hit_rate.pct",
            "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "lts__t_sector_hit_rate.pct",
            "sm__warps_active.avg.pct_of_peak_sustained_active", "sm__throughput.avg.pct_of_peak_sustained_elapsed",
            "smsp__thread_inst_executed_per_inst_executed.ratio", "launch__registers_per_thread", "launch__grid_size",
@@ -45,7 +46,7 @@ def report(path):
         agg = defaultdict(int)
         for r in rows[2:]:
             for i in cols:
-                if r[i].isdigit():
+                if i < len(r) and r[i].isdigit():
                     agg[h[i]] += int(r[i])
         tot = sum(agg.values()) or 1
         out.append("  warp stall samples: " + ", ".join(f"{k[6:]} {100 * v / tot:.0f}%" for k, v in
