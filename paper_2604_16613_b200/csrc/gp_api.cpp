@@ -54,6 +54,8 @@ struct gp_ctx {
     size_t d_ws_cap = 0;
     uint8_t *h_out = nullptr;
     size_t h_out_cap = 0;
+    uint8_t *h_map = nullptr;  // mapped pinned output of small compiles (copy_out_kernel)
+    size_t h_map_cap = 0;
     DeviceHeader *h_hdr = nullptr;
 
     cudaEvent_t ev_start = nullptr, ev_h2d = nullptr, ev_end = nullptr;
@@ -72,6 +74,15 @@ struct gp_ctx {
     uint64_t *d_dbg = nullptr;  // experiments only (option 99, bit 2)
     uint64_t *d_bases = nullptr;  // [8] zero bases in / scratch bases out (unpipelined compiles)
     int pipeline = -1;            // GP_OPT_PIPELINE: -1 auto, 0 off, 1 on
+    // CUDA graph of the device pipeline, keyed by the launch plan's bytes: a
+    // plan seen twice in a row is captured once and then relaunched as one
+    // graph (repeated compiles of one circuit shape: the JIT case).
+    struct {
+        uint64_t key = 0, pending = 0;
+        cudaGraphExec_t exec = nullptr;
+        int launches = 0;
+        bool used = false;  // the last compile ran as the graph (no per-stage events)
+    } graph;
     gp::PipeState *pipe = nullptr;
 };
 
@@ -242,6 +253,65 @@ struct HostOut {
     uint32_t *det_ids, *obs_ids;
 };
 
+uint64_t plan_key(const DevPlan &p) {
+    const unsigned char *b = reinterpret_cast<const unsigned char *>(&p);
+    uint64_t h = 0xcbf29ce484222325ull;
+    for (size_t i = 0; i < sizeof(DevPlan); i++) h = (h ^ b[i]) * 0x100000001b3ull;
+    return h;
+}
+
+// Enqueues the device pipeline of plan p: directly, or as the cached graph
+// when the same plan was launched just before (see gp_ctx::graph).
+int launch_pipeline(gp_ctx *ctx, const DevPlan &p, cudaError_t *e) {
+    auto &g = ctx->graph;
+    const uint64_t key = p.dbg ? 0 : plan_key(p);
+    g.used = false;
+    if (key && g.exec && g.key == key) {
+        *e = cudaGraphLaunch(g.exec, ctx->stream);
+        cudaEventRecord(ctx->stage_ev.reduced, ctx->stream);  // stage events are not recorded inside the graph
+        g.used = true;
+        return g.launches;
+    }
+    if (!key || g.pending != key) {
+        g.pending = key;
+        return gp::enqueue_pipeline(p, ctx->stream, &ctx->stage_ev, nullptr, e);
+    }
+    cudaGraph_t graph = nullptr;
+    *e = cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal);
+    if (*e != cudaSuccess) return 0;
+    cudaError_t le = cudaSuccess;
+    const int n = gp::enqueue_pipeline(p, ctx->stream, nullptr, nullptr, &le);
+    *e = cudaStreamEndCapture(ctx->stream, &graph);
+    if (*e == cudaSuccess && le != cudaSuccess) *e = le;
+    if (*e != cudaSuccess) {
+        if (graph) cudaGraphDestroy(graph);
+        return 0;
+    }
+    bool updated = false;
+    if (g.exec) {
+        cudaGraphExecUpdateResultInfo info;
+        updated = cudaGraphExecUpdate(g.exec, graph, &info) == cudaSuccess;
+        if (!updated) {
+            cudaGetLastError();
+            cudaGraphExecDestroy(g.exec);
+            g.exec = nullptr;
+        }
+    }
+    if (!updated) *e = cudaGraphInstantiate(&g.exec, graph, 0);
+    cudaGraphDestroy(graph);
+    if (*e != cudaSuccess) {
+        g.exec = nullptr;
+        g.key = 0;
+        return 0;
+    }
+    g.key = key;
+    g.launches = n;
+    *e = cudaGraphLaunch(g.exec, ctx->stream);
+    cudaEventRecord(ctx->stage_ev.reduced, ctx->stream);
+    g.used = true;
+    return n;
+}
+
 gp_status run_batch(gp_ctx *ctx, const gp_circuit_view *cs, size_t count, uint8_t level, HostOut &ho,
                     DeviceHeader &hdr, gp_stats *stats) {
     const auto t0 = clk::now();
@@ -354,17 +424,52 @@ gp_status run_batch(gp_ctx *ctx, const gp_circuit_view *cs, size_t count, uint8_
         carve(ctx, p, t, ctx->d_ws, K, ids_cap, pool, slabs, items_cap, true);
         p.base_in = ctx->d_bases;
         p.base_out = ctx->d_bases + 4;
+        // Small outputs go straight to mapped host memory (one wait, no round trip).
+        {
+            size_t mo = 0;
+            auto mtake = [&](size_t bytes) {
+                const size_t at = mo;
+                mo = (size_t)align16(mo + bytes);
+                return at;
+            };
+            const size_t m_hdr = mtake(sizeof(DeviceHeader)), m_det_off = mtake((p.e_cap + 1) * 8),
+                         m_obs_off = mtake((p.e_cap + 1) * 8), m_prob = mtake(p.e_cap * 8),
+                         m_det = mtake(p.ids_cap * 4), m_obs = mtake(p.ids_cap * 4), m_edge = mtake((t.C + 1) * 8);
+            p.out_mapped = mo <= (size_t(128) << 20);
+            if (p.out_mapped && ctx->h_map_cap < mo) {
+                if (ctx->h_map) cudaFreeHost(ctx->h_map);
+                ctx->h_map = nullptr;
+                ctx->h_map_cap = 0;
+                if (cudaHostAlloc(&ctx->h_map, mo + mo / 4, cudaHostAllocMapped) == cudaSuccess) {
+                    ctx->h_map_cap = mo + mo / 4;
+                } else {
+                    cudaGetLastError();
+                    p.out_mapped = 0;
+                }
+            }
+            if (p.out_mapped) {
+                p.hmap.hdr = (DeviceHeader *)(ctx->h_map + m_hdr);
+                p.hmap.det_off = (uint64_t *)(ctx->h_map + m_det_off);
+                p.hmap.obs_off = (uint64_t *)(ctx->h_map + m_obs_off);
+                p.hmap.probs = (double *)(ctx->h_map + m_prob);
+                p.hmap.det_ids = (uint32_t *)(ctx->h_map + m_det);
+                p.hmap.obs_ids = (uint32_t *)(ctx->h_map + m_obs);
+                p.hmap.edge_off = (uint64_t *)(ctx->h_map + m_edge);
+            }
+        }
         if (ctx->trav_debug & 4) {  // experiments: per-step walk timestamps of every CTA
             if (!ctx->d_dbg) cudaMalloc(&ctx->d_dbg, (size_t)8192 * 512 * 4 * 8);
             cudaMemsetAsync(ctx->d_dbg, 0, (size_t)8192 * 512 * 4 * 8, ctx->stream);
             p.dbg = t.groups <= 8192 ? ctx->d_dbg : nullptr;
         }
-        launches += gp::enqueue_pipeline(p, ctx->stream, &ctx->stage_ev, nullptr, &e);
+        launches += launch_pipeline(ctx, p, &e);
         if (e != cudaSuccess) return cuda_fail(ctx, e, "kernel launch");
-        e = cudaMemcpyAsync(ctx->h_hdr, p.hdr, sizeof(DeviceHeader), cudaMemcpyDeviceToHost, ctx->stream);
+        if (!p.out_mapped)
+            e = cudaMemcpyAsync(ctx->h_hdr, p.hdr, sizeof(DeviceHeader), cudaMemcpyDeviceToHost, ctx->stream);
+        cudaEventRecord(ctx->ev_end, ctx->stream);
         if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
         if (e != cudaSuccess) return cuda_fail(ctx, e, "device pipeline");
-        hdr = *ctx->h_hdr;
+        hdr = p.out_mapped ? *p.hmap.hdr : *ctx->h_hdr;
         if (attempt > 4) return fail(ctx, GP_ERR_CUDA, "capacity retry loop did not converge");
         if (hdr.items_overflow) {  // more nonempty signatures than items: use every source
             items_cap = t.sources + 16;
@@ -403,6 +508,37 @@ gp_status run_batch(gp_ctx *ctx, const gp_circuit_view *cs, size_t count, uint8_
             }
     }
     const uint64_t E = hdr.num_edges, nd = hdr.num_det_ids, no = hdr.num_obs_ids;
+    if (p.out_mapped) {  // already in mapped host memory
+        ho.det_off = p.hmap.det_off;
+        ho.obs_off = p.hmap.obs_off;
+        ho.probs = p.hmap.probs;
+        ho.det_ids = p.hmap.det_ids;
+        ho.obs_ids = p.hmap.obs_ids;
+        ho.edge_off = p.hmap.edge_off;
+        if (stats) {
+            const double h2d = elapsed_ms(ctx->ev_start, ctx->ev_h2d);
+            const bool g = ctx->graph.used;
+            const double low = g ? 0 : elapsed_ms(ctx->ev_h2d, ctx->stage_ev.lowered);
+            const double trav = g ? 0 : elapsed_ms(ctx->stage_ev.lowered, ctx->stage_ev.traversed);
+            const double red = g ? elapsed_ms(ctx->ev_h2d, ctx->stage_ev.reduced)
+                                 : elapsed_ms(ctx->stage_ev.traversed, ctx->stage_ev.reduced);
+            const double out_ms = elapsed_ms(ctx->stage_ev.reduced, ctx->ev_end);
+            *stats = gp_stats{};
+            stats->h2d_ns = (uint64_t)(h2d * 1e6);
+            stats->lower_ns = pack_ns + (uint64_t)((h2d + low) * 1e6);
+            stats->traverse_ns = (uint64_t)(trav * 1e6);
+            stats->traverse_kernel_ns = (uint64_t)(trav * 1e6);
+            stats->reduce_ns = (uint64_t)((red + out_ms) * 1e6);
+            stats->kernel_ns = (uint64_t)((low + trav + red) * 1e6);  // includes the mapped-output copy
+            stats->d2h_ns = (uint64_t)(out_ms * 1e6);
+            stats->num_sources = t.sources;
+            stats->h2d_bytes = L.total;
+            stats->d2h_bytes = sizeof(DeviceHeader) + (E + 1) * 16 + E * 8 + (nd + no) * 4 + (count + 1) * 8;
+            stats->kernel_launches = (uint64_t)launches;
+            stats->total_ns = ns_since(t0);
+        }
+        return GP_OK;
+    }
     size_t o = 0;
     auto take = [&](size_t bytes) {
         const size_t at = o;
@@ -433,9 +569,11 @@ gp_status run_batch(gp_ctx *ctx, const gp_circuit_view *cs, size_t count, uint8_
     ho.edge_off = (uint64_t *)(ctx->h_out + o_edge);
     if (stats) {
         const double h2d = elapsed_ms(ctx->ev_start, ctx->ev_h2d);
-        const double low = elapsed_ms(ctx->ev_h2d, ctx->stage_ev.lowered);
-        const double trav = elapsed_ms(ctx->stage_ev.lowered, ctx->stage_ev.traversed);
-        const double red = elapsed_ms(ctx->stage_ev.traversed, ctx->stage_ev.reduced);
+        const bool g = ctx->graph.used;  // one graph launch: device time without the stage split
+        const double low = g ? 0 : elapsed_ms(ctx->ev_h2d, ctx->stage_ev.lowered);
+        const double trav = g ? 0 : elapsed_ms(ctx->stage_ev.lowered, ctx->stage_ev.traversed);
+        const double red = g ? elapsed_ms(ctx->ev_h2d, ctx->stage_ev.reduced)
+                             : elapsed_ms(ctx->stage_ev.traversed, ctx->stage_ev.reduced);
         const double d2h_ms = elapsed_ms(ctx->stage_ev.reduced, ctx->ev_end);
         *stats = gp_stats{};
         stats->h2d_ns = (uint64_t)(h2d * 1e6);
@@ -841,11 +979,13 @@ void gp_ctx_destroy(gp_ctx *ctx) {
     cudaStreamSynchronize(ctx->stream);
     if (ctx->h_stage) cudaFreeHost(ctx->h_stage);
     if (ctx->h_out) cudaFreeHost(ctx->h_out);
+    if (ctx->h_map) cudaFreeHost(ctx->h_map);
     if (ctx->h_hdr) cudaFreeHost(ctx->h_hdr);
     if (ctx->d_img) cudaFree(ctx->d_img);
     if (ctx->d_ws) cudaFree(ctx->d_ws);
     if (ctx->d_flush) cudaFree(ctx->d_flush);
     if (ctx->d_bases) cudaFree(ctx->d_bases);
+    if (ctx->graph.exec) cudaGraphExecDestroy(ctx->graph.exec);
     gp::pipe_destroy(ctx->pipe);
     for (cudaEvent_t ev : ctx->prof)
         if (ev) cudaEventDestroy(ev);

@@ -92,6 +92,16 @@ struct DevPlan {
     const uint64_t *base_in;          // [4] edges, detector ids, observable ids, circuits before this compile
     uint64_t *base_out;               // [4] the same after it
     DeviceHeader *hdr_out;            // final header copy (output region, or mapped host memory)
+    // Mapped output (small compiles): copy_out_kernel moves the output region
+    // and the header straight into mapped pinned host memory, so the host
+    // waits once and reads everything there (no header round trip).
+    struct {
+        uint64_t *det_off, *obs_off, *edge_off;
+        double *probs;
+        uint32_t *det_ids, *obs_ids;
+        DeviceHeader *hdr;
+    } hmap;
+    uint32_t out_mapped;
     DeviceHeader *hdr;
     uint64_t *dbg;  // experiments only (TravCfg.debug bit 2): per-step walk timestamps
 };

@@ -16,6 +16,9 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <mutex>
+#include <set>
+#include <utility>
 
 #include "gp_device.h"
 
@@ -423,6 +426,23 @@ void launch_scan(F f, uint64_t n, uint4 *bsum, uint4 *out, uint4 *total, cudaStr
 
 uint32_t blocks_for(uint64_t n, uint32_t tpb) { return (uint32_t)((n + tpb - 1) / tpb); }
 
+// Opt a kernel into the device's full dynamic shared memory once per
+// (function, device), not once per launch (a host call on the latency path).
+template <class K>
+void smem_optin(K kern) {
+    static std::mutex mu;
+    static std::set<std::pair<const void *, int>> done;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> g(mu);
+    if (!done.insert({reinterpret_cast<const void *>(kern), dev}).second) return;
+    int optin = 0;
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    cudaFuncAttributes fa{};
+    cudaFuncGetAttributes(&fa, kern);  // static shared memory counts against the opt-in limit
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - (int)fa.sharedSizeBytes);
+}
+
 constexpr uint32_t kWalkNpl = 4;  // target nodes per walk thread (issue-bound: more warps)
 
 template <int WPC, class F>
@@ -564,7 +584,7 @@ int enqueue_pipeline(const DevPlan &p, cudaStream_t st, const StageEvents *ev, c
     // K2 traversal.
     if (p.tot.groups && p.trav.split) {
         auto launch = [&](auto kern) {
-            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.trav_smem);
+            smem_optin(kern);
             kern<<<(uint32_t)p.tot.groups, p.trav.walk_threads, p.trav_smem, st>>>(p, p.trav);
         };
         walk_dispatch(p.trav.walk_threads / 32, p.trav.walk_npt, launch);
@@ -576,7 +596,7 @@ int enqueue_pipeline(const DevPlan &p, cudaStream_t st, const StageEvents *ev, c
         const int threads = 32 * (1 + (int)c.node_warps + (int)c.emit_warps);
         const uint32_t tm = c.T <= 1 ? 1 : c.T <= 2 ? 2 : c.T <= 4 ? 4 : 8;
         auto launch = [&](auto kern) {
-            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.trav_smem);
+            smem_optin(kern);
             kern<<<(uint32_t)p.tot.groups, threads, p.trav_smem, st>>>(p, c);
         };
         if (tm == 1) launch(trav::traverse_kernel<1>);
@@ -608,11 +628,7 @@ int enqueue_pipeline(const DevPlan &p, cudaStream_t st, const StageEvents *ev, c
         const uint64_t ctas = (NB + red::kBucketThreads / 32 - 1) / (red::kBucketThreads / 32);
         red::bucket_kernel<<<(uint32_t)std::min<uint64_t>(std::max<uint64_t>(ctas, 1), 148 * 32),
                              red::kBucketThreads, 0, st>>>(p);
-        static bool attr = false;  // once per process (the device attribute is per function)
-        if (!attr) {
-            cudaFuncSetAttribute(red::huge_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)red::kHugeSmem);
-            attr = true;
-        }
+        smem_optin(red::huge_kernel);
         red::huge_kernel<<<kHugeCtas, 256, red::kHugeSmem, st>>>(p);
         launches += 2;
     }
@@ -626,6 +642,7 @@ int enqueue_pipeline(const DevPlan &p, cudaStream_t st, const StageEvents *ev, c
         launches++;
     }
     mark(kProfWrite);
+    if (p.out_mapped) red::copy_out_kernel<<<32, 256, 0, st>>>(p), launches++;
     if (ev) cudaEventRecord(ev->reduced, st);
     *err = cudaGetLastError();
     return launches;

@@ -928,4 +928,24 @@ __global__ void write_kernel(__grid_constant__ const DevPlan p, const uint4 *out
     }
 }
 
+// Mapped output: the output region and the header into mapped pinned host
+// memory (coalesced stores over PCIe; sizes from the device header).
+__global__ void copy_out_kernel(__grid_constant__ const DevPlan p) {
+    const DeviceHeader hd = *p.hdr;
+    const bool ok = hd.num_det_ids != 0xFFFFFFFFu && !hd.items_overflow && !hd.record_overflow && !hd.pool_overflow;
+    const uint64_t E = hd.num_edges, nd = ok ? hd.num_det_ids : 0, no = hd.num_obs_ids, C = p.tot.C;
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x, t0 = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (ok) {
+        for (uint64_t i = t0; i <= E; i += stride) {
+            p.hmap.det_off[i] = p.o_det_off[i];
+            p.hmap.obs_off[i] = p.o_obs_off[i];
+            if (i < E) p.hmap.probs[i] = p.o_prob[i];
+        }
+        for (uint64_t i = t0; i < nd; i += stride) p.hmap.det_ids[i] = p.o_det[i];
+        for (uint64_t i = t0; i < no; i += stride) p.hmap.obs_ids[i] = p.o_obs[i];
+        for (uint64_t i = t0; i <= C; i += stride) p.hmap.edge_off[i] = p.o_edge_off[i];
+    }
+    if (t0 == 0) *p.hmap.hdr = hd;
+}
+
 }  // namespace red
