@@ -324,9 +324,9 @@ gp_status run_batch(gp_ctx *ctx, const gp_circuit_view *cs, size_t count, uint8_
     for (size_t c = 0; c < count; c++)
         ops += (uint64_t)(cs[c].gate_offsets[cs[c].num_layers] - cs[c].gate_offsets[0]) +
                (cs[c].noise_offsets[cs[c].num_layers] - cs[c].noise_offsets[0]);
-    if (!ctx->pool && ops >= (1u << 16))
+    if (!ctx->pool && ops >= (1u << 14))
         ctx->pool = std::make_unique<gp::HostPool>(std::max(1u, std::thread::hardware_concurrency()) - 1);
-    gp::HostPool *hpool = ops >= (1u << 16) ? ctx->pool.get() : nullptr;
+    gp::HostPool *hpool = ops >= (1u << 14) ? ctx->pool.get() : nullptr;
     gp::pack_plan(hpool, cs, count, level, pp);
     if (pp.err == gp::kPackIndexSpace || pp.err == gp::kPackTooWide) {
         // Circuits before the first index-space failure may still hold leaf

@@ -90,7 +90,7 @@ uint64_t bits_of(double d) {
     return b;
 }
 
-constexpr uint64_t kTaskOps = 1 << 15;  // ops (gates + noise, or list entries) per task
+constexpr uint64_t kTaskOps = 1 << 13;  // ops (gates + noise, or list entries) per task
 
 StageLayout stage_layout(const BatchTotals &t) {
     StageLayout L{};
