@@ -123,26 +123,11 @@ def shard(rank: int, world: int, per_rank: int) -> range:
 
 
 def gather_flat(dist, arrays: dict, device: str):
-    """Gathers variable-length flat DEM arrays (per-rank tables) to every rank
-    with two all_gathers per array (sizes, then padded payloads): the final
-    exchange step of SURVEY.md 8e. Returns {name: [per-rank np.ndarray]}."""
-    import numpy as np
-    import torch
-    out = {}
-    for name, a in arrays.items():
-        a = np.ascontiguousarray(a)
-        as_i64 = a.dtype in (np.uint32, np.uint64, np.int32)
-        t = torch.from_numpy(a.astype(np.int64) if as_i64 else a.astype(np.float64)).to(device)
-        n = torch.tensor([t.numel()], dtype=torch.int64, device=device)
-        sizes = [torch.zeros_like(n) for _ in range(dist.ws)]
-        dist.td.all_gather(sizes, n)
-        mx = int(max(int(x.item()) for x in sizes))
-        pad = torch.zeros(mx, dtype=t.dtype, device=device)
-        pad[:t.numel()] = t
-        parts = [torch.zeros_like(pad) for _ in range(dist.ws)]
-        dist.td.all_gather(parts, pad)
-        out[name] = [parts[r][:int(sizes[r].item())].cpu().numpy().astype(a.dtype) for r in range(dist.ws)]
-    return out
+    """Gathers variable-length flat DEM arrays (per-rank tables) to every rank:
+    the final exchange step of SURVEY.md 8e (paper_2604_16613_b200.shard).
+    Returns {name: [per-rank np.ndarray]}."""
+    from paper_2604_16613_b200.shard import gather_flat as g
+    return g(arrays, device)
 
 
 def build_branches(first: int, count: int):

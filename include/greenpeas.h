@@ -153,6 +153,38 @@ gp_status gp_compile(gp_ctx *ctx, const gp_circuit_view *circuit, uint8_t level,
 gp_status gp_compile_batch(gp_ctx *ctx, const gp_circuit_view *circuits, size_t count,
                            uint8_t level, gp_dem_batch_view *out, gp_stats *stats);
 
+/* Fault-range sharding of ONE circuit: shard k of n owns the
+ * error sources placed in layers [l*k/n, l*(k+1)/n) -- noise ops of those
+ * layers and the outcome flips of their measurements. gp_compile_shard walks
+ * the circuit (Alg. 1) down to the shard's first layer and emits only the
+ * shard's sources, as a PARTIAL TABLE: every nonempty signature with its own
+ * probability (unfolded, so a merge is bit-exact: dem.cpp:97-106 folds a
+ * group's sorted member probabilities). `memory` chooses where the table is
+ * returned: GP_MEM_HOST (pinned host memory) or GP_MEM_DEVICE (the context's
+ * device memory, ready for an NCCL gather over NVLink).
+ * gp_merge_partials reduces the union of the shards' tables (any order; each
+ * part's arrays on the host or on the context's device, per part.memory)
+ * into the circuit's DEM -- identical to gp_compile of the whole circuit.
+ * Views stay valid until the next call on ctx; merge inputs may be views
+ * returned by this ctx. See paper_2604_16613_b200/shard.py. */
+enum { GP_MEM_HOST = 0, GP_MEM_DEVICE = 1 };
+typedef struct gp_partial_view {
+    uint32_t num_detectors;
+    uint32_t num_observables;
+    uint64_t num_sources;         /* nonempty signatures of the shard */
+    uint64_t num_records;
+    uint32_t memory;              /* GP_MEM_HOST or GP_MEM_DEVICE */
+    uint32_t reserved;
+    const double *probs;          /* [num_sources] */
+    const uint32_t *rec_offsets;  /* [num_sources + 1] into rec_words / rec_bits */
+    const uint32_t *rec_words;    /* [num_records] 64-bit id word (ids 64w .. 64w+63) */
+    const uint64_t *rec_bits;     /* [num_records] its bits; detector d = bit d, observable o = bit D+o */
+} gp_partial_view;
+gp_status gp_compile_shard(gp_ctx *ctx, const gp_circuit_view *circuit, uint8_t level, uint32_t shard,
+                           uint32_t nshards, uint32_t memory, gp_partial_view *out, gp_stats *stats);
+gp_status gp_merge_partials(gp_ctx *ctx, const gp_partial_view *parts, size_t nparts, gp_dem_view *out,
+                            gp_stats *stats);
+
 /* Benchmark hooks (not part of the reference API). gp_replay re-runs the
  * device pipeline `iterations` times on the batch uploaded by the last
  * successful compile on this context: inputs already resident in HBM, outputs

@@ -15,8 +15,10 @@ from .api import (  # noqa: F401
     Compiler,
     CorrelationLevel,
     Dem,
+    DevicePartialTable,
     GenCircuit,
     GreenpeasError,
+    PartialTable,
     algorithmic_bytes,
     circuit_metrics,
     compile_circuit,

@@ -50,6 +50,14 @@ class DemBatchView(C.Structure):
     ]
 
 
+class PartialView(C.Structure):
+    _fields_ = [
+        ("num_detectors", C.c_uint32), ("num_observables", C.c_uint32), ("num_sources", C.c_uint64),
+        ("num_records", C.c_uint64), ("memory", C.c_uint32), ("reserved", C.c_uint32), ("probs", _f64p), ("rec_offsets", _u32p), ("rec_words", _u32p),
+        ("rec_bits", _u64p),
+    ]
+
+
 class Metrics(C.Structure):
     _fields_ = [(n, C.c_uint64) for n in ("base_nodes", "succ_refs", "source_rows", "sources", "words",
                                           "measurements")]
@@ -83,6 +91,10 @@ def lib() -> C.CDLL:
         L.gp_compile.argtypes = [vp, C.POINTER(CircuitView), C.c_uint8, C.POINTER(DemView), C.POINTER(Stats)]
         L.gp_compile_batch.argtypes = [vp, C.POINTER(CircuitView), C.c_size_t, C.c_uint8,
                                        C.POINTER(DemBatchView), C.POINTER(Stats)]
+        L.gp_compile_shard.argtypes = [vp, C.POINTER(CircuitView), C.c_uint8, C.c_uint32, C.c_uint32,
+                                       C.c_uint32, C.POINTER(PartialView), C.POINTER(Stats)]
+        L.gp_merge_partials.argtypes = [vp, C.POINTER(PartialView), C.c_size_t, C.POINTER(DemView),
+                                        C.POINTER(Stats)]
         L.gp_replay.argtypes = [vp, C.c_uint32, C.c_int, C.POINTER(Stats)]
         L.gp_profile_stages.argtypes = [vp, C.POINTER(C.c_uint64), C.POINTER(C.c_char_p), C.c_int]
         L.gp_circuit_metrics.argtypes = [C.POINTER(CircuitView), C.c_uint8, C.POINTER(Metrics)]

@@ -29,6 +29,7 @@ class CorrelationLevel(IntEnum):  # stepg.hpp:28
 
 GP_OK, GP_ERR_INVALID_ARGUMENT, GP_ERR_CUDA, GP_ERR_OOM, GP_ERR_NO_DEVICE, GP_ERR_UNSUPPORTED = range(6)
 OPT_FORCE_HASH_COLLISIONS, OPT_RECORD_SLOTS = 1, 2
+GP_MEM_HOST, GP_MEM_DEVICE = 0, 1
 NOISE_MODEL_PAPER, NOISE_MODEL_SI1000, NOISE_MODEL_UNIFORM = 0, 1, 2
 
 
@@ -76,6 +77,73 @@ class Dem:
         return N.take_string(p, n.value)
 
 
+@dataclass
+class PartialTable:
+    """One fault-range shard's partial table (gp_partial_view):
+    every nonempty source signature of the shard with its own probability,
+    unfolded. Records: (64-bit id word, bits) pairs, detector d = bit d,
+    observable o = bit D + o."""
+
+    num_detectors: int
+    num_observables: int
+    probs: np.ndarray        # f64 [n]
+    rec_offsets: np.ndarray  # u32 [n + 1]
+    rec_words: np.ndarray    # u32 [r]
+    rec_bits: np.ndarray     # u64 [r]
+
+    @property
+    def num_sources(self) -> int:
+        return len(self.probs)
+
+    def view(self):
+        arrs = (np.ascontiguousarray(self.probs, np.float64), np.ascontiguousarray(self.rec_offsets, np.uint32),
+                np.ascontiguousarray(self.rec_words, np.uint32), np.ascontiguousarray(self.rec_bits, np.uint64))
+        arrs = tuple(a if a.size else np.zeros(1, a.dtype) for a in arrs)
+        v = N.PartialView(self.num_detectors, self.num_observables, len(self.probs), len(self.rec_words),
+                          GP_MEM_HOST, 0, N.ptr(arrs[0], N._f64p), N.ptr(arrs[1], N._u32p),
+                          N.ptr(arrs[2], N._u32p), N.ptr(arrs[3], N._u64p))
+        return v, arrs
+
+
+class _CudaArray:
+    """A raw device range as __cuda_array_interface__ (torch.as_tensor wraps it
+    without a copy). Unsigned ids travel as same-width signed integers."""
+
+    def __init__(self, ptr: int, n: int, typestr: str):
+        self.__cuda_array_interface__ = {"shape": (n,), "typestr": typestr, "data": (int(ptr or 0), False),
+                                         "version": 3, "strides": None}
+
+
+@dataclass
+class DevicePartialTable:
+    """A partial table in device memory (GP_MEM_DEVICE) as torch tensors:
+    probs f64, rec_offsets / rec_words int32 (u32 bits), rec_bits int64 (u64
+    bits). Tensors returned by compile_shard(on_device=True) are views of the
+    compiler's workspace: valid until its next call (clone to keep)."""
+
+    num_detectors: int
+    num_observables: int
+    probs: object
+    rec_offsets: object
+    rec_words: object
+    rec_bits: object
+
+    @property
+    def num_sources(self) -> int:
+        return int(self.probs.numel())
+
+    def arrays(self) -> dict:
+        return {"probs": self.probs, "rec_offsets": self.rec_offsets, "rec_words": self.rec_words,
+                "rec_bits": self.rec_bits}
+
+    def view(self):
+        ts = tuple(t.contiguous() for t in (self.probs, self.rec_offsets, self.rec_words, self.rec_bits))
+        v = N.PartialView(self.num_detectors, self.num_observables, ts[0].numel(), ts[2].numel(), GP_MEM_DEVICE, 0,
+                          C.cast(C.c_void_p(ts[0].data_ptr()), N._f64p), C.cast(C.c_void_p(ts[1].data_ptr()), N._u32p),
+                          C.cast(C.c_void_p(ts[2].data_ptr()), N._u32p), C.cast(C.c_void_p(ts[3].data_ptr()), N._u64p))
+        return v, ts
+
+
 def _dem_from_view(v, lo: int, hi: int, nd: int, no: int) -> Dem:
     E = hi - lo
     doff = N.copy_u64(v.det_offsets, v.num_edges + 1) if v.num_edges else np.zeros(1, np.uint64)
@@ -94,6 +162,7 @@ class Compiler:
     def __init__(self, device: int = 0):
         self._lib = N.lib()
         self._ctx = C.c_void_p()
+        self.device = int(device)
         st = self._lib.gp_ctx_create(int(device), C.byref(self._ctx))
         if st != GP_OK:
             raise GreenpeasError(f"gp_ctx_create(device={device}) failed with status {st} "
@@ -127,6 +196,55 @@ class Compiler:
         out = N.DemView()
         st = N.Stats()
         self._check(self._lib.gp_compile(self._ctx, C.byref(v), int(level), C.byref(out), C.byref(st)))
+        self.last_stats = st.as_dict()
+        return _dem_from_view(out, 0, int(out.num_edges), out.num_detectors, out.num_observables)
+
+    def compile_shard(self, circuit, shard: int, nshards: int, level=CorrelationLevel.L0,
+                      on_device: bool = False):
+        """Fault-range shard `shard` of `nshards` (layers [l*k/n, l*(k+1)/n))
+        of one circuit as a partial table (gp_compile_shard): a PartialTable
+        in host memory, or with on_device a DevicePartialTable (torch views of
+        the device workspace, ready for an NCCL gather)."""
+        v, keep = circuit.view() if hasattr(circuit, "view") else N.view_of(circuit)
+        out = N.PartialView()
+        st = N.Stats()
+        mem = GP_MEM_DEVICE if on_device else GP_MEM_HOST
+        self._check(self._lib.gp_compile_shard(self._ctx, C.byref(v), int(level), int(shard), int(nshards), mem,
+                                               C.byref(out), C.byref(st)))
+        self.last_stats = st.as_dict()
+        n, r = int(out.num_sources), int(out.num_records)
+        if on_device:
+            import torch
+            dev = torch.device("cuda", self.device)
+
+            def wrap(ptr, count, ts):
+                if count == 0:
+                    return torch.zeros(0, dtype={"<f8": torch.float64, "<i4": torch.int32,
+                                                 "<i8": torch.int64}[ts], device=dev)
+                return torch.as_tensor(_CudaArray(C.cast(ptr, C.c_void_p).value, count, ts), device=dev)
+            return DevicePartialTable(int(out.num_detectors), int(out.num_observables), wrap(out.probs, n, "<f8"),
+                                      wrap(out.rec_offsets, n + 1, "<i4"), wrap(out.rec_words, r, "<i4"),
+                                      wrap(out.rec_bits, r, "<i8"))
+        return PartialTable(
+            int(out.num_detectors), int(out.num_observables), N.copy_f64(out.probs, n) if n else
+            np.zeros(0, np.float64), N.copy_u32(out.rec_offsets, n + 1), N.copy_u32(out.rec_words, r) if r else
+            np.zeros(0, np.uint32), N.copy_u64(out.rec_bits, r) if r else np.zeros(0, np.uint64))
+
+    def merge_partials(self, parts: list) -> Dem:
+        """The DEM of the union of partial tables (gp_merge_partials): equal to
+        compile() of the whole circuit when the parts cover every shard."""
+        arr = (N.PartialView * len(parts))()
+        keep = []
+        if any(isinstance(t, DevicePartialTable) for t in parts):
+            import torch
+            torch.cuda.synchronize(self.device)  # producers of device tables ran on torch's streams
+        for i, t in enumerate(parts):
+            v, k = t.view()
+            arr[i] = v
+            keep.append(k)
+        out = N.DemView()
+        st = N.Stats()
+        self._check(self._lib.gp_merge_partials(self._ctx, arr, len(parts), C.byref(out), C.byref(st)))
         self.last_stats = st.as_dict()
         return _dem_from_view(out, 0, int(out.num_edges), out.num_detectors, out.num_observables)
 

@@ -73,6 +73,8 @@ struct gp_ctx {
     uint8_t *d_flush = nullptr;
     uint64_t *d_dbg = nullptr;  // experiments only (option 99, bit 2)
     uint64_t *d_bases = nullptr;  // [8] zero bases in / scratch bases out (unpipelined compiles)
+    uint8_t *d_merge = nullptr;   // gp_merge_partials: the parts' tables, concatenated
+    size_t d_merge_cap = 0;
     int pipeline = -1;            // GP_OPT_PIPELINE: -1 auto, 0 off, 1 on
     // CUDA graph of the device pipeline, keyed by the launch plan's bytes: a
     // plan seen twice in a row is captured once and then relaunched as one
@@ -181,6 +183,13 @@ size_t carve(gp_ctx *ctx, DevPlan &p, const BatchTotals &t, uint8_t *base, uint3
     p.e_ndno = (uint32_t *)take(items_cap * 4);
     p.e_prob = (double *)take(items_cap * 8);
     p.huge = (uint32_t *)take(NB * 4);
+    if (p.mode == gp::kModeShard) {  // compact partial table of the shard
+        p.p_prob = (double *)take(S * 8);
+        p.p_roff = (uint32_t *)take(S * 4 + 4);
+        p.p_word = (uint32_t *)take(S * K * 4);
+        p.p_bits = (uint64_t *)take(S * K * 8);
+        p.p_scan = (uint4 *)take(S * 16 + 16);
+    }
     p.ids_cap = ids_cap;
     p.bsum = (uint4 *)take(nb * 16);
     p.bsum_cap = nb;
@@ -312,8 +321,18 @@ int launch_pipeline(gp_ctx *ctx, const DevPlan &p, cudaError_t *e) {
     return n;
 }
 
+// Partial table of a shard compile (gp_compile_shard), in ctx-owned pinned memory.
+struct PartialOut {
+    bool on_device = false;  // in: leave the table in device memory
+    uint64_t n = 0, r = 0;
+    double *prob = nullptr;
+    uint32_t *roff = nullptr, *word = nullptr;
+    uint64_t *bits = nullptr;
+};
+
 gp_status run_batch(gp_ctx *ctx, const gp_circuit_view *cs, size_t count, uint8_t level, HostOut &ho,
-                    DeviceHeader &hdr, gp_stats *stats) {
+                    DeviceHeader &hdr, gp_stats *stats, uint32_t mode = gp::kModeFull, uint32_t sh_lo = 0,
+                    uint32_t sh_hi = 0xFFFFFFFFu, PartialOut *part = nullptr) {
     const auto t0 = clk::now();
     if (level > 2) return fail(ctx, GP_ERR_INVALID_ARGUMENT, "correlation level must be 0, 1 or 2");
     if (cudaSetDevice(ctx->device) != cudaSuccess) return fail(ctx, GP_ERR_CUDA, "cudaSetDevice failed");
@@ -419,6 +438,9 @@ gp_status run_batch(gp_ctx *ctx, const gp_circuit_view *cs, size_t count, uint8_
         p.trav = tcfg;
         p.trav.debug = ctx->trav_debug;
         p.trav_smem = tsmem;
+        p.mode = mode;
+        p.shard_lo = sh_lo;
+        p.shard_hi = sh_hi;
         const size_t need = carve(ctx, p, t, nullptr, K, ids_cap, pool, slabs, items_cap, true);
         if ((st = ensure_device(ctx, &ctx->d_ws, &ctx->d_ws_cap, need)) != GP_OK) return st;
         carve(ctx, p, t, ctx->d_ws, K, ids_cap, pool, slabs, items_cap, true);
@@ -435,7 +457,7 @@ gp_status run_batch(gp_ctx *ctx, const gp_circuit_view *cs, size_t count, uint8_
             const size_t m_hdr = mtake(sizeof(DeviceHeader)), m_det_off = mtake((p.e_cap + 1) * 8),
                          m_obs_off = mtake((p.e_cap + 1) * 8), m_prob = mtake(p.e_cap * 8),
                          m_det = mtake(p.ids_cap * 4), m_obs = mtake(p.ids_cap * 4), m_edge = mtake((t.C + 1) * 8);
-            p.out_mapped = mo <= (size_t(128) << 20);
+            p.out_mapped = mode == gp::kModeFull && mo <= (size_t(128) << 20);
             if (p.out_mapped && ctx->h_map_cap < mo) {
                 if (ctx->h_map) cudaFreeHost(ctx->h_map);
                 ctx->h_map = nullptr;
@@ -506,6 +528,52 @@ gp_status run_batch(gp_ctx *ctx, const gp_circuit_view *cs, size_t count, uint8_
                 std::fwrite(h.data(), 8, h.size(), f);
                 std::fclose(f);
             }
+    }
+    if (mode == gp::kModeShard) {  // the partial table: sources hdr.num_edges, records hdr.num_det_ids
+        const uint64_t n = hdr.num_edges, r = hdr.num_det_ids;
+        part->n = n;
+        part->r = r;
+        if (stats) {
+            *stats = gp_stats{};
+            stats->num_sources = t.sources;
+            stats->h2d_bytes = L.total;
+            stats->kernel_ns = (uint64_t)(elapsed_ms(ctx->ev_h2d, ctx->ev_end) * 1e6);
+            stats->kernel_launches = (uint64_t)launches;
+        }
+        if (part->on_device) {
+            part->prob = p.p_prob;
+            part->roff = p.p_roff;
+            part->word = p.p_word;
+            part->bits = p.p_bits;
+            if (stats) stats->total_ns = ns_since(t0);
+            return GP_OK;
+        }
+        size_t o = 0;
+        auto take = [&](size_t bytes) {
+            const size_t at = o;
+            o = (size_t)align16(o + bytes);
+            return at;
+        };
+        const size_t a_prob = take(n * 8), a_roff = take((n + 1) * 4), a_word = take(r * 4), a_bits = take(r * 8);
+        if ((st = ensure_host(ctx, &ctx->h_out, &ctx->h_out_cap, o)) != GP_OK) return st;
+        if (n) e = cudaMemcpyAsync(ctx->h_out + a_prob, p.p_prob, n * 8, cudaMemcpyDeviceToHost, ctx->stream);
+        if (e == cudaSuccess)
+            e = cudaMemcpyAsync(ctx->h_out + a_roff, p.p_roff, (n + 1) * 4, cudaMemcpyDeviceToHost, ctx->stream);
+        if (r && e == cudaSuccess)
+            e = cudaMemcpyAsync(ctx->h_out + a_word, p.p_word, r * 4, cudaMemcpyDeviceToHost, ctx->stream);
+        if (r && e == cudaSuccess)
+            e = cudaMemcpyAsync(ctx->h_out + a_bits, p.p_bits, r * 8, cudaMemcpyDeviceToHost, ctx->stream);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+        if (e != cudaSuccess) return cuda_fail(ctx, e, "shard download");
+        part->prob = (double *)(ctx->h_out + a_prob);
+        part->roff = (uint32_t *)(ctx->h_out + a_roff);
+        part->word = (uint32_t *)(ctx->h_out + a_word);
+        part->bits = (uint64_t *)(ctx->h_out + a_bits);
+        if (stats) {
+            stats->d2h_bytes = o;
+            stats->total_ns = ns_since(t0);
+        }
+        return GP_OK;
     }
     const uint64_t E = hdr.num_edges, nd = hdr.num_det_ids, no = hdr.num_obs_ids;
     if (p.out_mapped) {  // already in mapped host memory
@@ -984,6 +1052,7 @@ void gp_ctx_destroy(gp_ctx *ctx) {
     if (ctx->d_img) cudaFree(ctx->d_img);
     if (ctx->d_ws) cudaFree(ctx->d_ws);
     if (ctx->d_flush) cudaFree(ctx->d_flush);
+    if (ctx->d_merge) cudaFree(ctx->d_merge);
     if (ctx->d_bases) cudaFree(ctx->d_bases);
     if (ctx->graph.exec) cudaGraphExecDestroy(ctx->graph.exec);
     gp::pipe_destroy(ctx->pipe);
@@ -1061,6 +1130,211 @@ gp_status gp_compile_batch(gp_ctx *ctx, const gp_circuit_view *circuits, size_t 
     out->obs_offsets = ho.obs_off;
     out->obs_ids = ho.obs_ids;
     out->probs = ho.probs;
+    return GP_OK;
+}
+
+gp_status gp_compile_shard(gp_ctx *ctx, const gp_circuit_view *circuit, uint8_t level, uint32_t shard,
+                           uint32_t nshards, uint32_t memory, gp_partial_view *out, gp_stats *stats) {
+    ctx->err.clear();
+    if (!circuit || !out) return fail(ctx, GP_ERR_INVALID_ARGUMENT, "null argument");
+    if (memory != GP_MEM_HOST && memory != GP_MEM_DEVICE) return fail(ctx, GP_ERR_INVALID_ARGUMENT, "bad memory kind");
+    if (nshards == 0 || shard >= nshards) return fail(ctx, GP_ERR_INVALID_ARGUMENT, "shard index out of range");
+    const uint64_t l = circuit->num_layers;
+    const uint32_t lo = (uint32_t)(l * shard / nshards), hi = (uint32_t)(l * (shard + 1) / nshards);
+    HostOut ho{};
+    DeviceHeader hdr{};
+    PartialOut part;
+    part.on_device = memory == GP_MEM_DEVICE;
+    const gp_status st = run_batch(ctx, circuit, 1, level, ho, hdr, stats, gp::kModeShard, lo,
+                                   shard + 1 == nshards ? 0xFFFFFFFFu : hi, &part);
+    if (st != GP_OK) return st;
+    out->num_detectors = circuit->num_detectors;
+    out->num_observables = circuit->num_observables;
+    out->num_sources = part.n;
+    out->num_records = part.r;
+    out->memory = memory;
+    out->reserved = 0;
+    out->probs = part.prob;
+    out->rec_offsets = part.roff;
+    out->rec_words = part.word;
+    out->rec_bits = part.bits;
+    return GP_OK;
+}
+
+// The union of the shards' partial tables as ONE synthetic circuit whose
+// sources are the table entries: the parts are copied (host or device) into
+// one device buffer, unpack_kernel lays them out as the emit stage would
+// (counts, probabilities, slot-major records), and the device reduce runs
+// unchanged (mode Merge).
+gp_status gp_merge_partials(gp_ctx *ctx, const gp_partial_view *parts, size_t nparts, gp_dem_view *out,
+                            gp_stats *stats) {
+    const auto t0 = clk::now();
+    ctx->err.clear();
+    if (!parts || !out || nparts == 0) return fail(ctx, GP_ERR_INVALID_ARGUMENT, "no partial tables");
+    if (cudaSetDevice(ctx->device) != cudaSuccess) return fail(ctx, GP_ERR_CUDA, "cudaSetDevice failed");
+    const uint32_t D = parts[0].num_detectors, O = parts[0].num_observables;
+    const uint32_t W = (uint32_t)(((uint64_t)D + O + 63) / 64);
+    uint64_t S = 0, R = 0;
+    std::vector<uint4> desc(nparts);
+    for (size_t k = 0; k < nparts; k++) {
+        const gp_partial_view &v = parts[k];
+        if (v.num_detectors != D || v.num_observables != O)
+            return fail(ctx, GP_ERR_INVALID_ARGUMENT, "partial tables of different circuits");
+        if (v.memory != GP_MEM_HOST && v.memory != GP_MEM_DEVICE)
+            return fail(ctx, GP_ERR_INVALID_ARGUMENT, "bad memory kind");
+        if (!v.rec_offsets || (v.num_sources && !v.probs) || (v.num_records && (!v.rec_words || !v.rec_bits)))
+            return fail(ctx, GP_ERR_INVALID_ARGUMENT, "null partial table array");
+        desc[k] = make_uint4((uint32_t)S, (uint32_t)(S + k), (uint32_t)R, (uint32_t)v.num_records);
+        S += v.num_sources;
+        R += v.num_records;
+    }
+    if (S + nparts >= 0xFFFFFFFFull || R >= 0xFFFFFFFFull || (uint64_t)D + 1 >= 0xFFFFFFFFull)
+        return fail(ctx, GP_ERR_UNSUPPORTED, "merge exceeds 32-bit device indexing");
+
+    BatchTotals t{};
+    t.C = 1;
+    t.sources = S;
+    t.buckets = (uint64_t)D + 1;
+    t.dets = D;
+    t.obss = O;
+    t.tiles = W;
+    t.max_W = W;
+    const StageLayout L = gp::stage_layout(t);
+    // Concatenated input: probs [S] | offsets [S + parts] | words [R] | bits [R] | descriptors.
+    size_t o = 0;
+    auto take = [&](size_t bytes) {
+        const size_t at = o;
+        o = (size_t)align16(o + bytes + 16);
+        return at;
+    };
+    const size_t a_prob = take(S * 8), a_roff = take((S + nparts) * 4), a_word = take(R * 4), a_bits = take(R * 8),
+                 a_desc = take(nparts * 16);
+    gp_status st = GP_OK;
+    cudaError_t e = cudaSuccess;
+    // (the parts may be views into this ctx's workspace: copy them out first)
+    if ((st = ensure_device(ctx, &ctx->d_merge, &ctx->d_merge_cap, o)) != GP_OK) return st;
+    if ((st = ensure_host(ctx, &ctx->h_stage, &ctx->h_stage_cap, L.total + nparts * 16)) != GP_OK) return st;
+    cudaEventRecord(ctx->ev_start, ctx->stream);
+    uint8_t *m = ctx->d_merge;
+    auto cp = [&](size_t dst, const void *src, size_t bytes, uint32_t mem) {
+        if (bytes && e == cudaSuccess)
+            e = cudaMemcpyAsync(m + dst, src, bytes, mem == GP_MEM_DEVICE ? cudaMemcpyDeviceToDevice
+                                                                         : cudaMemcpyHostToDevice, ctx->stream);
+    };
+    uint64_t h2d = 0;
+    for (size_t k = 0; k < nparts; k++) {
+        const gp_partial_view &v = parts[k];
+        const uint4 d = desc[k];
+        cp(a_prob + (size_t)d.x * 8, v.probs, v.num_sources * 8, v.memory);
+        cp(a_roff + (size_t)d.y * 4, v.rec_offsets, (v.num_sources + 1) * 4, v.memory);
+        cp(a_word + (size_t)d.z * 4, v.rec_words, v.num_records * 4, v.memory);
+        cp(a_bits + (size_t)d.z * 8, v.rec_bits, v.num_records * 8, v.memory);
+        if (v.memory == GP_MEM_HOST) h2d += v.num_sources * 12 + 4 + v.num_records * 12;
+    }
+    uint8_t *h = ctx->h_stage;  // synthetic circuit image + part descriptors
+    std::memset(h, 0, L.total);
+    CircuitMeta cm{};
+    cm.D = D;
+    cm.O = O;
+    cm.W = W;
+    cm.src_noise = (uint32_t)S;
+    std::memcpy(h + L.meta, &cm, sizeof cm);
+    const uint64_t circ_src[2] = {0, S};
+    const uint32_t circ_bkt[2] = {0, D + 1};
+    std::memcpy(h + L.circ_src, circ_src, sizeof circ_src);
+    std::memcpy(h + L.circ_bkt, circ_bkt, sizeof circ_bkt);
+    std::memcpy(h + L.total, desc.data(), nparts * 16);
+    cp(a_desc, h + L.total, nparts * 16, GP_MEM_HOST);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "merge input copy");
+    if ((st = ensure_device(ctx, &ctx->d_img, &ctx->d_img_cap, L.total)) != GP_OK) return st;
+    e = cudaMemcpyAsync(ctx->d_img, h, L.total, cudaMemcpyHostToDevice, ctx->stream);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "merge upload");
+    ctx->has_plan = false;  // the staged circuit image is replaced
+
+    const uint32_t K = 16;  // record slots: the widest signature the reduce accepts
+    uint64_t ids_cap = std::max<uint64_t>(ctx->ids_hint, 3 * S + 1024);
+    const uint64_t items_cap = S + 16;
+    DevPlan p{};
+    int launches = 0;
+    DeviceHeader hdr{};
+    cudaEventRecord(ctx->ev_h2d, ctx->stream);
+    for (int attempt = 0;; attempt++) {
+        p = DevPlan{};
+        p.img = ctx->d_img;
+        p.lay = L;
+        p.tot = t;
+        p.mode = gp::kModeMerge;
+        const size_t need = carve(ctx, p, t, nullptr, K, ids_cap, 0, 0, items_cap, true);
+        if ((st = ensure_device(ctx, &ctx->d_ws, &ctx->d_ws_cap, need)) != GP_OK) return st;
+        carve(ctx, p, t, ctx->d_ws, K, ids_cap, 0, 0, items_cap, true);
+        p.base_in = ctx->d_bases;
+        p.base_out = ctx->d_bases + 4;
+        p.p_prob = (double *)(m + a_prob);
+        p.p_roff = (uint32_t *)(m + a_roff);
+        p.p_word = (uint32_t *)(m + a_word);
+        p.p_bits = (uint64_t *)(m + a_bits);
+        p.m_desc = (const uint4 *)(m + a_desc);
+        p.m_parts = (uint32_t)nparts;
+        launches += gp::enqueue_pipeline(p, ctx->stream, &ctx->stage_ev, nullptr, &e);
+        if (e != cudaSuccess) return cuda_fail(ctx, e, "kernel launch");
+        e = cudaMemcpyAsync(ctx->h_hdr, p.hdr, sizeof(DeviceHeader), cudaMemcpyDeviceToHost, ctx->stream);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+        if (e != cudaSuccess) return cuda_fail(ctx, e, "merge pipeline");
+        hdr = *ctx->h_hdr;
+        if (hdr.bad_input)
+            return fail(ctx, GP_ERR_INVALID_ARGUMENT,
+                        "malformed partial table: " + std::to_string(hdr.bad_input) +
+                            " entries without records, wider than 16 words or outside the circuit");
+        if (attempt > 4) return fail(ctx, GP_ERR_CUDA, "capacity retry loop did not converge");
+        if (hdr.num_det_ids == 0xFFFFFFFFu) {  // id capacity overflow
+            ids_cap *= 4;
+            ctx->ids_hint = ids_cap;
+            continue;
+        }
+        break;
+    }
+    const uint64_t E = hdr.num_edges, nd = hdr.num_det_ids, no = hdr.num_obs_ids;
+    size_t q = 0;
+    auto otake = [&](size_t bytes) {
+        const size_t at = q;
+        q = (size_t)align16(q + bytes);
+        return at;
+    };
+    const size_t o_det_off = otake((E + 1) * 8), o_obs_off = otake((E + 1) * 8), o_prob = otake(E * 8),
+                 o_det = otake(nd * 4), o_obs = otake(no * 4);
+    if ((st = ensure_host(ctx, &ctx->h_out, &ctx->h_out_cap, q)) != GP_OK) return st;
+    auto d2h = [&](size_t off, const void *src, size_t bytes) {
+        if (bytes && e == cudaSuccess)
+            e = cudaMemcpyAsync(ctx->h_out + off, src, bytes, cudaMemcpyDeviceToHost, ctx->stream);
+    };
+    d2h(o_det_off, p.o_det_off, (E + 1) * 8);
+    d2h(o_obs_off, p.o_obs_off, (E + 1) * 8);
+    d2h(o_prob, p.o_prob, E * 8);
+    d2h(o_det, p.o_det, nd * 4);
+    d2h(o_obs, p.o_obs, no * 4);
+    cudaEventRecord(ctx->ev_end, ctx->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "merge download");
+    out->num_detectors = D;
+    out->num_observables = O;
+    out->num_edges = E;
+    out->det_offsets = (uint64_t *)(ctx->h_out + o_det_off);
+    out->obs_offsets = (uint64_t *)(ctx->h_out + o_obs_off);
+    out->probs = (double *)(ctx->h_out + o_prob);
+    out->det_ids = (uint32_t *)(ctx->h_out + o_det);
+    out->obs_ids = (uint32_t *)(ctx->h_out + o_obs);
+    if (stats) {
+        *stats = gp_stats{};
+        stats->h2d_ns = (uint64_t)(elapsed_ms(ctx->ev_start, ctx->ev_h2d) * 1e6);
+        stats->reduce_ns = (uint64_t)(elapsed_ms(ctx->ev_h2d, ctx->stage_ev.reduced) * 1e6);
+        stats->kernel_ns = stats->reduce_ns;
+        stats->d2h_ns = (uint64_t)(elapsed_ms(ctx->stage_ev.reduced, ctx->ev_end) * 1e6);
+        stats->num_sources = S;
+        stats->h2d_bytes = h2d + L.total + nparts * 16;
+        stats->d2h_bytes = q;
+        stats->kernel_launches = (uint64_t)launches;
+        stats->total_ns = ns_since(t0);
+    }
     return GP_OK;
 }
 

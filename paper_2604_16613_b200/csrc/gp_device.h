@@ -102,9 +102,25 @@ struct DevPlan {
         DeviceHeader *hdr;
     } hmap;
     uint32_t out_mapped;
+    // Pipeline mode: kModeFull (circuit -> DEM), kModeShard (sources of
+    // layers [shard_lo, shard_hi) -> compact partial table, no reduce),
+    // kModeMerge (uploaded partial tables -> DEM: the reduce only).
+    uint32_t mode = 0, shard_lo = 0, shard_hi = 0xFFFFFFFFu;  // defaults: the whole circuit
+    double *p_prob;      // partial table (kModeShard): [S]
+    uint32_t *p_roff;    // [S + 1]
+    uint32_t *p_word;    // [S * K]
+    uint64_t *p_bits;    // [S * K]
+    uint4 *p_scan;       // [S + 1] (nonempty, records) exclusive scan
+    // kModeMerge input: the parts' tables concatenated (p_prob [S], p_roff
+    // [S + parts], p_word / p_bits [R]); part k = (first source, first
+    // offset, first record, records) in m_desc[k].
+    const uint4 *m_desc;
+    uint32_t m_parts;
     DeviceHeader *hdr;
     uint64_t *dbg;  // experiments only (TravCfg.debug bit 2): per-step walk timestamps
 };
+
+enum PipeMode : uint32_t { kModeFull = 0, kModeShard = 1, kModeMerge = 2 };
 
 struct StageEvents {
     cudaEvent_t lowered, traversed, reduced;

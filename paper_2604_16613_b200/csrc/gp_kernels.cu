@@ -383,6 +383,15 @@ struct BucketScanF {
     __device__ uint4 operator()(uint64_t b) const { return make_uint4(bcount[b], 0, 0, 0); }
 };
 
+struct PartialScanF {  // (nonempty sources, records) in source order
+    const uint32_t *cnt;
+    __device__ bool active(uint64_t) const { return true; }
+    __device__ uint4 operator()(uint64_t s) const {
+        const uint32_t n = cnt[s];
+        return make_uint4(n ? 1u : 0u, n, 0, 0);
+    }
+};
+
 struct OutScanF {  // (edges, detector ids, observable ids) per bucket, in canonical order
     const uint32_t *ecount;
     const uint2 *eids;
@@ -399,6 +408,70 @@ struct ZeroRanges {
     uint64_t n16[8];  // 16-byte units
     int count;
 };
+
+// Shard mode: the nonempty sources' probabilities and records, compacted in
+// source order (the partial table a merge consumes); header = (sources, records).
+__global__ void partial_kernel(__grid_constant__ const DevPlan p) {
+    const uint64_t s = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const uint64_t S = p.tot.sources;
+    if (s > S) return;
+    const uint4 at = p.p_scan[s];
+    if (s == S) {  // totals
+        p.p_roff[at.x] = at.y;
+        p.hdr->num_edges = at.x;
+        p.hdr->num_det_ids = at.y;
+        return;
+    }
+    const uint32_t n = p.cnt[s];
+    if (n == 0) return;
+    if (n > p.K) {
+        atomicMax(&p.hdr->record_overflow, n);
+        return;
+    }
+    p.p_prob[at.x] = p.prob[s];
+    p.p_roff[at.x] = at.y;
+    for (uint32_t j = 0; j < n; j++) {
+        p.p_word[at.y + j] = p.rtile[rec_at(p, s, j)];
+        p.p_bits[at.y + j] = p.rbits[rec_at(p, s, j)];
+    }
+}
+
+// Merge mode: the concatenated partial tables -> per-source counts,
+// probabilities and slot-major records (the emit stage's layout), one thread
+// per source. Malformed entries (no records, more than K, ids outside the
+// circuit) are dropped and counted in hdr->bad_input.
+__global__ void unpack_kernel(__grid_constant__ const DevPlan p) {
+    const uint64_t S = p.tot.sources;
+    const uint64_t s = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= S) {
+        if (s == S) p.cnt[S] = 0;
+        return;
+    }
+    uint32_t lo = 0, hi = p.m_parts;  // part k: m_desc[k].x <= s < m_desc[k + 1].x
+    while (hi - lo > 1) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (p.m_desc[mid].x <= s) lo = mid;
+        else hi = mid;
+    }
+    const uint4 d = p.m_desc[lo];
+    const uint32_t i = (uint32_t)s - d.x;
+    const uint32_t base = p.p_roff[d.y], r0 = p.p_roff[d.y + i] - base, r1 = p.p_roff[d.y + i + 1] - base;
+    const uint32_t W = (uint32_t)p.tot.tiles;
+    bool ok = r1 > r0 && r1 - r0 <= p.K && r1 <= d.w;
+    for (uint32_t j = 0; ok && j < r1 - r0; j++)
+        ok = p.p_word[d.z + r0 + j] < W && p.p_bits[d.z + r0 + j] != 0;
+    if (!ok) {
+        p.cnt[s] = 0;
+        atomicAdd(&p.hdr->bad_input, 1u);
+        return;
+    }
+    p.cnt[s] = r1 - r0;
+    p.prob[s] = p.p_prob[s];
+    for (uint32_t j = 0; j < r1 - r0; j++) {
+        p.rtile[rec_at(p, s, j)] = p.p_word[d.z + r0 + j];
+        p.rbits[rec_at(p, s, j)] = p.p_bits[d.z + r0 + j];
+    }
+}
 
 __global__ void zero_kernel(ZeroRanges z) {
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
@@ -559,9 +632,11 @@ int enqueue_pipeline(const DevPlan &p, cudaStream_t st, const StageEvents *ev, c
             z.n16[z.count] = (bytes + 15) / 16;
             z.count++;
         };
-        add(p.ell, p.tot.ell * 4);
-        add(p.leaf, p.tot.leaf * 8);
-        add(p.cnt, S * 4 + 4);
+        if (p.mode != kModeMerge) {  // (merge: counts and records are uploaded)
+            add(p.ell, p.tot.ell * 4);
+            add(p.leaf, p.tot.leaf * 8);
+            add(p.cnt, S * 4 + 4);
+        }
         add(p.bcount, NB * 4 + 4);
         add(p.hdr, sizeof(DeviceHeader));
         uint64_t units = 0;
@@ -571,6 +646,11 @@ int enqueue_pipeline(const DevPlan &p, cudaStream_t st, const StageEvents *ev, c
     }
     mark(kProfMemset);
 
+    if (p.mode == kModeMerge) {  // partial tables in: unpack, then the reduce only
+        unpack_kernel<<<(uint32_t)blocks_for(S + 1, 256), 256, 0, st>>>(p);
+        launches++;
+        goto reduce;
+    }
     // K1 lowering.
     {
         const uint32_t tpb = 256;
@@ -612,6 +692,16 @@ int enqueue_pipeline(const DevPlan &p, cudaStream_t st, const StageEvents *ev, c
     if (!p.trav.split) mark(kProfTraverse);
     mark(kProfEmit);
     if (ev) cudaEventRecord(ev->traversed, st);
+    if (p.mode == kModeShard) {  // compact partial table of the shard's nonempty sources
+        uint4 *ptot = p.bsum + p.bsum_cap - 4;
+        launch_scan(PartialScanF{p.cnt}, S + 1, p.bsum, p.p_scan, &ptot[2], st, &launches);
+        partial_kernel<<<(uint32_t)std::max<uint64_t>(blocks_for(S + 1, 256), 1), 256, 0, st>>>(p);
+        launches++;
+        if (ev) cudaEventRecord(ev->reduced, st);
+        *err = cudaGetLastError();
+        return launches;
+    }
+reduce:
 
     // K3 reduce (gp_reduce.cuh): bucket by (circuit, first detector) with a
     // counting sort, sort + group + fold each bucket on chip, write in order.

@@ -137,7 +137,8 @@ struct DeviceHeader {
     uint32_t pool_overflow;    // chunks requested beyond capacity (re-run larger)
     uint32_t huge_count;       // buckets too large for shared memory
     uint32_t items_overflow;   // nonempty signatures beyond the item capacity (re-run larger)
-    uint32_t pad[2];
+    uint32_t bad_input;        // merge: malformed partial-table entries (dropped; the call fails)
+    uint32_t pad;
 };
 
 }  // namespace gp

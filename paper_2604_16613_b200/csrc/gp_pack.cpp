@@ -92,6 +92,8 @@ uint64_t bits_of(double d) {
 
 constexpr uint64_t kTaskOps = 1 << 13;  // ops (gates + noise, or list entries) per task
 
+}  // namespace
+
 StageLayout stage_layout(const BatchTotals &t) {
     StageLayout L{};
     uint64_t o = 0;
@@ -124,6 +126,8 @@ StageLayout stage_layout(const BatchTotals &t) {
     L.total = o;
     return L;
 }
+
+namespace {
 
 // Splits [a, b) into pieces of about `per` units (at least one piece).
 template <class F>

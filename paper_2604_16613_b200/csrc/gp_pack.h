@@ -62,6 +62,9 @@ struct PackPlan {
     size_t err_circuit = 0;
 };
 
+// Byte offsets of every array of a staging image with these totals.
+StageLayout stage_layout(const BatchTotals &t);
+
 // Phase 0 (sizes, bases, index-space checks) + probability table. Cheap:
 // O(C) plus one parallel pass over noise probabilities.
 void pack_plan(HostPool *pool, const gp_circuit_view *cs, size_t C, uint8_t level, PackPlan &pp);

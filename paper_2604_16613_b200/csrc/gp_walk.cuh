@@ -152,7 +152,10 @@ __global__ void __launch_bounds__(32 * WPC) walk_kernel(__grid_constant__ const 
     const int first_layer = layer_of(min_m);
     const int b_hi = layer_of(max_m) - 1;
     const int G = (int)L.G;
-    const int ngroups = b_hi >= 0 ? (b_hi + G) / G : 0;
+    // Fault-range shard [shard_lo, shard_hi): boundaries below shard_lo are
+    // never walked, words whose leaves all lie below it not at all.
+    const int b_lo = (int)min(p.shard_lo, 0x7FFFFFFFu);
+    const int ngroups = b_hi >= b_lo ? (b_hi + G) / G : 0;
 
     uint64_t *full = L.bars(smem);
     uint32_t *mbal = L.mbal(smem);
@@ -278,7 +281,7 @@ __global__ void __launch_bounds__(32 * WPC) walk_kernel(__grid_constant__ const 
             }
             if (dbg && j < 512) dbg[j * 4 + 3] = clock64();
             if (producer) s_live[j] = live;
-            if (!live && first_layer > b) {  // zero here and no leaves below: done
+            if ((!live && first_layer > b) || b <= b_lo) {  // zero with no leaves below, or shard start: done
                 stopped = true;
                 consumed = q + 1;
                 j++;
@@ -321,6 +324,7 @@ __global__ void __launch_bounds__(256) emit_kernel(__grid_constant__ const DevPl
     for (uint64_t sl = blockIdx.x; sl < used; sl += gridDim.x) {
         const uint4 h = p.slab_hdr[sl];
         if (h.w != kSlabLive) continue;
+        if (h.z < p.shard_lo || h.z >= p.shard_hi) continue;  // fault-range shard: layer outside
         const CircuitMeta &m = meta[h.x];
         const uint64_t *st = p.slab + sl * p.slab_words;
         const uint32_t n0 = lay_noise[m.layer_base + h.z], n1 = lay_noise[m.layer_base + h.z + 1];
@@ -381,8 +385,12 @@ __global__ void __launch_bounds__(256) emit_kernel(__grid_constant__ const DevPl
         }
         const CircuitMeta &m = meta[c];
         const uint64_t *row = p.leaf + m.leaf_base + (uint64_t)(bit >> 6) * leaf_stride(m.M);
+        const uint32_t *lm = arr<uint32_t>(p, p.lay.lay_meas) + m.layer_base;
+        const uint32_t m_lo = p.shard_lo <= m.l ? lm[p.shard_lo] : m.M;  // measurements of shard layers
+        const uint32_t m_hi = p.shard_hi <= m.l ? lm[p.shard_hi] : m.M;
         for (uint32_t k = k0; k < k1; k++) {
             const uint32_t mm = ms[k];
+            if (mm < m_lo || mm >= m_hi) continue;
             if (!(flip[m.meas_base + mm] > 0)) continue;
             const uint64_t v = row[mm];
             if (v && (uint32_t)__ffsll((long long)v) - 1 == (bit & 63)) put_record(p, m.src_base + m.src_noise + mm, bit >> 6, v);

@@ -305,3 +305,98 @@ def test_pipelined_batch_matches_unpipelined():
     for _ in range(2):  # the first call learns output sizes, the second is pipelined
         got = [d.hyperedges() for d in comp.compile_batch(gens, 0)]
         assert got == want
+
+
+SHARD_CASES = [("surface_d5_r5", lambda: gp.gen_surface(5, 5, 1e-3)),
+               ("bb72_branch7_r4", lambda: gp.gen_bb72_branch(7, rounds=4)),
+               ("surface_d11_r11_si1000", lambda: gp.gen_surface(11, 11, 1e-3, gp.NOISE_MODEL_SI1000))]
+
+
+@pytest.mark.parametrize("name,make", SHARD_CASES, ids=[n for n, _ in SHARD_CASES])
+@pytest.mark.parametrize("level", [0, 2])
+def test_fault_range_shards_merge_to_whole_compile(compiler, name, make, level):
+    """the merge of n fault-range shards' partial tables (in any
+    order) is the DEM of the whole circuit, byte for byte; the shards
+    partition the nonempty sources."""
+    g = make()
+    want = compiler.compile(g, level).to_text()
+    whole = compiler.compile_shard(g, 0, 1, level)
+    assert compiler.merge_partials([whole]).to_text() == want
+    for n in (2, 3, 8):
+        parts = [compiler.compile_shard(g, k, n, level) for k in range(n)]
+        assert sum(p.num_sources for p in parts) == whole.num_sources
+        assert sum(len(p.rec_words) for p in parts) == len(whole.rec_words)
+        assert compiler.merge_partials(parts).to_text() == want
+        assert compiler.merge_partials(parts[::-1]).to_text() == want
+
+
+def test_fault_range_shard_layers_and_errors(compiler):
+    g = gp.gen_surface(3, 3, 1e-3)
+    n = g.num_layers + 3  # more shards than layers: the extra shards are empty
+    parts = [compiler.compile_shard(g, k, n) for k in range(n)]
+    assert compiler.merge_partials(parts).to_text() == compiler.compile(g, 0).to_text()
+    assert any(p.num_sources == 0 for p in parts)
+    with pytest.raises(ValueError, match="shard index"):
+        compiler.compile_shard(g, 2, 2)
+    other = compiler.compile_shard(gp.gen_surface(5, 2, 1e-3), 0, 1)
+    with pytest.raises(ValueError, match="different circuits"):
+        compiler.merge_partials([parts[0], other])
+    assert compiler.merge_partials([parts[0].__class__(g.num_detectors, g.num_observables, np.zeros(0),
+                                                       np.zeros(1, np.uint32), np.zeros(0, np.uint32),
+                                                       np.zeros(0, np.uint64))]).num_edges == 0
+
+
+def test_fault_range_shards_device_tables(compiler):
+    """GP_MEM_DEVICE partial tables (torch views of the workspace, cloned as
+    an NCCL gather would) merge like host ones, alone or mixed with them."""
+    import torch
+    g = gp.gen_surface(7, 7, 1e-3, gp.NOISE_MODEL_SI1000)
+    want = compiler.compile(g, 1).to_text()
+    dev, host = [], []
+    for k in range(4):
+        t = compiler.compile_shard(g, k, 4, 1, on_device=True)
+        dev.append(gp.DevicePartialTable(t.num_detectors, t.num_observables,
+                                         *(x.clone() for x in t.arrays().values())))
+        h = compiler.compile_shard(g, k, 4, 1)
+        # same entries (sources in order; a source's records in emission order)
+        assert np.array_equal(dev[-1].probs.cpu().numpy(), h.probs)
+        assert np.array_equal(dev[-1].rec_offsets.cpu().numpy().view(np.uint32), h.rec_offsets)
+        dw, db = dev[-1].rec_words.cpu().numpy().view(np.uint32), dev[-1].rec_bits.cpu().numpy().view(np.uint64)
+        o = np.lexsort((db, dw))
+        p = np.lexsort((h.rec_bits, h.rec_words))
+        assert np.array_equal(dw[o], h.rec_words[p]) and np.array_equal(db[o], h.rec_bits[p])
+        host.append(h)
+    assert compiler.merge_partials(dev).to_text() == want
+    assert compiler.merge_partials([dev[0], host[1], dev[2], host[3]]).to_text() == want
+    # a device view of this compiler's own workspace is consumed before reuse
+    last = compiler.compile_shard(g, 3, 4, 1, on_device=True)
+    assert compiler.merge_partials(host[:3] + [last]).to_text() == want
+    assert torch.cuda.is_available()
+
+
+def test_malformed_partial_table_rejected(compiler):
+    g = gp.gen_surface(3, 2, 1e-3)
+    t = compiler.compile_shard(g, 0, 1)
+    bad = gp.PartialTable(t.num_detectors, t.num_observables, t.probs, t.rec_offsets,
+                          t.rec_words + np.uint32(1000), t.rec_bits)
+    with pytest.raises(ValueError, match="malformed partial table"):
+        compiler.merge_partials([bad])
+    assert compiler.merge_partials([t]).to_text() == compiler.compile(g, 0).to_text()
+
+
+def test_compile_sharded_over_nccl_single_rank():
+    """shard.compile_sharded end to end through torch.distributed/NCCL
+    (world size 1 on the one GPU: device tables, all-gather, device merge)."""
+    import socket
+    import torch.distributed as td
+    from paper_2604_16613_b200.shard import compile_sharded
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    td.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1)
+    try:
+        comp = gp.Compiler(0)
+        g = gp.gen_bb72_branch(5, rounds=4)
+        assert compile_sharded(comp, g, 2).to_text() == comp.compile(g, 2).to_text()
+    finally:
+        td.destroy_process_group()

@@ -58,3 +58,57 @@ def test_two_rank_sharding_and_gather():
     assert g0 == g1
     assert g0["ids"] == [ids0, ids1]
     assert [len(x) for x in g0["p"]] == [3, 4]  # ragged per-rank tables
+
+
+def _shard_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world),
+                      LOCAL_RANK=str(rank))
+    import sys
+    sys.path.insert(0, str(ROOT))
+    import torch.distributed as td
+    from paper_2604_16613_b200 import shard
+    from paper_2604_16613_b200.api import PartialTable
+    try:
+        td.init_process_group("gloo")
+        rng = np.random.default_rng(rank)
+        n = 3 + 4 * rank  # ragged per-rank tables
+        cnt = rng.integers(1, 4, n)
+        roff = np.concatenate([[0], np.cumsum(cnt)]).astype(np.uint32)
+        r = int(roff[-1])
+        t = PartialTable(100, 2, rng.random(n), roff, rng.integers(0, 2, r).astype(np.uint32),
+                         rng.integers(0, 2**64, r, dtype=np.uint64) | np.uint64(1 << 63))
+        got = shard.tables_from(shard.gather_flat(shard.table_arrays(t), "cpu"))
+        td.destroy_process_group()
+        q.put((rank, [(g.num_detectors, g.num_observables, g.probs.tobytes(), g.rec_offsets.tobytes(),
+                       g.rec_words.tobytes(), g.rec_bits.tobytes()) for g in got],
+               (t.probs.tobytes(), roff.tobytes(), t.rec_words.tobytes(), t.rec_bits.tobytes())))
+    except Exception as e:  # pragma: no cover
+        q.put((rank, "error", repr(e)))
+
+
+def test_two_rank_partial_table_gather_is_bit_exact():
+    """The fault-range sharding exchange (paper_2604_16613_b200.shard): ragged
+    partial tables (f64 probabilities, u64 records with the top bit set)
+    reach every rank bit-exactly, in rank order."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_shard_worker, args=(r, 2, port, q)) for r in range(2)]
+    [p.start() for p in procs]
+    res = sorted([q.get(timeout=120) for _ in procs], key=lambda x: x[0])
+    [p.join(timeout=60) for p in procs]
+    for r in res:
+        assert r[1] != "error", r
+    own = [r[2] for r in res]
+    for _, got, _ in res:
+        assert [g[:2] for g in got] == [(100, 2), (100, 2)]
+        assert [g[2:] for g in got] == own
+
+
+def test_shard_layer_ranges_partition():
+    from paper_2604_16613_b200.shard import shard_of
+    for layers in (1, 5, 17, 100):
+        for world in (1, 2, 3, 8, 13):
+            rs = [shard_of(k, world, layers) for k in range(world)]
+            assert rs[0][0] == 0 and rs[-1][1] == layers
+            assert all(a[1] == b[0] for a, b in zip(rs, rs[1:]))
