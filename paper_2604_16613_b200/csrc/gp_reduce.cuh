@@ -483,28 +483,29 @@ struct CtaTeam {
     __device__ void sync() const { __syncthreads(); }
 };
 
-// Shared workspace of one team for a bucket of up to `cap` items.
+// Shared workspace of one team for a bucket of up to `cap` (< 65535) items;
+// 16-bit item indices keep a warp's workspace at 5.6 KB (occupancy).
 struct GroupWs {
-    uint32_t *tab;   // [tcap] representative item or ~0
-    uint32_t *rep;   // [cap] item -> representative
-    uint32_t *cnt;   // [cap] members per representative, then fill counters
-    uint32_t *off;   // [cap] member offset per representative
-    uint32_t *grp;   // [cap] representatives (groups), canonical order after the sort
     double *mp;      // [cap] member probabilities grouped; [off[r]] = folded probability
+    uint32_t *cnt;   // [cap] members per representative, then fill counters
     uint32_t *tot;   // [4] team scratch: group count, id sums
+    uint16_t *tab;   // [tcap] representative item or 0xFFFF
+    uint16_t *rep;   // [cap] item -> representative
+    uint16_t *off;   // [cap] member offset per representative
+    uint16_t *grp;   // [cap] representatives (groups), canonical order after the sort
     uint32_t tcap;   // power of two >= 2 cap
     __device__ static size_t bytes(uint32_t cap, uint32_t tcap) {
-        return (size_t)tcap * 4 + (size_t)cap * (4 * 4 + 8) + 16 + 8;
+        return ((size_t)cap * (8 + 4 + 2 * 3) + 16 + (size_t)tcap * 2 + 15) & ~(size_t)15;
     }
     __device__ void carve(uint8_t *base, uint32_t cap, uint32_t tc) {
         tcap = tc;
         mp = reinterpret_cast<double *>(base);  // 8-byte aligned first
-        tab = reinterpret_cast<uint32_t *>(mp + cap);
+        cnt = reinterpret_cast<uint32_t *>(mp + cap);
+        tot = cnt + cap;
+        tab = reinterpret_cast<uint16_t *>(tot + 4);
         rep = tab + tcap;
-        cnt = rep + cap;
-        off = cnt + cap;
+        off = rep + cap;
         grp = off + cap;
-        tot = grp + cap;
     }
 };
 
@@ -545,9 +546,9 @@ __device__ __forceinline__ uint32_t scan_groups(const Team &tm, const GroupWs &w
     }
     uint32_t om = bm + im - sm, og = bg + ig - sg;
     for (uint32_t i = a; i < e; i++) {
-        w.off[i] = om;
+        w.off[i] = (uint16_t)om;
         om += w.cnt[i];
-        if (w.cnt[i]) w.grp[og++] = i;
+        if (w.cnt[i]) w.grp[og++] = (uint16_t)i;
     }
     if (t0 == nt - 1) w.tot[0] = og;  // the last thread ends at the total
     tm.sync();
@@ -560,7 +561,7 @@ template <class Team>
 __device__ void group_bucket(const DevPlan &p, const Team &tm, uint32_t b, uint32_t base, uint32_t n,
                              const Item *it, GroupWs &w) {
     const uint32_t t0 = tm.t0(), nt = tm.nt();
-    for (uint32_t x = t0; x < w.tcap; x += nt) w.tab[x] = 0xFFFFFFFFu;
+    for (uint32_t x = t0; x < w.tcap; x += nt) w.tab[x] = 0xFFFF;
     for (uint32_t x = t0; x < n; x += nt) w.cnt[x] = 0;
     tm.sync();
     // 1. representatives: hash + full key compare
@@ -569,9 +570,9 @@ __device__ void group_bucket(const DevPlan &p, const Team &tm, uint32_t b, uint3
         uint32_t h = item_hash(me) & (w.tcap - 1), r = i;
         while (true) {
             uint32_t cur = w.tab[h];
-            if (cur == 0xFFFFFFFFu) {
-                cur = atomicCAS(&w.tab[h], 0xFFFFFFFFu, i);
-                if (cur == 0xFFFFFFFFu) break;  // this item founds the group
+            if (cur == 0xFFFF) {
+                cur = atomicCAS(&w.tab[h], (unsigned short)0xFFFF, (unsigned short)i);
+                if (cur == 0xFFFF) break;  // this item founds the group
             }
             if (key_eq(it[cur], me)) {
                 r = cur;
@@ -579,7 +580,7 @@ __device__ void group_bucket(const DevPlan &p, const Team &tm, uint32_t b, uint3
             }
             h = (h + 1) & (w.tcap - 1);
         }
-        w.rep[i] = r;
+        w.rep[i] = (uint16_t)r;
         atomicAdd(&w.cnt[r], 1u);
     }
     tm.sync();
@@ -614,8 +615,8 @@ __device__ void group_bucket(const DevPlan &p, const Team &tm, uint32_t b, uint3
     auto cas = [&](uint32_t x, uint32_t y) {
         const uint32_t u = w.grp[x], v = w.grp[y];
         if (key_cmp(it[v], it[u]) < 0) {
-            w.grp[x] = v;
-            w.grp[y] = u;
+            w.grp[x] = (uint16_t)v;
+            w.grp[y] = (uint16_t)u;
         }
     };
     for (uint32_t k = 2; k <= np; k <<= 1) {
@@ -770,7 +771,7 @@ __device__ void bucket_cta(const DevPlan &p, uint32_t b, uint32_t n, uint32_t D,
 
 constexpr uint32_t kBucketThreads = 128, kWarpItems = 256;
 constexpr uint32_t kWarpTab = 512;                                   // >= 2 kWarpItems
-constexpr uint32_t kWarpWs = 512 * 4 + 256 * 24 + 24;                 // GroupWs::bytes(256, 512)
+constexpr uint32_t kWarpWs = (256 * 18 + 16 + 512 * 2 + 15) & ~15u;  // GroupWs::bytes(256, 512)
 constexpr uint32_t kHugeSmem = 196 * 1024;                            // huge_kernel dynamic smem
 
 // One warp per bucket, no CTA synchronisation: empty buckets, buckets of up
