@@ -165,55 +165,47 @@ __device__ __forceinline__ Item make_item_small(const DevPlan &p, uint32_t s, ui
     cs(0, 2);
     cs(1, 3);
     cs(1, 2);
-    // detector ids in order: record r, its remaining detector bits
-    uint32_t r = 0;
-    uint64_t rem = w[0] & det_mask(t[0], D);
-    uint32_t tile = t[0];
-    auto next_det = [&]() -> uint32_t {  // id + 1, or 0 at the end
-        while (rem == 0 && r < 3) {
-            r++;
-            const uint32_t tt = r == 1 ? t[1] : r == 2 ? t[2] : t[3];
-            const uint64_t ww = r == 1 ? w[1] : r == 2 ? w[2] : w[3];
-            tile = tt;
-            rem = tt == 0xFFFFFFFFu ? 0 : ww & det_mask(tt, D);
-        }
-        if (rem == 0) return 0;
-        const uint32_t b = (uint32_t)__ffsll((long long)rem) - 1;
-        rem &= rem - 1;
-        return tile * 64 + b + 1;
-    };
-    Item it;
-    const uint32_t q0 = next_det();
-    bool sep = q0 == 0, fits = true;
-    uint32_t sl[16];
-#pragma unroll
-    for (int x = 0; x < 16; x++) {
-        uint32_t v = 0;
-        if (!sep) {
-            const uint32_t e = next_det();
-            if (e == 0) sep = true;
-            else {
-                v = e - q0;
-                if (v >= 0xFFFFu) fits = false;
-            }
-        }
-        sl[x] = v & 0xFFFF;
-    }
-    if (!sep) fits = false;
+    // Detector ids in order (records sorted by word, bits ascending): the
+    // first is the bucket (q0), the next ones go to 16-bit slots relative to
+    // it, four per 64-bit word, most significant first. Observables: a mask.
+    uint64_t kw[4] = {0, 0, 0, 0};
+    uint32_t q0 = 0, cnt = 0;
+    bool fits = true;
     uint64_t obs = 0;
 #pragma unroll
     for (int j = 0; j < 4; j++) {
         if (t[j] == 0xFFFFFFFFu) continue;
-        uint64_t ob = w[j] & ~det_mask(t[j], D);
-        while (ob) {
+        const uint64_t dm = det_mask(t[j], D);
+        for (uint64_t m = w[j] & dm; m; m &= m - 1) {
+            const uint32_t id1 = t[j] * 64 + (uint32_t)__ffsll((long long)m);  // id + 1
+            if (cnt == 0) {
+                q0 = id1;
+            } else {
+                const uint32_t slot = cnt - 1, v = id1 - q0;
+                if (slot >= 15 || v >= 0xFFFFu) fits = false;  // no room for the separator / delta too wide
+                if (slot < 16) {
+                    const uint64_t add = (uint64_t)(v & 0xFFFF) << (48 - 16 * (slot & 3));
+                    const uint32_t wi = slot >> 2;
+                    kw[0] |= wi == 0 ? add : 0;
+                    kw[1] |= wi == 1 ? add : 0;
+                    kw[2] |= wi == 2 ? add : 0;
+                    kw[3] |= wi == 3 ? add : 0;
+                }
+            }
+            cnt++;
+        }
+        for (uint64_t ob = w[j] & ~dm; ob; ob &= ob - 1) {
             const uint32_t o = t[j] * 64 + (uint32_t)__ffsll((long long)ob) - 1 - D;
-            ob &= ob - 1;
             if (o < 64) obs |= 1ull << o;
             else fits = false;
         }
     }
+    Item it;
 #pragma unroll
-    for (int x = 0; x < 8; x++) it.k[x] = sl[2 * x] << 16 | sl[2 * x + 1];
+    for (int x = 0; x < 4; x++) {
+        it.k[2 * x] = (uint32_t)(kw[x] >> 32);
+        it.k[2 * x + 1] = (uint32_t)kw[x];
+    }
     it.obs = obs;
     it.prob = p.prob[s];
     it.src = s;
