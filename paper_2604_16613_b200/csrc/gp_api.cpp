@@ -675,9 +675,10 @@ gp_status run_batch(gp_ctx *ctx, const gp_circuit_view *cs, size_t count, uint8_
 namespace {
 struct PipeLane {
     gp::PackPlan pp;
-    uint8_t *h_stage = nullptr, *d_img = nullptr, *d_out = nullptr;
-    size_t h_stage_cap = 0, d_img_cap = 0, d_out_cap = 0;
-    cudaEvent_t ev_in = nullptr, ev_done = nullptr, ev_out = nullptr;
+    uint8_t *h_stage = nullptr, *d_img = nullptr, *d_out = nullptr, *d_ws = nullptr;
+    size_t h_stage_cap = 0, d_img_cap = 0, d_out_cap = 0, d_ws_cap = 0;
+    cudaStream_t s_comp = nullptr;  // the lane's device pipeline (lanes overlap each other's tails)
+    cudaEvent_t ev_in = nullptr, ev_done = nullptr, ev_out = nullptr, ev_written = nullptr;
     bool used = false;
 };
 }  // namespace
@@ -698,7 +699,9 @@ void pipe_destroy(PipeState *ps) {
         if (l.h_stage) cudaFreeHost(l.h_stage);
         if (l.d_img) cudaFree(l.d_img);
         if (l.d_out) cudaFree(l.d_out);
-        for (cudaEvent_t e : {l.ev_in, l.ev_done, l.ev_out})
+        if (l.d_ws) cudaFree(l.d_ws);
+        if (l.s_comp) cudaStreamDestroy(l.s_comp);
+        for (cudaEvent_t e : {l.ev_in, l.ev_done, l.ev_out, l.ev_written})
             if (e) cudaEventDestroy(e);
     }
     if (ps->s_in) cudaStreamDestroy(ps->s_in);
@@ -799,6 +802,7 @@ gp_status run_batch_pipelined(gp_ctx *ctx, const gp_circuit_view *cs, size_t cou
     int launches = 0;
     auto drain = [&] {
         cudaStreamSynchronize(ps.s_in);
+        for (PipeLane &l : ps.lane) cudaStreamSynchronize(l.s_comp);
         cudaStreamSynchronize(ctx->stream);
         cudaStreamSynchronize(ps.s_out);
     };
@@ -882,9 +886,9 @@ gp_status run_batch_pipelined(gp_ctx *ctx, const gp_circuit_view *cs, size_t cou
         p.trav_smem = tsmem;
         const size_t need_ws = carve(ctx, p, t, nullptr, K, sub_ids, pool, slabs, sub_items, false);
         const size_t need_out = carve_out(p, nullptr, sub_items, sub_ids, t.C);
-        if (need_ws > ctx->d_ws_cap) {  // the workspace serves every sub-batch in stream order
-            cudaStreamSynchronize(ctx->stream);
-            if ((st = ensure_device(ctx, &ctx->d_ws, &ctx->d_ws_cap, need_ws)) != GP_OK) return drain(), st;
+        if (need_ws > ln.d_ws_cap) {  // the lane's workspace serves its sub-batches in stream order
+            cudaStreamSynchronize(ln.s_comp);
+            if ((st = ensure_device(ctx, &ln.d_ws, &ln.d_ws_cap, need_ws)) != GP_OK) return drain(), st;
         }
         if (ln.used && (need_out > ln.d_out_cap || pp.L.total > ln.d_img_cap)) {
             cudaEventSynchronize(ln.ev_out);
@@ -893,7 +897,7 @@ gp_status run_batch_pipelined(gp_ctx *ctx, const gp_circuit_view *cs, size_t cou
         if (ensure_dev_plain(&ln.d_out, &ln.d_out_cap, need_out) != GP_OK ||
             ensure_dev_plain(&ln.d_img, &ln.d_img_cap, pp.L.total) != GP_OK)
             return drain(), fail(ctx, GP_ERR_OUT_OF_MEMORY, "device allocation failed");
-        carve(ctx, p, t, ctx->d_ws, K, sub_ids, pool, slabs, sub_items, false);
+        carve(ctx, p, t, ln.d_ws, K, sub_ids, pool, slabs, sub_items, false);
         carve_out(p, ln.d_out, sub_items, sub_ids, t.C);
         p.img = ln.d_img;
         p.base_in = bases + 4 * k;
@@ -905,16 +909,17 @@ gp_status run_batch_pipelined(gp_ctx *ctx, const gp_circuit_view *cs, size_t cou
         if (ln.used) cudaStreamWaitEvent(ps.s_in, ln.ev_done, 0);
         cudaError_t e = cudaMemcpyAsync(ln.d_img, ln.h_stage, pp.L.total, cudaMemcpyHostToDevice, ps.s_in);
         cudaEventRecord(ln.ev_in, ps.s_in);
-        cudaStreamWaitEvent(ctx->stream, ln.ev_in, 0);
-        if (ln.used) cudaStreamWaitEvent(ctx->stream, ln.ev_out, 0);  // the lane's download read d_out
+        cudaStreamWaitEvent(ln.s_comp, ln.ev_in, 0);
+        if (ln.used) cudaStreamWaitEvent(ln.s_comp, ln.ev_out, 0);  // the lane's download read d_out
         if (trace) {
             tpack.push_back(ns_since(tp0) / 1e3);
             for (int x = 0; x < 3; x++) tev.push_back(nullptr), cudaEventCreate(&tev.back());
             cudaEventRecord(tev[tev.size() - 3], ps.s_in);
         }
-        launches += gp::enqueue_pipeline(p, ctx->stream, nullptr, nullptr, &e);
-        if (trace) cudaEventRecord(tev[tev.size() - 2], ctx->stream);
-        cudaEventRecord(ln.ev_done, ctx->stream);
+        cudaEvent_t prev_written = k ? ps.lane[(k - 1) % gp::kLanes].ev_written : nullptr;
+        launches += gp::enqueue_pipeline(p, ln.s_comp, nullptr, nullptr, &e, prev_written, ln.ev_written);
+        if (trace) cudaEventRecord(tev[tev.size() - 2], ln.s_comp);
+        cudaEventRecord(ln.ev_done, ln.s_comp);
         ln.used = true;
         if (e != cudaSuccess) return drain(), cuda_fail(ctx, e, "pipelined launch");
         h2d_bytes += pp.L.total;
@@ -987,9 +992,11 @@ gp_status run_batch_any(gp_ctx *ctx, const gp_circuit_view *cs, size_t count, ui
             cudaStreamCreateWithFlags(&ps.s_in, cudaStreamNonBlocking);
             cudaStreamCreateWithFlags(&ps.s_out, cudaStreamNonBlocking);
             for (PipeLane &l : ps.lane) {
+                cudaStreamCreateWithFlags(&l.s_comp, cudaStreamNonBlocking);
                 cudaEventCreateWithFlags(&l.ev_in, cudaEventDisableTiming);
                 cudaEventCreateWithFlags(&l.ev_done, cudaEventDisableTiming);
                 cudaEventCreateWithFlags(&l.ev_out, cudaEventDisableTiming);
+                cudaEventCreateWithFlags(&l.ev_written, cudaEventDisableTiming);
             }
             if (cudaHostAlloc(&ps.h_misc, (kMaxSub + 1) * 4 * 8 + 64 + kMaxSub * sizeof(DeviceHeader),
                               cudaHostAllocMapped) != cudaSuccess) {

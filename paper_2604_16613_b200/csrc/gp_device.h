@@ -148,8 +148,12 @@ constexpr const char *kProfNames[kProfCount] = {"start",  "memset",      "lower"
 // Enqueues the whole device pipeline on `stream`: lowering, traversal,
 // reduce, canonical order, output gather. Returns the number of kernel
 // launches (memsets included). `events` may be null.
+// wait_write / written (optional): the write stage waits for / then marks an
+// event -- sub-batches on concurrent streams publish their global output
+// bases (base_in -> base_out) in order.
 int enqueue_pipeline(const DevPlan &p, cudaStream_t stream, const StageEvents *events,
-                     const cudaEvent_t *prof, cudaError_t *err);
+                     const cudaEvent_t *prof, cudaError_t *err, cudaEvent_t wait_write = nullptr,
+                     cudaEvent_t written = nullptr);
 
 // Chooses the traversal configuration for a batch (group width, ring depths,
 // warp roles) and its dynamic shared memory; false if a circuit is too wide

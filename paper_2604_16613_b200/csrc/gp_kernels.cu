@@ -615,7 +615,7 @@ bool plan_traversal(const BatchTotals &t, int device, TravCfg *cfg, size_t *smem
 }
 
 int enqueue_pipeline(const DevPlan &p, cudaStream_t st, const StageEvents *ev, const cudaEvent_t *prof,
-                     cudaError_t *err) {
+                     cudaError_t *err, cudaEvent_t wait_write, cudaEvent_t written) {
     int launches = 0;
     auto mark = [&](int k) {
         if (prof) cudaEventRecord(prof[k], st);
@@ -725,6 +725,7 @@ reduce:
     mark(kProfBucket);
     launch_scan(OutScanF{p.ecount, p.eids}, NB, p.bsum, p.oscan, &totals[1], st, &launches);
     mark(kProfScanOut);
+    if (wait_write) cudaStreamWaitEvent(st, wait_write, 0);  // the previous sub-batch's bases
     {
         const uint64_t threads = std::max<uint64_t>(NB * 32, p.tot.C + 1);
         red::write_kernel<<<(uint32_t)std::min<uint64_t>(blocks_for(threads, tpb), 148 * 32), tpb, 0, st>>>(
@@ -732,6 +733,7 @@ reduce:
         launches++;
     }
     mark(kProfWrite);
+    if (written) cudaEventRecord(written, st);
     if (p.out_mapped) red::copy_out_kernel<<<32, 256, 0, st>>>(p), launches++;
     if (ev) cudaEventRecord(ev->reduced, st);
     *err = cudaGetLastError();
