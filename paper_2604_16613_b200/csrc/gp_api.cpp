@@ -346,6 +346,8 @@ gp_status run_batch(gp_ctx *ctx, const gp_circuit_view *cs, size_t count, uint8_
     if (!ctx->pool && ops >= (1u << 14))
         ctx->pool = std::make_unique<gp::HostPool>(std::max(1u, std::thread::hardware_concurrency()) - 1);
     gp::HostPool *hpool = ops >= (1u << 14) ? ctx->pool.get() : nullptr;
+    pp.force_wide = false;
+repack:  // (again with per-op probabilities when the table overflowed)
     gp::pack_plan(hpool, cs, count, level, pp);
     if (pp.err == gp::kPackIndexSpace || pp.err == gp::kPackTooWide) {
         // Circuits before the first index-space failure may still hold leaf
@@ -390,6 +392,11 @@ gp_status run_batch(gp_ctx *ctx, const gp_circuit_view *cs, size_t count, uint8_
         slice(L.obs_meas, 4, a.obs_entry_base, last ? tt.obs_entries : b->obs_entry_base);
     }
     if (pp.err) return fail_pack(ctx, pp.err);
+    if (pp.need_wide.load() && !pp.force_wide) {
+        cudaStreamSynchronize(ctx->stream);  // chunk uploads read the staging image
+        pp.force_wide = true;
+        goto repack;
+    }
     gp::pack_finish(pp, ctx->h_stage);
     BatchTotals t = pp.t;
     if (t.sources >= 0xFFFFFFFFull || t.tiles >= 0xFFFFFFFFull || t.gates >= 0xFFFFFFFFull ||
@@ -403,7 +410,7 @@ gp_status run_batch(gp_ctx *ctx, const gp_circuit_view *cs, size_t count, uint8_
     for (const CircuitMeta &m : M) t.groups += (m.W + tcfg.T - 1) / tcfg.T;
     gp::pack_head(pp, tcfg.T, ctx->h_stage);
     if (nchunk == 1) {
-        slice(0, 1, 0, L.total);  // the whole image in one copy
+        slice(0, 1, 0, pp.image_bytes());  // the whole image in one copy
     } else {
         slice(L.lay_meas, 4, 0, t.layer_slots);  // finished prefix tables
         slice(L.lay_src, 4, 0, t.layer_slots);
@@ -536,7 +543,7 @@ gp_status run_batch(gp_ctx *ctx, const gp_circuit_view *cs, size_t count, uint8_
         if (stats) {
             *stats = gp_stats{};
             stats->num_sources = t.sources;
-            stats->h2d_bytes = L.total;
+            stats->h2d_bytes = pp.image_bytes();
             stats->kernel_ns = (uint64_t)(elapsed_ms(ctx->ev_h2d, ctx->ev_end) * 1e6);
             stats->kernel_launches = (uint64_t)launches;
         }
@@ -600,7 +607,7 @@ gp_status run_batch(gp_ctx *ctx, const gp_circuit_view *cs, size_t count, uint8_
             stats->kernel_ns = (uint64_t)((low + trav + red) * 1e6);  // includes the mapped-output copy
             stats->d2h_ns = (uint64_t)(out_ms * 1e6);
             stats->num_sources = t.sources;
-            stats->h2d_bytes = L.total;
+            stats->h2d_bytes = pp.image_bytes();
             stats->d2h_bytes = sizeof(DeviceHeader) + (E + 1) * 16 + E * 8 + (nd + no) * 4 + (count + 1) * 8;
             stats->kernel_launches = (uint64_t)launches;
             stats->total_ns = ns_since(t0);
@@ -652,7 +659,7 @@ gp_status run_batch(gp_ctx *ctx, const gp_circuit_view *cs, size_t count, uint8_
         stats->kernel_ns = (uint64_t)((low + trav + red) * 1e6);
         stats->d2h_ns = (uint64_t)(d2h_ms * 1e6);
         stats->num_sources = t.sources;
-        stats->h2d_bytes = L.total;
+        stats->h2d_bytes = pp.image_bytes();
         stats->d2h_bytes = sizeof(DeviceHeader) + o;
         stats->kernel_launches = (uint64_t)launches;
         stats->total_ns = ns_since(t0);
@@ -848,6 +855,8 @@ gp_status run_batch_pipelined(gp_ctx *ctx, const gp_circuit_view *cs, size_t cou
         const size_t c0 = count * k / P, c1 = count * (k + 1) / P, n = c1 - c0;
         if (ln.used) cudaEventSynchronize(ln.ev_in);  // the lane's previous staging was uploaded
         gp::PackPlan &pp = ln.pp;
+        pp.force_wide = false;
+    repack:
         gp::pack_plan(hpool, cs + c0, n, level, pp);
         if (pp.err == gp::kPackIndexSpace || pp.err == gp::kPackTooWide) {
             drain();
@@ -858,6 +867,10 @@ gp_status run_batch_pipelined(gp_ctx *ctx, const gp_circuit_view *cs, size_t cou
             return drain(), fail(ctx, st, "pinned host allocation failed");
         gp::pack_range(hpool, cs + c0, pp, ln.h_stage, 0, n);
         if (pp.err) return drain(), fail_pack(ctx, pp.err);
+        if (pp.need_wide.load() && !pp.force_wide) {
+            pp.force_wide = true;
+            goto repack;
+        }
         gp::pack_finish(pp, ln.h_stage);
         BatchTotals t = pp.t;
         if (t.sources >= 0xFFFFFFFFull || t.tiles >= 0xFFFFFFFFull || t.gates >= 0xFFFFFFFFull ||
@@ -907,7 +920,7 @@ gp_status run_batch_pipelined(gp_ctx *ctx, const gp_circuit_view *cs, size_t cou
         // stream); the upload overwrites the lane's image only once the lane's
         // previous kernels are done reading it
         if (ln.used) cudaStreamWaitEvent(ps.s_in, ln.ev_done, 0);
-        cudaError_t e = cudaMemcpyAsync(ln.d_img, ln.h_stage, pp.L.total, cudaMemcpyHostToDevice, ps.s_in);
+        cudaError_t e = cudaMemcpyAsync(ln.d_img, ln.h_stage, pp.image_bytes(), cudaMemcpyHostToDevice, ps.s_in);
         cudaEventRecord(ln.ev_in, ps.s_in);
         cudaStreamWaitEvent(ln.s_comp, ln.ev_in, 0);
         if (ln.used) cudaStreamWaitEvent(ln.s_comp, ln.ev_out, 0);  // the lane's download read d_out
@@ -922,7 +935,7 @@ gp_status run_batch_pipelined(gp_ctx *ctx, const gp_circuit_view *cs, size_t cou
         cudaEventRecord(ln.ev_done, ln.s_comp);
         ln.used = true;
         if (e != cudaSuccess) return drain(), cuda_fail(ctx, e, "pipelined launch");
-        h2d_bytes += pp.L.total;
+        h2d_bytes += pp.image_bytes();
         sources += t.sources;
     }
     for (size_t j = 0; j < P; j++)

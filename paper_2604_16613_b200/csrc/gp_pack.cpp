@@ -4,6 +4,9 @@
 #include <algorithm>
 #include <chrono>
 #include <cstring>
+#if defined(__x86_64__)
+#include <immintrin.h>
+#endif
 
 namespace gp {
 
@@ -92,6 +95,23 @@ uint64_t bits_of(double d) {
 
 constexpr uint64_t kTaskOps = 1 << 13;  // ops (gates + noise, or list entries) per task
 
+// Streaming store of an 8-byte word into the pinned staging image: written
+// once, read only by the DMA engine, so it bypasses the caches (no
+// read-for-ownership of the destination lines: the packer is bound by host
+// memory traffic).
+inline void put64(uint64_t *dst, uint64_t v) {
+#if defined(__x86_64__)
+    _mm_stream_si64(reinterpret_cast<long long *>(dst), (long long)v);
+#else
+    *dst = v;
+#endif
+}
+inline void put_fence() {
+#if defined(__x86_64__)
+    _mm_sfence();
+#endif
+}
+
 }  // namespace
 
 StageLayout stage_layout(const BatchTotals &t) {
@@ -116,13 +136,13 @@ StageLayout stage_layout(const BatchTotals &t) {
     L.gates = put(t.gates * 8);
     L.noise = put(t.noise * 8);
     L.noise_prob = put(t.wide_prob ? t.noise * 8 : 0);
-    L.prob_table = put((uint64_t)t.prob_table_n * 8);
     L.lay_src = put(t.layer_slots * 4);
     L.meas_flip = put(t.meas * 8);
     L.det_off = put(t.det_slots * 4);
     L.det_meas = put(t.det_entries * 4);
     L.obs_off = put(t.obs_slots * 4);
     L.obs_meas = put(t.obs_entries * 4);
+    L.prob_table = put((uint64_t)t.prob_table_n * 8);  // last: uploads stop at the entries used
     L.total = o;
     return L;
 }
@@ -142,23 +162,75 @@ void run_tasks(HostPool *pool, size_t n, const std::function<void(size_t)> &f) {
         for (size_t i = 0; i < n; i++) f(i);
 }
 
-// Lookup of a probability's table index with a last-value cache (runs of
-// equal probabilities are the norm).
-struct ProbIndex {
-    const std::vector<uint64_t> *keys;
-    uint64_t last_key = ~0ull;
-    uint32_t last_idx = 0;
+// Per-task cache in front of the shared dictionary (a layer's noise ops
+// cycle through a few probabilities).
+struct ProbCache {
+    ProbDict *d;
+    uint64_t k[4] = {~0ull, ~0ull, ~0ull, ~0ull};
+    uint32_t v[4] = {ProbDict::kFull, ProbDict::kFull, ProbDict::kFull, ProbDict::kFull};
+    uint32_t next = 0;
     uint32_t operator()(double p) {
         const uint64_t b = bits_of(p);
-        if (b != last_key) {
-            last_key = b;
-            last_idx = (uint32_t)(std::lower_bound(keys->begin(), keys->end(), b) - keys->begin());
-        }
-        return last_idx;
+        for (int i = 0; i < 4; i++)
+            if (k[i] == b) return v[i];
+        const uint32_t x = d->index(b);
+        k[next] = b;
+        v[next] = x;
+        next = (next + 1) & 3;
+        return x;
     }
 };
 
 }  // namespace
+
+// ---------------------------------------------------------------- dictionary
+
+ProbDict::ProbDict()
+    : key_(new std::atomic<uint64_t>[kSlots]), val_(new std::atomic<uint32_t>[kSlots]),
+      slot_of_(new uint32_t[kNoisePidxMax + 2]) {
+    for (uint32_t x = 0; x < kSlots; x++) {
+        key_[x].store(0, std::memory_order_relaxed);
+        val_[x].store(kEmpty, std::memory_order_relaxed);
+    }
+}
+
+void ProbDict::clear() {
+    const uint32_t n = std::min<uint32_t>(n_.load(), kNoisePidxMax + 2);
+    for (uint32_t i = 0; i < n; i++) val_[slot_of_[i]].store(kEmpty, std::memory_order_relaxed);
+    n_.store(0);
+}
+
+uint32_t ProbDict::size() const { return std::min<uint32_t>(n_.load(), kNoisePidxMax + 1); }
+
+uint32_t ProbDict::index(uint64_t bits) {
+    uint64_t h = bits * 0x9e3779b97f4a7c15ull;
+    uint32_t x = (uint32_t)(h >> 48) & (kSlots - 1);
+    for (;;) {
+        uint32_t v = val_[x].load(std::memory_order_acquire);
+        if (v == kEmpty) {
+            if (val_[x].compare_exchange_strong(v, kBusy, std::memory_order_acq_rel)) {
+                key_[x].store(bits, std::memory_order_relaxed);
+                const uint32_t i = n_.fetch_add(1);
+                if (i < kNoisePidxMax + 2) slot_of_[i] = x;
+                val_[x].store(i, std::memory_order_release);
+                return i <= kNoisePidxMax ? i : kFull;
+            }
+        }
+        while (v == kBusy) v = val_[x].load(std::memory_order_acquire);
+        if (v == kEmpty) continue;  // (lost a race to a claim that has now published: re-read)
+        if (key_[x].load(std::memory_order_relaxed) == bits) return v <= kNoisePidxMax ? v : kFull;
+        x = (x + 1) & (kSlots - 1);
+    }
+}
+
+void ProbDict::values(std::vector<double> &out) const {
+    const uint32_t n = size();
+    out.resize(n);
+    for (uint32_t i = 0; i < n; i++) {
+        const uint64_t b = key_[slot_of_[i]].load(std::memory_order_relaxed);
+        std::memcpy(&out[i], &b, 8);
+    }
+}
 
 // ---------------------------------------------------------------- phases
 
@@ -222,52 +294,13 @@ void pack_plan(HostPool *pool, const gp_circuit_view *cs, size_t C, uint8_t leve
         t.leaf += (uint64_t)m.W * leaf_stride(m.M);
         t.buckets += (uint64_t)m.D + 1;
     }
-    // Distinct noise probabilities (bit-exact keys), one pass in parallel.
-    struct Piece {
-        uint32_t c;
-        uint64_t o0, o1;
-    };
-    std::vector<Piece> pieces;
-    for (size_t c = 0; c < C; c++)
-        split_range(cs[c].noise_offsets[0], cs[c].noise_offsets[cs[c].num_layers], kTaskOps,
-                    [&](uint64_t a, uint64_t b) { pieces.push_back({(uint32_t)c, a, b}); });
-    std::vector<std::vector<uint64_t>> found(pieces.size());
-    std::vector<uint8_t> many(pieces.size(), 0);
-    run_tasks(pool, pieces.size(), [&](size_t k) {
-        const Piece &pc = pieces[k];
-        const double *pr = cs[pc.c].noise_prob;
-        std::vector<uint64_t> &f = found[k];
-        uint64_t last = ~0ull;
-        for (uint64_t o = pc.o0; o < pc.o1; o++) {
-            const uint64_t b = bits_of(pr[o]);
-            if (b == last) continue;
-            last = b;
-            if (std::find(f.begin(), f.end(), b) == f.end()) {
-                if (f.size() >= 64) {
-                    many[k] = 1;
-                    return;
-                }
-                f.push_back(b);
-            }
-        }
-    });
-    std::vector<uint64_t> keys;
-    bool wide = false;
-    for (size_t k = 0; k < pieces.size(); k++) {
-        wide |= many[k] != 0;
-        keys.insert(keys.end(), found[k].begin(), found[k].end());
-    }
-    std::sort(keys.begin(), keys.end());
-    keys.erase(std::unique(keys.begin(), keys.end()), keys.end());
-    t.wide_prob = wide || keys.size() > kNoisePidxMax;
+    // Probability table: filled by pack_range; reserved at its maximum size
+    // at the end of the image (image_bytes() uploads the part used).
+    t.wide_prob = pp.force_wide;
+    t.prob_table_n = t.wide_prob ? 0 : kNoisePidxMax + 1;
+    pp.dict.clear();
+    pp.need_wide.store(false);
     pp.prob_table.clear();
-    if (!t.wide_prob)
-        for (uint64_t b : keys) {
-            double q;
-            std::memcpy(&q, &b, 8);
-            pp.prob_table.push_back(q);
-        }
-    t.prob_table_n = (uint32_t)pp.prob_table.size();
     pp.L = stage_layout(t);
 }
 
@@ -288,8 +321,6 @@ void pack_range(HostPool *pool, const gp_circuit_view *cs, PackPlan &pp, uint8_t
     auto *det_meas = (uint32_t *)at(L.det_meas);
     auto *obs_off = (uint32_t *)at(L.obs_off);
     auto *obs_meas = (uint32_t *)at(L.obs_meas);
-    std::vector<uint64_t> keys(pp.prob_table.size());
-    for (size_t x = 0; x < keys.size(); x++) keys[x] = bits_of(pp.prob_table[x]);
 
     // Tasks: 0 = layer range, 1 = detector range, 2 = observable range.
     struct Task {
@@ -317,7 +348,7 @@ void pack_range(HostPool *pool, const gp_circuit_view *cs, PackPlan &pp, uint8_t
         const CircuitMeta &m = pp.metas[tk.c];
         if (tk.kind == 0) {
             const uint32_t g0 = v.gate_offsets[0], n0 = v.noise_offsets[0];
-            ProbIndex pidx{&keys};
+            ProbCache pidx{&pp.dict};
             for (uint32_t i = tk.a; i < tk.b; i++) {
                 const uint32_t li = m.layer_base + i;
                 lay_gate[li] = (uint32_t)(m.gate_base + v.gate_offsets[i] - g0);
@@ -332,7 +363,7 @@ void pack_range(HostPool *pool, const gp_circuit_view *cs, PackPlan &pp, uint8_t
                         flip[m.meas_base + hi] = v.gate_flip[g];
                         meas++;
                     }
-                    gates[m.gate_base + g - g0] = (uint64_t)hi << 32 | (v.gate_q0[g] | (uint32_t)kd << kGateKindShift);
+                    put64(&gates[m.gate_base + g - g0], (uint64_t)hi << 32 | (v.gate_q0[g] | (uint32_t)kd << kGateKindShift));
                 }
                 lay_meas[li] = meas;  // count; prefix in pack_finish
                 uint32_t src = 0;
@@ -340,15 +371,23 @@ void pack_range(HostPool *pool, const gp_circuit_view *cs, PackPlan &pp, uint8_t
                     const uint8_t kd = v.noise_kind[o];
                     const uint64_t idx = m.noise_base + o - n0;
                     uint64_t pi = 0;
-                    if (t.wide_prob) nprob[idx] = v.noise_prob[o];
-                    else pi = pidx(v.noise_prob[o]);
-                    noise[idx] = (uint64_t)v.noise_q0[o] |
-                                 (uint64_t)(kd == GP_NOISE_DEPOLARIZE2 ? v.noise_q1[o] : 0) << kNoiseQubitBits |
-                                 (uint64_t)kd << kNoiseKindShift | pi << kNoisePidxShift;
+                    if (t.wide_prob) {
+                        nprob[idx] = v.noise_prob[o];
+                    } else {
+                        pi = pidx(v.noise_prob[o]);
+                        if (pi == ProbDict::kFull) {  // more distinct values than the table: repack wide
+                            pp.need_wide.store(true, std::memory_order_relaxed);
+                            pi = 0;
+                        }
+                    }
+                    put64(&noise[idx], (uint64_t)v.noise_q0[o] |
+                                           (uint64_t)(kd == GP_NOISE_DEPOLARIZE2 ? v.noise_q1[o] : 0) << kNoiseQubitBits |
+                                           (uint64_t)kd << kNoiseKindShift | pi << kNoisePidxShift);
                     src += components(kd, level);
                 }
                 lay_src[li] = src;  // count; prefix in pack_finish
             }
+            put_fence();
             if (tk.b == m.l) {  // closing entries of the circuit's layer tables
                 const uint32_t li = m.layer_base + m.l;
                 lay_gate[li] = (uint32_t)(m.gate_base + v.gate_offsets[m.l] - g0);
@@ -401,6 +440,10 @@ int validate_leaves(const gp_circuit_view *cs, size_t c0, size_t c1) {
 
 void pack_finish(PackPlan &pp, uint8_t *img) {
     BatchTotals &t = pp.t;
+    if (!t.wide_prob) {
+        pp.dict.values(pp.prob_table);
+        t.prob_table_n = (uint32_t)pp.prob_table.size();  // (the layout keeps its reserve)
+    }
     const StageLayout &L = pp.L;
     auto *lay_noise = (uint32_t *)(img + L.lay_noise);
     auto *lay_meas = (uint32_t *)(img + L.lay_meas);

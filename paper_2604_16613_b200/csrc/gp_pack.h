@@ -53,20 +53,48 @@ private:
 // Per-circuit results of the packer (validation codes in reference order).
 enum PackErr : int { kPackOk = 0, kPackIndexSpace = 1, kPackDetLeaf = 2, kPackObsLeaf = 3, kPackTooWide = 4 };
 
+// Distinct noise probabilities (bit patterns) -> table index, filled
+// concurrently while the noise ops are packed (first come, first indexed):
+// the probabilities are read once, by the packer itself.
+class ProbDict {
+public:
+    static constexpr uint32_t kSlots = 1u << 16;  // >= 4 x table capacity
+    static constexpr uint32_t kFull = 0xFFFFFFFFu;
+    ProbDict();
+    void clear();                  // O(entries)
+    uint32_t index(uint64_t bits);  // inserts; kFull beyond kNoisePidxMax + 1 entries
+    uint32_t size() const;
+    void values(std::vector<double> &out) const;  // by index
+
+private:
+    static constexpr uint32_t kEmpty = 0xFFFFFFFFu, kBusy = 0xFFFFFFFEu;
+    std::unique_ptr<std::atomic<uint64_t>[]> key_;
+    std::unique_ptr<std::atomic<uint32_t>[]> val_;
+    std::unique_ptr<uint32_t[]> slot_of_;  // [kNoisePidxMax + 2] index -> slot
+    std::atomic<uint32_t> n_{0};
+};
+
 struct PackPlan {
     BatchTotals t{};
     std::vector<CircuitMeta> metas;
     StageLayout L{};
-    std::vector<double> prob_table;  // sorted distinct noise probabilities (bit patterns)
+    std::vector<double> prob_table;  // distinct noise probabilities by table index (pack_head)
+    ProbDict dict;
+    bool force_wide = false;            // in: per-op fp64 probabilities
+    std::atomic<bool> need_wide{false};  // out: more distinct probabilities than the table holds
     int err = kPackOk;               // first failing circuit's error
     size_t err_circuit = 0;
+    // Bytes of the packed image to upload (the probability table is last and
+    // reserved at its maximum size).
+    uint64_t image_bytes() const { return L.prob_table + (uint64_t)t.prob_table_n * 8; }
 };
 
 // Byte offsets of every array of a staging image with these totals.
 StageLayout stage_layout(const BatchTotals &t);
 
-// Phase 0 (sizes, bases, index-space checks) + probability table. Cheap:
-// O(C) plus one parallel pass over noise probabilities.
+// Phase 0 (sizes, bases, index-space checks, layout). O(C). With
+// force_wide unset the noise probabilities go through the table; if
+// pack_range then sets need_wide, plan and pack again with force_wide.
 void pack_plan(HostPool *pool, const gp_circuit_view *cs, size_t C, uint8_t level, PackPlan &pp);
 
 // Leaf checks of circuits [c0, c1) only (init_leaves, eec.cpp:40-58): the
@@ -83,7 +111,7 @@ void pack_range(HostPool *pool, const gp_circuit_view *cs, PackPlan &pp, uint8_t
 void pack_finish(PackPlan &pp, uint8_t *img);
 
 // Phase 3: meta and cumulative per-circuit tables at the head of the image
-// (needs the traversal group width T).
+// (needs the traversal group width T), the probability table at its end.
 void pack_head(const PackPlan &pp, uint32_t T, uint8_t *img);
 
 }  // namespace gp
