@@ -22,7 +22,11 @@
 // only when two keys tie, so distinct signatures never merge
 // (dem.cpp:73-78, test_dem.cpp:94-101).
 
+#include <type_traits>
+
 namespace red {
+
+constexpr uint32_t kBucketThreads = 128, kWarpItems = 256;  // bucket_kernel: a warp groups up to kWarpItems
 
 
 // Slots of source s's records sorted by word (insertion sort, n <= 16).
@@ -578,6 +582,8 @@ __device__ void group_bucket(const DevPlan &p, const Team &tm, uint32_t b, uint3
     tm.sync();
     // 2. members grouped by representative; sorted ascending fold per group
     const uint32_t G = scan_groups(tm, w, n);
+    constexpr bool kWarp = std::is_same<Team, WarpTeam>::value;
+    {
     for (uint32_t i = t0; i < n; i += nt) {
         const uint32_t r = w.rep[i];
         w.mp[w.off[r] + atomicSub(&w.cnt[r], 1u) - 1] = it[i].prob;
@@ -601,7 +607,21 @@ __device__ void group_bucket(const DevPlan &p, const Team &tm, uint32_t b, uint3
         v[0] = acc;
     }
     tm.sync();
-    // 3. groups in canonical order: bitonic ("flip" form) on representatives
+    }
+    // 3. groups in canonical order. A warp with at most 32 groups ranks them
+    // (one group per lane, keys distinct); otherwise bitonic ("flip" form).
+    if (kWarp && G <= 32) {
+        const uint32_t lane = t0;
+        const uint32_t mine = lane < G ? w.grp[lane] : 0;
+        uint32_t rank = 0;
+        if (lane < G) {
+            const Item me = it[mine];
+            for (uint32_t h = 0; h < G; h++) rank += (h != lane && key_cmp(it[w.grp[h]], me) < 0) ? 1u : 0u;
+        }
+        __syncwarp();
+        if (lane < G) w.grp[rank] = (uint16_t)mine;
+        __syncwarp();
+    } else {
     uint32_t np = 1;
     while (np < G) np <<= 1;
     auto cas = [&](uint32_t x, uint32_t y) {
@@ -624,6 +644,7 @@ __device__ void group_bucket(const DevPlan &p, const Team &tm, uint32_t b, uint3
             }
             tm.sync();
         }
+    }
     }
     // 4. edges
     uint32_t nd = 0, no = 0;
@@ -761,7 +782,6 @@ __device__ void bucket_cta(const DevPlan &p, uint32_t b, uint32_t n, uint32_t D,
     }
 }
 
-constexpr uint32_t kBucketThreads = 128, kWarpItems = 256;
 constexpr uint32_t kWarpTab = 512;                                   // >= 2 kWarpItems
 constexpr uint32_t kWarpWs = (256 * 18 + 16 + 512 * 2 + 15) & ~15u;  // GroupWs::bytes(256, 512)
 constexpr uint32_t kHugeSmem = 196 * 1024;                            // huge_kernel dynamic smem

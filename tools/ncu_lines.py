@@ -1,10 +1,11 @@
 """Per-source-line hot spots of one kernel in an ncu report (developer tool).
-usage: python tools/ncu_lines.py report.ncu-rep [top]"""
+usage: python tools/ncu_lines.py report.ncu-rep [top] [kernel-regex]"""
 import csv, subprocess, sys
 
 rep = sys.argv[1]
 top = int(sys.argv[2]) if len(sys.argv) > 2 else 25
-out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"],
+kfilt = ["--kernel-name", "regex:" + sys.argv[3]] if len(sys.argv) > 3 else []
+out = subprocess.run(["ncu", "-i", rep, *kfilt, "--page", "source", "--csv", "--print-source", "cuda,sass"],
                      capture_output=True, text=True).stdout
 rows = list(csv.reader(out.splitlines()))
 fname, hdr, lines = "?", None, []
