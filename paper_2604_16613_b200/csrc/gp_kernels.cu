@@ -16,6 +16,7 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <cstdio>
 #include <mutex>
 #include <set>
 #include <utility>
@@ -557,6 +558,13 @@ bool plan_traversal(const BatchTotals &t, int device, TravCfg *cfg, size_t *smem
     const uint32_t n2 = 2 * t.max_n;
     c.node_warps = n2 <= 512 ? 4 : n2 <= 2048 ? 8 : 12;
     c.emit_warps = c.node_warps;
+    if (const char *o = std::getenv("GP_TRAV_WARPS")) {  // tuning: "node,emit"
+        unsigned a = 0, b = 0;
+        if (std::sscanf(o, "%u,%u", &a, &b) == 2 && a && b) {
+            c.node_warps = a;
+            c.emit_warps = b;
+        }
+    }
     // Wide groups (one CTA per circuit, atomic-free emission) when the batch
     // alone fills the machine; one word per CTA for single large circuits.
     uint32_t T = 1;
@@ -674,7 +682,7 @@ int enqueue_pipeline(const DevPlan &p, cudaStream_t st, const StageEvents *ev, c
     } else if (p.tot.groups) {
         const TravCfg &c = p.trav;
         const int threads = 32 * (1 + (int)c.node_warps + (int)c.emit_warps);
-        const uint32_t tm = c.T <= 1 ? 1 : c.T <= 2 ? 2 : c.T <= 4 ? 4 : 8;
+        const uint32_t tm = c.T <= 1 ? 1 : c.T <= 2 ? 2 : c.T <= 4 ? 4 : c.T <= 6 ? 6 : 8;
         auto launch = [&](auto kern) {
             smem_optin(kern);
             kern<<<(uint32_t)p.tot.groups, threads, p.trav_smem, st>>>(p, c);
@@ -682,6 +690,7 @@ int enqueue_pipeline(const DevPlan &p, cudaStream_t st, const StageEvents *ev, c
         if (tm == 1) launch(trav::traverse_kernel<1>);
         else if (tm == 2) launch(trav::traverse_kernel<2>);
         else if (tm == 4) launch(trav::traverse_kernel<4>);
+        else if (tm == 6) launch(trav::traverse_kernel<6>);  // (6-word circuits: [[72,12,6]] branches)
         else launch(trav::traverse_kernel<8>);
         launches++;
         if (p.pool_chunks_cap) {
