@@ -558,6 +558,13 @@ bool plan_traversal(const BatchTotals &t, int device, TravCfg *cfg, size_t *smem
     const uint32_t n2 = 2 * t.max_n;
     c.node_warps = n2 <= 512 ? 4 : n2 <= 2048 ? 8 : 12;
     c.emit_warps = c.node_warps;
+    if (t.C >= 2u * (uint32_t)sms && t.max_W <= 8 && n2 <= 512) {
+        // wide-group batches of small circuits: emission (source expansion) is
+        // the heavier role; 224 threads and a 2-deep state ring fit four CTAs
+        // per SM (registers and shared memory), which beats deeper rings
+        c.node_warps = 2;
+        c.emit_warps = 4;
+    }
     if (const char *o = std::getenv("GP_TRAV_WARPS")) {  // tuning: "node,emit"
         unsigned a = 0, b = 0;
         if (std::sscanf(o, "%u,%u", &a, &b) == 2 && a && b) {
@@ -571,7 +578,7 @@ bool plan_traversal(const BatchTotals &t, int device, TravCfg *cfg, size_t *smem
     if (t.C >= 2u * (uint32_t)sms && t.max_W <= 8) T = t.max_W;
     // Batches: shallow rings (more CTAs per SM); single circuits: deep rings
     // (the copy latency of a boundary's stage hides behind NST-1 boundaries).
-    static const uint32_t kBatch[][2] = {{3, 3}, {2, 3}, {2, 2}};
+    static const uint32_t kBatch[][2] = {{2, 3}, {2, 2}, {3, 3}};
     static const uint32_t kSingle[][2] = {{6, 8}, {4, 8}, {4, 6}, {4, 4}, {3, 3}, {2, 2}};
     if (T == 1) {  // split traversal: walk_kernel + emit_kernel
         c.T = 1;
@@ -605,8 +612,11 @@ bool plan_traversal(const BatchTotals &t, int device, TravCfg *cfg, size_t *smem
         const bool batch = T > 1;
         const uint32_t(*opts)[2] = batch ? kBatch : kSingle;
         const int nopt = batch ? 3 : 6;
+        uint32_t force_r = 0, force_n = 0;  // tuning: GP_TRAV_RN="R,NST"
+        if (const char *o = std::getenv("GP_TRAV_RN")) std::sscanf(o, "%u,%u", &force_r, &force_n);
         for (int o = 0; o < nopt; o++) {
-            const uint32_t R = opts[o][0], N = opts[o][1];
+            uint32_t R = opts[o][0], N = opts[o][1];
+            if (force_r && force_n) R = force_r, N = force_n;
             const trav::Dims d(T, R, N, t.max_n, t.max_layer_meas, t.max_layer_noise, t.max_l);
             if (d.total_bytes() <= budget) {
                 c.T = T;
