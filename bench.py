@@ -192,7 +192,7 @@ def run_reference(args, dist):
                          "cpu": model},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
-    print(json.dumps(line), flush=True)
+    emit_line(line)
 
 
 def single_circuit_block(compiler, ref_ok: bool, quick: bool):
@@ -233,6 +233,49 @@ def single_circuit_block(compiler, ref_ok: bool, quick: bool):
                 entry["ref_hyperedges_per_s"] = e / (rp50 / 1e3)
                 entry["speedup_p50"] = rp50 / p50
             out[f"{name}_L{lv}"] = entry
+    return out
+
+
+def sharded_single_block(compiler, dist, reps: int = 10):
+    """one large circuit (surface d25 r25, L0) compiled across
+    the ranks by fault-range sharding -- shard compile into device tables,
+    NCCL all-gather, merge on rank 0 -- wall p50 (max over ranks), with the
+    one-GPU compile of the same circuit beside it and the merged DEM checked
+    byte for byte against it."""
+    import socket
+
+    import torch.distributed as td
+
+    import paper_2604_16613_b200 as gp
+    from paper_2604_16613_b200.shard import compile_sharded
+    if not td.is_initialized():  # N = 1 (--sharded): a one-rank NCCL group
+        with socket.socket() as sk:
+            sk.bind(("127.0.0.1", 0))
+            port = sk.getsockname()[1]
+        td.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1)
+    g = gp.gen_surface(25, 25, 1e-3)
+    for _ in range(3):
+        compile_sharded(compiler, g, 0)
+    ts = []
+    dem = None
+    for _ in range(reps):
+        dist.barrier()
+        t = time.perf_counter()
+        dem = compile_sharded(compiler, g, 0)
+        dist.barrier()
+        ts.append(dist.max(time.perf_counter() - t))
+    out = {"circuit": "surface_d25_r25_paper_L0", "shards": max(dist.ws, 1),
+           "p50_ms": statistics.median(ts) * 1e3}
+    if dist.rank == 0:
+        whole = compiler.compile(g, 0)
+        tw = []
+        for _ in range(reps):
+            t = time.perf_counter()
+            compiler.compile(g, 0)
+            tw.append(time.perf_counter() - t)
+        out["one_gpu_p50_ms"] = statistics.median(tw) * 1e3
+        out["identical"] = dem.to_text() == whole.to_text()
+        out["edges"] = dem.num_edges
     return out
 
 
@@ -375,11 +418,33 @@ def run_gpu(args, dist):
                                           f"on a {threads}-thread pool ({wall:.2f} s wall)", "cpu": model}
     if rank == 0 and ws == 1 and not args.no_single:
         line["single_circuit"] = single_circuit_block(compiler, ref_ok=not args.no_cpu_baseline, quick=args.quick)
+    if ws > 1 or args.sharded:
+        blk = sharded_single_block(compiler, dist)
+        if rank == 0:
+            line["sharded_single"] = blk
     if rank == 0:
-        print(json.dumps(line), flush=True)
+        emit_line(line)
+
+
+_JSON_FD = None
+
+
+def emit_line(line: dict) -> None:
+    """The one JSON line, on the original stdout (everything else -- library
+    or NCCL chatter included -- goes to stderr, see main)."""
+    data = (json.dumps(line) + "\n").encode()
+    if _JSON_FD is None:
+        sys.stdout.write(data.decode())
+        sys.stdout.flush()
+    else:
+        os.write(_JSON_FD, data)
 
 
 def main():
+    global _JSON_FD
+    sys.stdout.flush()
+    _JSON_FD = os.dup(1)
+    os.dup2(2, 1)  # fd 1 -> stderr for the rest of the run
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
@@ -391,6 +456,7 @@ def main():
     ap.add_argument("--ref-sample", type=int, default=512)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-single", action="store_true")
+    ap.add_argument("--sharded", action="store_true", help="also at N=1: fault-range sharded d25 block (over NCCL)")
     ap.add_argument("--quick", action="store_true")
     ap.add_argument("--ncu-traffic", type=float, default=None)
     args = ap.parse_args()
