@@ -378,6 +378,29 @@ __global__ void scan_apply_kernel(F f, uint64_t n, const uint4 *bsum, uint4 *out
     }
 }
 
+// The whole scan in one launch when it fits one tile (small compiles: a
+// launch saved is a few microseconds of latency).
+template <class F>
+__global__ void scan_single_kernel(F f, uint64_t n, uint4 *out, uint4 *total_out) {
+    uint4 v[kScanItems];
+    uint4 acc = make_uint4(0, 0, 0, 0);
+#pragma unroll
+    for (int k = 0; k < kScanItems; k++) {
+        const uint64_t idx = (uint64_t)threadIdx.x * kScanItems + k;
+        v[k] = idx < n ? f(idx) : make_uint4(0, 0, 0, 0);
+        acc = add4(acc, v[k]);
+    }
+    uint4 tot;
+    uint4 run = block_excl_scan(acc, &tot);
+#pragma unroll
+    for (int k = 0; k < kScanItems; k++) {
+        const uint64_t idx = (uint64_t)threadIdx.x * kScanItems + k;
+        if (idx < n) out[idx] = run;
+        run = add4(run, v[k]);
+    }
+    if (threadIdx.x == 0) *total_out = tot;
+}
+
 struct BucketScanF {
     const uint32_t *bcount;
     __device__ bool active(uint64_t) const { return true; }
@@ -490,6 +513,11 @@ void launch_scan(F f, uint64_t n, uint4 *bsum, uint4 *out, uint4 *total, cudaStr
     const uint32_t nb = (uint32_t)((n + kScanTile - 1) / kScanTile);
     if (nb == 0) {
         cudaMemsetAsync(total, 0, sizeof(uint4), st);
+        return;
+    }
+    if (nb == 1) {
+        scan_single_kernel<<<1, kScanThreads, 0, st>>>(f, n, out, total);
+        *launches += 1;
         return;
     }
     scan_reduce_kernel<<<nb, kScanThreads, 0, st>>>(f, n, bsum);
@@ -738,7 +766,9 @@ reduce:
         red::bucket_kernel<<<(uint32_t)std::min<uint64_t>(std::max<uint64_t>(ctas, 1), 148 * 32),
                              red::kBucketThreads, 0, st>>>(p);
         smem_optin(red::huge_kernel);
-        red::huge_kernel<<<kHugeCtas, 256, red::kHugeSmem, st>>>(p);
+        // (a bucket over kWarpItems sources: at most S / (kWarpItems + 1) of them)
+        const uint32_t hgrid = (uint32_t)std::min<uint64_t>(kHugeCtas, std::max<uint64_t>(1, S / (red::kWarpItems + 1)));
+        red::huge_kernel<<<hgrid, 256, red::kHugeSmem, st>>>(p);
         launches += 2;
     }
     mark(kProfBucket);
