@@ -181,6 +181,7 @@ size_t carve(gp_ctx *ctx, DevPlan &p, const BatchTotals &t, uint8_t *base, uint3
     p.oscan = (uint4 *)take((NB + 1) * 16);
     p.e_src = (uint32_t *)take(items_cap * 4);
     p.e_ndno = (uint32_t *)take(items_cap * 4);
+    p.e_item = (uint32_t *)take(items_cap * 4);
     p.e_prob = (double *)take(items_cap * 8);
     p.huge = (uint32_t *)take(NB * 4);
     if (p.mode == gp::kModeShard) {  // compact partial table of the shard

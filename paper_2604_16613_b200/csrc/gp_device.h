@@ -71,6 +71,7 @@ struct DevPlan {
     uint4 *oscan;      // [NB + 1]
     // Per group (edge), at the bucket's slots: representative, probability, ids.
     uint32_t *e_src, *e_ndno;
+    uint32_t *e_item;  // representative's sort item (complete keys), or ~0: ids from the records
     double *e_prob;
     uint32_t *huge;    // [NB] buckets too large for a warp
     uint64_t ids_cap;

@@ -382,6 +382,7 @@ __device__ __forceinline__ uint32_t emit_group(const DevPlan &p, uint32_t base, 
     const uint32_t rep = at(i0).src;
     const uint32_t ndno = at(i0).ndno & 0x7FFFFFFFu;
     p.e_src[base + g] = rep;
+    p.e_item[base + g] = 0xFFFFFFFFu;  // (exact path: ids from the records)
     p.e_prob[base + g] = acc;
     p.e_ndno[base + g] = ndno;
     return ndno;
@@ -652,6 +653,7 @@ __device__ void group_bucket(const DevPlan &p, const Team &tm, uint32_t b, uint3
         const uint32_t r = w.grp[g];
         const uint32_t v = it[r].ndno & 0x7FFFFFFFu;
         p.e_src[base + g] = it[r].src;
+        p.e_item[base + g] = base + r;  // complete key: write_kernel decodes the ids from the item
         p.e_prob[base + g] = w.mp[w.off[r]];
         p.e_ndno[base + g] = v;
         nd += v & 0xFFFF;
@@ -894,7 +896,9 @@ __global__ void write_kernel(__grid_constant__ const DevPlan p, const uint4 *out
         if (ne == 0) continue;
         const uint4 o = p.oscan[b];  // (edges, det ids, obs ids) before this bucket
         const uint32_t base = p.boff[b].x;
-        const uint32_t D = meta[bucket_circuit(p, b)].D;
+        const CircuitMeta &cm = meta[bucket_circuit(p, b)];
+        const uint32_t D = cm.D, q0 = (uint32_t)b - cm.bucket_base;  // first detector + 1 (0: none)
+        const Item *items = items_of(p);
         uint32_t dcar = 0, ocar = 0;
         for (uint32_t k0 = 0; k0 < ne; k0 += 32) {
             const uint32_t k = k0 + lane;
@@ -919,19 +923,34 @@ __global__ void write_kernel(__grid_constant__ const DevPlan p, const uint4 *out
                 p.o_det_off[e] = bD + d0;
                 p.o_obs_off[e] = bO + o0;
                 p.o_prob[e] = p.e_prob[base + k];
-                const uint32_t r = p.e_src[base + k];
-                uint8_t ord[16];
-                const uint32_t n = min(p.cnt[r], 16u);
-                sig_order(p, r, n, ord);
-                uint32_t wd = d0, wo = o0;
-                for (uint32_t x = 0; x < n; x++) {
-                    const uint32_t t = p.rtile[rec_at(p, r, ord[x])];
-                    uint64_t bits = p.rbits[rec_at(p, r, ord[x])];
-                    while (bits) {
-                        const uint32_t id = t * 64 + (uint32_t)__ffsll((long long)bits) - 1;
-                        bits &= bits - 1;
-                        if (id < D) p.o_det[wd++] = id;
-                        else p.o_obs[wo++] = id - D;
+                const uint32_t ii = p.e_item[base + k];
+                if (ii != 0xFFFFFFFFu) {  // complete key: detectors q0 - 1 + slot deltas, observables by mask
+                    const Item q = items[ii];
+                    uint32_t wd = d0, wo = o0;
+                    if (q0) {
+                        p.o_det[wd++] = q0 - 1;
+                        for (uint32_t x = 0; x < 16; x++) {
+                            const uint32_t v = (q.k[x >> 1] >> ((x & 1) ? 0 : 16)) & 0xFFFF;
+                            if (v == 0) break;
+                            p.o_det[wd++] = q0 - 1 + v;
+                        }
+                    }
+                    for (uint64_t ob = q.obs; ob; ob &= ob - 1) p.o_obs[wo++] = (uint32_t)__ffsll((long long)ob) - 1;
+                } else {  // ids from the representative's records, in word order
+                    const uint32_t r = p.e_src[base + k];
+                    uint8_t ord[16];
+                    const uint32_t n = min(p.cnt[r], 16u);
+                    sig_order(p, r, n, ord);
+                    uint32_t wd = d0, wo = o0;
+                    for (uint32_t x = 0; x < n; x++) {
+                        const uint32_t t = p.rtile[rec_at(p, r, ord[x])];
+                        uint64_t bits = p.rbits[rec_at(p, r, ord[x])];
+                        while (bits) {
+                            const uint32_t id = t * 64 + (uint32_t)__ffsll((long long)bits) - 1;
+                            bits &= bits - 1;
+                            if (id < D) p.o_det[wd++] = id;
+                            else p.o_obs[wo++] = id - D;
+                        }
                     }
                 }
             }
