@@ -169,13 +169,19 @@ struct ProbCache {
     uint64_t k[4] = {~0ull, ~0ull, ~0ull, ~0ull};
     uint32_t v[4] = {ProbDict::kFull, ProbDict::kFull, ProbDict::kFull, ProbDict::kFull};
     uint32_t next = 0;
+    uint32_t last = 0;
     uint32_t operator()(double p) {
         const uint64_t b = bits_of(p);
-        for (int i = 0; i < 4; i++)
-            if (k[i] == b) return v[i];
+        if (k[last] == b) return v[last];  // runs of one value: one compare
+        for (uint32_t i = 0; i < 4; i++)
+            if (k[i] == b) {
+                last = i;
+                return v[i];
+            }
         const uint32_t x = d->index(b);
         k[next] = b;
         v[next] = x;
+        last = next;
         next = (next + 1) & 3;
         return x;
     }
@@ -349,6 +355,8 @@ void pack_range(HostPool *pool, const gp_circuit_view *cs, PackPlan &pp, uint8_t
         if (tk.kind == 0) {
             const uint32_t g0 = v.gate_offsets[0], n0 = v.noise_offsets[0];
             ProbCache pidx{&pp.dict};
+            uint32_t comp_tab[8];  // components per noise kind (stepg.cpp:66-103)
+            for (uint32_t x = 0; x < 8; x++) comp_tab[x] = components((uint8_t)x, level);
             for (uint32_t i = tk.a; i < tk.b; i++) {
                 const uint32_t li = m.layer_base + i;
                 lay_gate[li] = (uint32_t)(m.gate_base + v.gate_offsets[i] - g0);
@@ -383,7 +391,7 @@ void pack_range(HostPool *pool, const gp_circuit_view *cs, PackPlan &pp, uint8_t
                     put64(&noise[idx], (uint64_t)v.noise_q0[o] |
                                            (uint64_t)(kd == GP_NOISE_DEPOLARIZE2 ? v.noise_q1[o] : 0) << kNoiseQubitBits |
                                            (uint64_t)kd << kNoiseKindShift | pi << kNoisePidxShift);
-                    src += components(kd, level);
+                    src += comp_tab[kd & 7];
                 }
                 lay_src[li] = src;  // count; prefix in pack_finish
             }
