@@ -416,6 +416,44 @@ __global__ void __launch_bounds__(800, 1) traverse_kernel(__grid_constant__ cons
             const uint32_t *s_src = L.src(smem, k) + h->src_shift;
             const uint64_t *now = L.slot(smem, r);
             const uint32_t nops = (cfg.debug & 1) ? 0 : h->n1 - h->n0;
+            if (TM > 1 && direct && nops) {
+                // Source-major: consecutive lanes take consecutive sources of
+                // the layer (an op's components are consecutive sources), so
+                // the signature stores of a warp are coalesced. Lane -> op by a
+                // binary search over the ops' first-source offsets.
+                const uint32_t sfirst = s_src[0];
+                const uint32_t klast = noise_kind(s_noise[nops - 1]);
+                const uint32_t ncl = klast <= 1 ? 1 : klast == 2 ? (level ? 3 : 2) : (level == 0 ? 6 : level == 1 ? 10 : 15);
+                const uint32_t ns = s_src[nops - 1] + ncl - sfirst;
+                for (uint32_t i = te; i < ns; i += emit_threads) {
+                    const uint32_t ls = sfirst + i;
+                    uint32_t lo = 0, hi = nops;
+                    while (hi - lo > 1) {
+                        const uint32_t mid = (lo + hi) >> 1;
+                        if (s_src[mid] <= ls) lo = mid;
+                        else hi = mid;
+                    }
+                    const uint64_t wd = s_noise[lo];
+                    const uint32_t kind = noise_kind(wd), c = ls - s_src[lo];
+                    const uint32_t q0 = noise_q0(wd), q1 = noise_q1(wd);
+                    const uint32_t mk = kind == 0 ? 1u : kind == 1 ? 2u : kind == 2 ? (c == 0 ? 1u : c == 1 ? 2u : 3u)
+                                                                                    : (uint32_t)kMask[c];
+                    uint64_t v[TM];
+#pragma unroll
+                    for (int w = 0; w < TM; w++) {
+                        uint64_t x = 0;
+                        if ((uint32_t)w < tw) {
+                            const uint64_t *row = now + (size_t)w * n2;
+                            if (mk & 1) x ^= row[2 * q0];
+                            if (mk & 2) x ^= row[2 * q0 + 1];
+                            if (mk & 4) x ^= row[2 * q1];
+                            if (mk & 8) x ^= row[2 * q1 + 1];
+                        }
+                        v[w] = x;
+                    }
+                    emit_source<TM>(p, m.src_base + ls, t0, tw, v, direct);
+                }
+            } else
             // Warp-uniform trip count (the pool path needs whole-warp rounds).
             for (uint32_t ob = te - lane; ob < nops; ob += emit_threads) {
                 const uint32_t o = ob + lane;
