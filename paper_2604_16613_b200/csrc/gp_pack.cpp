@@ -193,7 +193,7 @@ struct ProbCache {
 
 ProbDict::ProbDict()
     : key_(new std::atomic<uint64_t>[kSlots]), val_(new std::atomic<uint32_t>[kSlots]),
-      slot_of_(new uint32_t[kNoisePidxMax + 2]) {
+      slot_of_(new uint32_t[kSlotLog]) {
     for (uint32_t x = 0; x < kSlots; x++) {
         key_[x].store(0, std::memory_order_relaxed);
         val_[x].store(kEmpty, std::memory_order_relaxed);
@@ -201,7 +201,7 @@ ProbDict::ProbDict()
 }
 
 void ProbDict::clear() {
-    const uint32_t n = std::min<uint32_t>(n_.load(), kNoisePidxMax + 2);
+    const uint32_t n = std::min<uint32_t>(n_.load(), kSlotLog);
     for (uint32_t i = 0; i < n; i++) val_[slot_of_[i]].store(kEmpty, std::memory_order_relaxed);
     n_.store(0);
 }
@@ -214,10 +214,12 @@ uint32_t ProbDict::index(uint64_t bits) {
     for (;;) {
         uint32_t v = val_[x].load(std::memory_order_acquire);
         if (v == kEmpty) {
+            // Full table: no new claims (only the racing few, all logged for clear()).
+            if (n_.load(std::memory_order_relaxed) > kNoisePidxMax) return kFull;
             if (val_[x].compare_exchange_strong(v, kBusy, std::memory_order_acq_rel)) {
                 key_[x].store(bits, std::memory_order_relaxed);
                 const uint32_t i = n_.fetch_add(1);
-                if (i < kNoisePidxMax + 2) slot_of_[i] = x;
+                if (i < kSlotLog) slot_of_[i] = x;
                 val_[x].store(i, std::memory_order_release);
                 return i <= kNoisePidxMax ? i : kFull;
             }

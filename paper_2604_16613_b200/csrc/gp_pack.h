@@ -68,9 +68,10 @@ public:
 
 private:
     static constexpr uint32_t kEmpty = 0xFFFFFFFFu, kBusy = 0xFFFFFFFEu;
+    static constexpr uint32_t kSlotLog = kNoisePidxMax + 1 + 4096;  // claims logged for clear() (+ racing threads)
     std::unique_ptr<std::atomic<uint64_t>[]> key_;
     std::unique_ptr<std::atomic<uint32_t>[]> val_;
-    std::unique_ptr<uint32_t[]> slot_of_;  // [kNoisePidxMax + 2] index -> slot
+    std::unique_ptr<uint32_t[]> slot_of_;  // [kSlotLog] index -> slot
     std::atomic<uint32_t> n_{0};
 };
 

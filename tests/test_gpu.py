@@ -279,8 +279,9 @@ def test_cpp_dropin_shim(tmp_path):
 
 
 def test_many_distinct_probabilities_use_wide_mode(compiler, port):
-    """> 64 distinct noise probabilities in a circuit: per-op fp64 upload path
-    (the probability table would not be exact otherwise); results unchanged."""
+    """Distinct noise probabilities: up to 16383 per batch go through the
+    packer's dictionary (14-bit table index); beyond that the batch is packed
+    again with per-op fp64 probabilities. Results unchanged either way."""
     import random
     rng = random.Random(5)
     g = gp.gen_surface(5, 3, 1e-3).to_circuit()
@@ -291,6 +292,22 @@ def test_many_distinct_probabilities_use_wide_mode(compiler, port):
     batch = compiler.compile_batch([g, small], 1)
     assert batch[0].hyperedges() == port.compile(g, 1)[0]
     assert batch[1].hyperedges() == port.compile(small, 1)[0]
+    # two circuits of ~14k distinct values each: the batch overflows the table
+    big = []
+    for seed in (1, 2):
+        c = gp.gen_surface(11, 11, 1e-3).to_circuit()
+        r = random.Random(seed)
+        c.noise_prob = np.array([r.uniform(1e-4, 3e-3) for _ in c.noise_prob])
+        big.append(c)
+    assert len(set(big[0].noise_prob.tolist()) | set(big[1].noise_prob.tolist())) > 16383
+    dems = compiler.compile_batch(big, 0)
+    assert compiler.last_stats["h2d_bytes"] > 8 * (len(big[0].noise_prob) + len(big[1].noise_prob))  # fp64 per op
+    for c, d in zip(big, dems):
+        assert d.hyperedges() == port.compile(c, 0)[0]
+        assert d.to_text() == compiler.compile(c, 0).to_text()  # (alone: the table path)
+    again = compiler.compile_batch(big, 0)  # the dictionary is reset between batches
+    assert [d.to_text() for d in again] == [d.to_text() for d in dems]
+    assert compiler.compile(small, 1).hyperedges() == port.compile(small, 1)[0]
 
 
 def test_pipelined_batch_matches_unpipelined():
