@@ -417,3 +417,16 @@ def test_compile_sharded_over_nccl_single_rank():
         assert compile_sharded(comp, g, 2).to_text() == comp.compile(g, 2).to_text()
     finally:
         td.destroy_process_group()
+
+
+@pytest.mark.parametrize("level", [0, 1, 2])
+def test_direct_batch_traversal_all_levels(compiler, port, level):
+    """>= 2 x SMs circuits take the batch traversal (one CTA per circuit, all
+    six words, source-major emission of every component kind); each DEM
+    equals the single-circuit compile (the split walk path) and the oracle."""
+    gens = [gp.gen_bb72_branch(b, rounds=2) for b in range(300)] + [gp.gen_surface(3, 2, 2e-3),
+                                                                    gp.gen_bb72_branch(5)]  # W = 6: 6-word CTAs
+    dems = compiler.compile_batch(gens, level)
+    for i in (0, 1, 150, 299, 300, 301):
+        assert dems[i].to_text() == compiler.compile(gens[i], level).to_text()
+    assert dems[7].hyperedges() == port.compile(gens[7].to_circuit(), level)[0]
