@@ -473,11 +473,13 @@ struct WarpTeam {
     __device__ uint32_t t0() const { return threadIdx.x & 31; }
     __device__ uint32_t nt() const { return 32; }
     __device__ void sync() const { __syncwarp(); }
+    __device__ bool any(bool v) const { return __any_sync(0xffffffffu, v); }
 };
 struct CtaTeam {
     __device__ uint32_t t0() const { return threadIdx.x; }
     __device__ uint32_t nt() const { return blockDim.x; }
     __device__ void sync() const { __syncthreads(); }
+    __device__ bool any(bool v) const { return __syncthreads_or(v) != 0; }
 };
 
 // Shared workspace of one team for a bucket of up to `cap` (< 65535) items;
@@ -554,16 +556,20 @@ __device__ __forceinline__ uint32_t scan_groups(const Team &tm, const GroupWs &w
     return G;
 }
 
+// Returns false, having written nothing, when some key of the bucket is
+// incomplete (found while hashing): the caller takes the exact path.
 template <class Team>
-__device__ void group_bucket(const DevPlan &p, const Team &tm, uint32_t b, uint32_t base, uint32_t n,
+__device__ bool group_bucket(const DevPlan &p, const Team &tm, uint32_t b, uint32_t base, uint32_t n,
                              const Item *it, GroupWs &w) {
     const uint32_t t0 = tm.t0(), nt = tm.nt();
     for (uint32_t x = t0; x < w.tcap; x += nt) w.tab[x] = 0xFFFF;
     for (uint32_t x = t0; x < n; x += nt) w.cnt[x] = 0;
     tm.sync();
     // 1. representatives: hash + full key compare
+    bool inc = false;
     for (uint32_t i = t0; i < n; i += nt) {
         const Item me = it[i];
+        inc |= !me.complete();
         uint32_t h = item_hash(me) & (w.tcap - 1), r = i;
         while (true) {
             uint32_t cur = w.tab[h];
@@ -581,6 +587,7 @@ __device__ void group_bucket(const DevPlan &p, const Team &tm, uint32_t b, uint3
         atomicAdd(&w.cnt[r], 1u);
     }
     tm.sync();
+    if (tm.any(inc)) return false;
     // 2. members grouped by representative; sorted ascending fold per group
     const uint32_t G = scan_groups(tm, w, n);
     constexpr bool kWarp = std::is_same<Team, WarpTeam>::value;
@@ -676,6 +683,7 @@ __device__ void group_bucket(const DevPlan &p, const Team &tm, uint32_t b, uint3
         p.eids[b] = make_uint2(w.tot[1], w.tot[2]);
     }
     tm.sync();
+    return true;
 }
 
 // Exact fallback for a bucket holding an incomplete key (pathological
@@ -814,14 +822,9 @@ __global__ void __launch_bounds__(kBucketThreads) bucket_kernel(__grid_constant_
             continue;
         }
         const Item *it = items_of(p) + base;
-        bool inc = false;
-        for (uint32_t i = lane; i < n; i += 32) inc |= !it[i].complete();
-        if (__any_sync(0xffffffffu, inc)) {
+        if (!group_bucket(p, WarpTeam{}, (uint32_t)b, base, n, it, w))  // (an incomplete key: exact ranks)
             bucket_exact_warp(p, (uint32_t)b, base, n, meta[bucket_circuit(p, b)].D,
                               reinterpret_cast<uint16_t *>(w.tab));
-            continue;
-        }
-        group_bucket(p, WarpTeam{}, (uint32_t)b, base, n, it, w);
     }
 }
 
