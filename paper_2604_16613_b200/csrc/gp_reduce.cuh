@@ -622,9 +622,14 @@ __device__ bool group_bucket(const DevPlan &p, const Team &tm, uint32_t b, uint3
         const uint32_t lane = t0;
         const uint32_t mine = lane < G ? w.grp[lane] : 0;
         uint32_t rank = 0;
-        if (lane < G) {
-            const Item me = it[mine];
-            for (uint32_t h = 0; h < G; h++) rank += (h != lane && key_cmp(it[w.grp[h]], me) < 0) ? 1u : 0u;
+        Item me{};
+        if (lane < G) me = it[mine];
+        for (uint32_t h = 0; h < G; h++) {  // the others' keys by shuffle (all lanes take part)
+            Item o;
+#pragma unroll
+            for (int x = 0; x < 8; x++) o.k[x] = __shfl_sync(0xffffffffu, me.k[x], h);
+            o.obs = __shfl_sync(0xffffffffu, me.obs, h);
+            rank += (lane < G && h != lane && key_cmp(o, me) < 0) ? 1u : 0u;
         }
         __syncwarp();
         if (lane < G) w.grp[rank] = (uint16_t)mine;
