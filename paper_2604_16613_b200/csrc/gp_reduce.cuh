@@ -355,13 +355,18 @@ __global__ void scatter_kernel(__grid_constant__ const DevPlan p) {
     for_sources(p, [&](uint64_t s, CircCache &cc) {
         const uint32_t n = p.cnt[s];
         if (n == 0 || n > p.K) return;
-        const uint64_t at = (uint64_t)p.boff[p.s_bkt[s]].x + p.s_pos[s];
+        // the slot's loads (bucket -> its offset) are issued first and land
+        // while the item is built from the records
+        const uint32_t bkt = p.s_bkt[s], pos = p.s_pos[s], ndno = p.s_ndno[s];
+        const uint32_t bo = p.boff[bkt].x;
+        cc.at(p, s);
+        const Item it = make_item(p, (uint32_t)s, cc.D, ndno);
+        const uint64_t at = (uint64_t)bo + pos;
         if (at >= p.items_cap) {  // capacity re-run with the learned count
             atomicOr(&p.hdr->items_overflow, 1u);
             return;
         }
-        cc.at(p, s);
-        items_of(p)[at] = make_item(p, (uint32_t)s, cc.D, p.s_ndno[s]);
+        items_of(p)[at] = it;
     });
 }
 
