@@ -407,6 +407,8 @@ repack:  // (again with per-op probabilities when the table overflowed)
     size_t tsmem;
     if (!gp::plan_traversal(t, ctx->device, &tcfg, &tsmem))
         return fail(ctx, GP_ERR_UNSUPPORTED, "circuit too wide for on-chip traversal state (2n words)");
+    if (mode == gp::kModeShard && !tcfg.split)  // (the layer filters live in the split walk / emission)
+        return fail(ctx, GP_ERR_UNSUPPORTED, "fault-range shards need the single-circuit (split) traversal");
     t.groups = 0;
     for (const CircuitMeta &m : M) t.groups += (m.W + tcfg.T - 1) / tcfg.T;
     gp::pack_head(pp, tcfg.T, ctx->h_stage);
