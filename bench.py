@@ -419,7 +419,10 @@ def run_gpu(args, dist):
     if rank == 0 and ws == 1 and not args.no_single:
         line["single_circuit"] = single_circuit_block(compiler, ref_ok=not args.no_cpu_baseline, quick=args.quick)
     if ws > 1 or args.sharded:
-        blk = sharded_single_block(compiler, dist)
+        try:
+            blk = sharded_single_block(compiler, dist)
+        except Exception as e:  # the headline line must still be printed
+            blk = {"error": repr(e)[:300]}
         if rank == 0:
             line["sharded_single"] = blk
     if rank == 0:
