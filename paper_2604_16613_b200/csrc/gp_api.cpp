@@ -170,7 +170,6 @@ size_t carve(gp_ctx *ctx, DevPlan &p, const BatchTotals &t, uint8_t *base, uint3
     p.slab_hdr = (uint4 *)take(slabs * 16);
     p.s_bkt = (uint32_t *)take(S * 4);
     p.s_pos = (uint32_t *)take(S * 4);
-    p.s_ndno = (uint32_t *)take(S * 4);
     p.force_collisions = ctx->force_collisions;
     p.bcount = (uint32_t *)take(NB * 4 + 4);
     p.boff = (uint4 *)take((NB + 1) * 16);

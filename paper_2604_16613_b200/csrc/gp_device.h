@@ -57,7 +57,7 @@ struct DevPlan {
     uint4 *slab_hdr;
     uint32_t slab_stride, slab_words;
     // Reduce (gp_reduce.cuh), per source: bucket, slot in the bucket, id counts.
-    uint32_t *s_bkt, *s_pos, *s_ndno;
+    uint32_t *s_bkt, *s_pos;
     int force_collisions;  // test hook: every sort key equal (exact compare decides)
     // Per bucket (circuit, first detector): sources, slot offsets (scan),
     // groups (edges) and their id counts, output offsets (scan).

@@ -146,8 +146,7 @@ __device__ __forceinline__ uint64_t det_mask(uint32_t t, uint32_t D) {
 
 // Item of a source with at most 4 records, all in registers: records sorted
 // by word with a compare-swap network, detector ids generated in order.
-__device__ __forceinline__ Item make_item_small(const DevPlan &p, uint32_t s, uint32_t n, uint32_t D,
-                                                uint32_t ndno) {
+__device__ __forceinline__ Item make_item_small(const DevPlan &p, uint32_t s, uint32_t n, uint32_t D) {
     uint32_t t[4];
     uint64_t w[4];
 #pragma unroll
@@ -173,7 +172,7 @@ __device__ __forceinline__ Item make_item_small(const DevPlan &p, uint32_t s, ui
     // first is the bucket (q0), the next ones go to 16-bit slots relative to
     // it, four per 64-bit word, most significant first. Observables: a mask.
     uint64_t kw[4] = {0, 0, 0, 0};
-    uint32_t q0 = 0, cnt = 0;
+    uint32_t q0 = 0, cnt = 0, nobs = 0;
     bool fits = true;
     uint64_t obs = 0;
 #pragma unroll
@@ -202,8 +201,10 @@ __device__ __forceinline__ Item make_item_small(const DevPlan &p, uint32_t s, ui
             const uint32_t o = t[j] * 64 + (uint32_t)__ffsll((long long)ob) - 1 - D;
             if (o < 64) obs |= 1ull << o;
             else fits = false;
+            nobs++;
         }
     }
+    const uint32_t ndno = cnt | nobs << 16;  // id counts (the DEM's offsets)
     Item it;
 #pragma unroll
     for (int x = 0; x < 4; x++) {
@@ -217,9 +218,16 @@ __device__ __forceinline__ Item make_item_small(const DevPlan &p, uint32_t s, ui
     return it;
 }
 
-__device__ __forceinline__ Item make_item(const DevPlan &p, uint32_t s, uint32_t D, uint32_t ndno) {
+__device__ __forceinline__ Item make_item(const DevPlan &p, uint32_t s, uint32_t D) {
     const uint32_t nrec = p.cnt[s];
-    if (nrec <= 4) return make_item_small(p, s, nrec, D, ndno);
+    if (nrec <= 4) return make_item_small(p, s, nrec, D);
+    uint32_t nd = 0, no = 0;
+    for (uint32_t x = 0; x < nrec; x++) {
+        const uint64_t b = p.rbits[rec_at(p, s, x)], dm = det_mask(p.rtile[rec_at(p, s, x)], D);
+        nd += __popcll(b & dm);
+        no += __popcll(b & ~dm);
+    }
+    const uint32_t ndno = nd | no << 16;
     Item it;
     SeqIt q;
     q.init(p, s, D);
@@ -298,7 +306,7 @@ __device__ __forceinline__ bool item_less(const DevPlan &p, const Item &a, const
 // ---------------------------------------------------------------- R1 keys
 // Per source with a nonempty signature (empty ones are dropped, dem.cpp:93):
 // bucket (circuit, first detector) with its slot claimed by a counting-sort
-// atomic, and the detector / observable id counts.
+// atomic (the id counts are taken when the sort item is built).
 // Source loops of the reduce: each CTA takes one contiguous chunk of sources
 // (threads stride by blockDim: coalesced), and each thread caches the circuit
 // its sources belong to (a circuit spans thousands of sources).
@@ -331,19 +339,15 @@ __global__ void key_kernel(__grid_constant__ const DevPlan p) {
         const uint32_t n = p.cnt[s];
         if (n == 0 || n > p.K) return;  // n > K: capacity re-run (record_overflow)
         cc.at(p, s);
-        uint32_t first = 0xFFFFFFFFu, nd = 0, no = 0;
+        uint32_t first = 0xFFFFFFFFu;
         for (uint32_t x = 0; x < n; x++) {
             const uint32_t t = p.rtile[rec_at(p, s, x)];
-            const uint64_t bits = p.rbits[rec_at(p, s, x)];
-            const uint64_t dm = det_mask(t, cc.D);
-            nd += __popcll(bits & dm);
-            no += __popcll(bits & ~dm);
-            if (bits & dm) first = min(first, t * 64 + (uint32_t)__ffsll((long long)(bits & dm)) - 1);
+            const uint64_t d = p.rbits[rec_at(p, s, x)] & det_mask(t, cc.D);
+            if (d) first = min(first, t * 64 + (uint32_t)__ffsll((long long)d) - 1);
         }
         const uint32_t bkt = cc.bucket_base + (first == 0xFFFFFFFFu ? 0 : first + 1);
         p.s_bkt[s] = bkt;
         p.s_pos[s] = atomicAdd(&p.bcount[bkt], 1u);
-        p.s_ndno[s] = nd | no << 16;
     });
 }
 
@@ -357,10 +361,10 @@ __global__ void scatter_kernel(__grid_constant__ const DevPlan p) {
         if (n == 0 || n > p.K) return;
         // the slot's loads (bucket -> its offset) are issued first and land
         // while the item is built from the records
-        const uint32_t bkt = p.s_bkt[s], pos = p.s_pos[s], ndno = p.s_ndno[s];
+        const uint32_t bkt = p.s_bkt[s], pos = p.s_pos[s];
         const uint32_t bo = p.boff[bkt].x;
         cc.at(p, s);
-        const Item it = make_item(p, (uint32_t)s, cc.D, ndno);
+        const Item it = make_item(p, (uint32_t)s, cc.D);
         const uint64_t at = (uint64_t)bo + pos;
         if (at >= p.items_cap) {  // capacity re-run with the learned count
             atomicOr(&p.hdr->items_overflow, 1u);
