@@ -339,11 +339,21 @@ __global__ void key_kernel(__grid_constant__ const DevPlan p) {
         const uint32_t n = p.cnt[s];
         if (n == 0 || n > p.K) return;  // n > K: capacity re-run (record_overflow)
         cc.at(p, s);
-        uint32_t first = 0xFFFFFFFFu;
+        // The first detector lies in the lowest word (words above the one
+        // holding detector D - 1 carry observables only; records are
+        // nonzero): the words of every record, the bits of one.
+        uint32_t tmin = 0xFFFFFFFFu, xmin = 0;
         for (uint32_t x = 0; x < n; x++) {
             const uint32_t t = p.rtile[rec_at(p, s, x)];
-            const uint64_t d = p.rbits[rec_at(p, s, x)] & det_mask(t, cc.D);
-            if (d) first = min(first, t * 64 + (uint32_t)__ffsll((long long)d) - 1);
+            if (t < tmin) {
+                tmin = t;
+                xmin = x;
+            }
+        }
+        uint32_t first = 0xFFFFFFFFu;
+        if (tmin * 64 < cc.D) {
+            const uint64_t d = p.rbits[rec_at(p, s, xmin)] & det_mask(tmin, cc.D);
+            if (d) first = tmin * 64 + (uint32_t)__ffsll((long long)d) - 1;
         }
         const uint32_t bkt = cc.bucket_base + (first == 0xFFFFFFFFu ? 0 : first + 1);
         p.s_bkt[s] = bkt;
