@@ -218,9 +218,9 @@ __device__ __forceinline__ Item make_item_small(const DevPlan &p, uint32_t s, ui
     return it;
 }
 
-__device__ __forceinline__ Item make_item(const DevPlan &p, uint32_t s, uint32_t D) {
-    const uint32_t nrec = p.cnt[s];
-    if (nrec <= 4) return make_item_small(p, s, nrec, D);
+// Sources with more than four records (rare): the generic path, out of line
+// so that the hot path keeps its registers.
+__device__ __noinline__ Item make_item_large(const DevPlan &p, uint32_t s, uint32_t D, uint32_t nrec) {
     uint32_t nd = 0, no = 0;
     for (uint32_t x = 0; x < nrec; x++) {
         const uint64_t b = p.rbits[rec_at(p, s, x)], dm = det_mask(p.rtile[rec_at(p, s, x)], D);
@@ -265,6 +265,11 @@ __device__ __forceinline__ Item make_item(const DevPlan &p, uint32_t s, uint32_t
     it.src = s;
     it.ndno = ndno | ((fits && !p.force_collisions) ? 1u << 31 : 0u);
     return it;
+}
+
+__device__ __forceinline__ Item make_item(const DevPlan &p, uint32_t s, uint32_t D) {
+    const uint32_t nrec = p.cnt[s];
+    return nrec <= 4 ? make_item_small(p, s, nrec, D) : make_item_large(p, s, D, nrec);
 }
 
 // Lexicographic compare of two sorted id lists given as masks (a != b): at
