@@ -754,7 +754,7 @@ reduce:
     // counting sort, sort + group + fold each bucket on chip, write in order.
     const uint32_t tpb = 256;
     uint4 *totals = p.bsum + p.bsum_cap - 4;  // scan totals live at the end of bsum
-    const uint32_t sgrid = (uint32_t)std::min<uint64_t>(std::max<uint64_t>(blocks_for(S, tpb), 1), 148 * 16);
+    const uint32_t sgrid = (uint32_t)std::min<uint64_t>(std::max<uint64_t>(blocks_for(S, tpb), 1), 148 * 32);
     red::key_kernel<<<sgrid, tpb, 0, st>>>(p), launches++;
     mark(kProfKey);
     launch_scan(BucketScanF{p.bcount}, NB + 1, p.bsum, p.boff, &totals[0], st, &launches);
