@@ -763,7 +763,7 @@ reduce:
     mark(kProfScatter);
     {
         const uint64_t ctas = (NB + red::kBucketThreads / 32 - 1) / (red::kBucketThreads / 32);
-        red::bucket_kernel<<<(uint32_t)std::min<uint64_t>(std::max<uint64_t>(ctas, 1), 148 * 32),
+        red::bucket_kernel<<<(uint32_t)std::min<uint64_t>(std::max<uint64_t>(ctas, 1), 148 * 256),
                              red::kBucketThreads, 0, st>>>(p);
         smem_optin(red::huge_kernel);
         // (a bucket over kWarpItems sources: at most S / (kWarpItems + 1) of them)
@@ -777,7 +777,7 @@ reduce:
     if (wait_write) cudaStreamWaitEvent(st, wait_write, 0);  // the previous sub-batch's bases
     {
         const uint64_t threads = std::max<uint64_t>(NB * 32, p.tot.C + 1);
-        red::write_kernel<<<(uint32_t)std::min<uint64_t>(blocks_for(threads, tpb), 148 * 32), tpb, 0, st>>>(
+        red::write_kernel<<<(uint32_t)std::min<uint64_t>(blocks_for(threads, tpb), 148 * 128), tpb, 0, st>>>(
             p, &totals[1]);
         launches++;
     }
