@@ -759,7 +759,10 @@ reduce:
     mark(kProfKey);
     launch_scan(BucketScanF{p.bcount}, NB + 1, p.bsum, p.boff, &totals[0], st, &launches);
     mark(kProfScanBucket);
-    red::scatter_kernel<<<sgrid, tpb, 0, st>>>(p), launches++;
+    {  // (512-thread CTAs measure best for the scatter, 128 for the write)
+        const uint32_t g512 = (uint32_t)std::min<uint64_t>(std::max<uint64_t>(blocks_for(S, 512), 1), 148 * 16);
+        red::scatter_kernel<<<g512, 512, 0, st>>>(p), launches++;
+    }
     mark(kProfScatter);
     {
         const uint64_t ctas = (NB + red::kBucketThreads / 32 - 1) / (red::kBucketThreads / 32);
@@ -777,7 +780,7 @@ reduce:
     if (wait_write) cudaStreamWaitEvent(st, wait_write, 0);  // the previous sub-batch's bases
     {
         const uint64_t threads = std::max<uint64_t>(NB * 32, p.tot.C + 1);
-        red::write_kernel<<<(uint32_t)std::min<uint64_t>(blocks_for(threads, tpb), 148 * 128), tpb, 0, st>>>(
+        red::write_kernel<<<(uint32_t)std::min<uint64_t>(blocks_for(threads, 128), 148 * 256), 128, 0, st>>>(
             p, &totals[1]);
         launches++;
     }
