@@ -385,7 +385,20 @@ __global__ void scatter_kernel(__grid_constant__ const DevPlan p) {
             atomicOr(&p.hdr->items_overflow, 1u);
             return;
         }
-        items_of(p)[at] = it;
+        // 16-byte stores where the 56-byte item allows (every other slot is 16-byte aligned)
+        const uint64_t *w = reinterpret_cast<const uint64_t *>(&it);
+        uint64_t *d = reinterpret_cast<uint64_t *>(items_of(p) + at);
+        if ((at & 1) == 0) {
+            reinterpret_cast<ulonglong2 *>(d)[0] = make_ulonglong2(w[0], w[1]);
+            reinterpret_cast<ulonglong2 *>(d)[1] = make_ulonglong2(w[2], w[3]);
+            reinterpret_cast<ulonglong2 *>(d)[2] = make_ulonglong2(w[4], w[5]);
+            d[6] = w[6];
+        } else {
+            d[0] = w[0];
+            reinterpret_cast<ulonglong2 *>(d + 1)[0] = make_ulonglong2(w[1], w[2]);
+            reinterpret_cast<ulonglong2 *>(d + 1)[1] = make_ulonglong2(w[3], w[4]);
+            reinterpret_cast<ulonglong2 *>(d + 1)[2] = make_ulonglong2(w[5], w[6]);
+        }
     });
 }
 
