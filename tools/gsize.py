@@ -1,3 +1,4 @@
+"""Group-size and records-per-source histograms of a BB72 branch circuit (developer tool, GPU)."""
 import sys; sys.path.insert(0,'/root/repo')
 import numpy as np, collections
 import paper_2604_16613_b200 as gp

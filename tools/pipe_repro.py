@@ -1,3 +1,5 @@
+"""Pipelined batch repro (developer tool): usage pipe_repro.py N ROUNDS; GP_PIPE_TRACE=1 prints per
+sub-batch host pack time and device event times."""
 import sys; sys.path.insert(0, '/root/repo')
 import paper_2604_16613_b200 as gp
 n = int(sys.argv[1]); r = int(sys.argv[2])
