@@ -22,6 +22,7 @@ struct TravCfg {
     uint32_t split;      // walk_kernel + emit_kernel (one word per CTA) instead of traverse_kernel
     uint32_t walk_threads, walk_npt;  // walk CTA size; base nodes per node thread (0: generic)
     uint32_t G;          // boundaries per staged group (walk_kernel)
+    uint32_t max_comp;   // sources per noise op at this level (6 / 10 / 15): the layer source map
     uint32_t debug;      // experiments only: bit0 skip emission work, bit1 skip node work
 };
 

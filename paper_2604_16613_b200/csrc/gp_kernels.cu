@@ -583,6 +583,7 @@ bool plan_traversal(const BatchTotals &t, int device, TravCfg *cfg, size_t *smem
     c.max_layer_noise = t.max_layer_noise;
     c.max_layer_meas = t.max_layer_meas;
     c.max_l = t.max_l;
+    c.max_comp = t.level == 0 ? 6 : t.level == 1 ? 10 : 15;
     const uint32_t n2 = 2 * t.max_n;
     c.node_warps = n2 <= 512 ? 4 : n2 <= 2048 ? 8 : 12;
     c.emit_warps = c.node_warps;
@@ -645,7 +646,7 @@ bool plan_traversal(const BatchTotals &t, int device, TravCfg *cfg, size_t *smem
         for (int o = 0; o < nopt; o++) {
             uint32_t R = opts[o][0], N = opts[o][1];
             if (force_r && force_n) R = force_r, N = force_n;
-            const trav::Dims d(T, R, N, t.max_n, t.max_layer_meas, t.max_layer_noise, t.max_l);
+            const trav::Dims d(T, R, N, t.max_n, t.max_layer_meas, t.max_layer_noise, t.max_l, c.max_comp);
             if (d.total_bytes() <= budget) {
                 c.T = T;
                 c.R = R;

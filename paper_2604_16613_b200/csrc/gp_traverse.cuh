@@ -42,9 +42,9 @@ struct StageHdr {  // written by the producer into each stage
 static_assert(sizeof(StageHdr) % 16 == 0, "bulk-copy destinations must stay 16-byte aligned");
 
 struct Dims {
-    uint32_t T, R, NST, n2, ell_w, leaf_w, noise_w, src_w, lay_w;
+    uint32_t T, R, NST, n2, ell_w, leaf_w, noise_w, src_w, lay_w, map_w;
     __host__ __device__ Dims(uint32_t t, uint32_t r, uint32_t nst, uint32_t max_n, uint32_t max_meas,
-                             uint32_t max_noise, uint32_t max_l)
+                             uint32_t max_noise, uint32_t max_l, uint32_t max_comp = 15)
         : T(t),
           R(r),
           NST(nst),
@@ -53,13 +53,14 @@ struct Dims {
           leaf_w((max_meas + 3) & ~1u),
           noise_w((max_noise + 3) & ~1u),
           src_w((max_noise + 9) & ~3u),
-          lay_w((max_l + 4) & ~3u) {}
+          lay_w((max_l + 4) & ~3u),
+          map_w((max_noise * max_comp + 8) & ~7u) {}
     __host__ __device__ size_t ring_bytes() const { return (size_t)R * T * n2 * 8; }
     __host__ __device__ size_t stage_bytes() const {
         return sizeof(StageHdr) + (size_t)ell_w * 4 + ((size_t)T * leaf_w + noise_w) * 8 + (size_t)src_w * 4;
     }
     __host__ __device__ size_t total_bytes() const {
-        return ring_bytes() + NST * stage_bytes() + (2 * NST + 2 * R) * 8 + (size_t)2 * lay_w * 4 + 64;
+        return ring_bytes() + NST * stage_bytes() + (2 * NST + 2 * R) * 8 + (size_t)2 * lay_w * 4 + (size_t)map_w * 2 + 64;
     }
     __device__ uint64_t *slot(uint8_t *base, uint32_t r) const {
         return reinterpret_cast<uint64_t *>(base) + (size_t)r * T * n2;
@@ -81,6 +82,8 @@ struct Dims {
     }
     // Per-layer tables of the CTA's circuit (measurement / noise-op offsets).
     __device__ uint32_t *lay(uint8_t *base) const { return reinterpret_cast<uint32_t *>(bars(base) + 2 * NST + 2 * R); }
+    // layer source -> op (source-major emission)
+    __device__ uint16_t *map(uint8_t *base) const { return reinterpret_cast<uint16_t *>(lay(base) + 2 * lay_w); }
 };
 
 __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
@@ -204,7 +207,7 @@ __global__ void __launch_bounds__(800, 1) traverse_kernel(__grid_constant__ cons
     __shared__ int s_issued_lo;      // lowest boundary the producer staged
     __shared__ uint32_t s_grp;
 
-    const Dims L(cfg.T, cfg.R, cfg.NST, cfg.max_n, cfg.max_layer_meas, cfg.max_layer_noise, cfg.max_l);
+    const Dims L(cfg.T, cfg.R, cfg.NST, cfg.max_n, cfg.max_layer_meas, cfg.max_layer_noise, cfg.max_l, cfg.max_comp);
     const uint32_t tid = threadIdx.x;
     const uint32_t warp = tid >> 5, lane = tid & 31;
     const uint32_t node_threads = cfg.node_warps * 32, emit_threads = cfg.emit_warps * 32;
@@ -425,14 +428,17 @@ __global__ void __launch_bounds__(800, 1) traverse_kernel(__grid_constant__ cons
                 const uint32_t klast = noise_kind(s_noise[nops - 1]);
                 const uint32_t ncl = klast <= 1 ? 1 : klast == 2 ? (level ? 3 : 2) : (level == 0 ? 6 : level == 1 ? 10 : 15);
                 const uint32_t ns = s_src[nops - 1] + ncl - sfirst;
+                uint16_t *smap = L.map(smem);  // layer source -> op, built per boundary
+                for (uint32_t o = te; o < nops; o += emit_threads) {
+                    const uint32_t kd = noise_kind(s_noise[o]);
+                    const uint32_t nc = kd <= 1 ? 1 : kd == 2 ? (level ? 3 : 2) : (level == 0 ? 6 : level == 1 ? 10 : 15);
+                    const uint32_t f = s_src[o] - sfirst;
+                    for (uint32_t c = 0; c < nc; c++) smap[f + c] = (uint16_t)o;
+                }
+                named_sync(kBarEmit, (int)emit_threads);
                 for (uint32_t i = te; i < ns; i += emit_threads) {
                     const uint32_t ls = sfirst + i;
-                    uint32_t lo = 0, hi = nops;
-                    while (hi - lo > 1) {
-                        const uint32_t mid = (lo + hi) >> 1;
-                        if (s_src[mid] <= ls) lo = mid;
-                        else hi = mid;
-                    }
+                    const uint32_t lo = smap[i];
                     const uint64_t wd = s_noise[lo];
                     const uint32_t kind = noise_kind(wd), c = ls - s_src[lo];
                     const uint32_t q0 = noise_q0(wd), q1 = noise_q1(wd);
