@@ -370,7 +370,7 @@ __global__ void key_kernel(__grid_constant__ const DevPlan p) {
 // records, probability, id counts) is written to its bucket slot, so the
 // bucket kernel reads every bucket as one contiguous run -- random gathers
 // (latency) become scattered stores (bandwidth).
-__global__ void scatter_kernel(__grid_constant__ const DevPlan p) {
+__global__ void __launch_bounds__(512, 3) scatter_kernel(__grid_constant__ const DevPlan p) {
     for_sources(p, [&](uint64_t s, CircCache &cc) {
         const uint32_t n = p.cnt[s];
         if (n == 0 || n > p.K) return;
