@@ -35,6 +35,8 @@ sys.path.insert(0, str(ROOT))
 METRIC = "hyperedges/sec and p50 DEM compile latency (ms) at 1/2/4/8 B200 vs CPU ref"
 OPT_PIPELINE = 4  # include/greenpeas.h GP_OPT_PIPELINE
 UNIT = "hyperedges/s"
+WORKLOAD = "bb72_adaptive_branches_r6_L0"
+GOLDEN_BRANCHES = ROOT / "tests" / "golden" / "bb72_branches_r6_L0.npz"
 L2_BYTES = 126 * 2**20
 
 
@@ -165,18 +167,27 @@ def cpu_info():
 
 
 def run_reference(args, dist):
-    """--impl reference: rank 0 times the reference CPU compiler."""
+    """--impl reference: rank 0 times the reference CPU compiler on the GPU
+    arm's per-GPU workload -- the same args.branches branch circuits (ids
+    0..B-1), every step -- on a std::thread pool of all host cores (the
+    demc_main.cpp:184-195 pattern). This process loads oracle/_ref/
+    libdemc_ref.so only: the branch circuits come from the repo's generator
+    source compiled into that library and reach the reference as text through
+    its own parse_circuit (oracle/ref_capi.cpp)."""
     if dist.rank != 0:
         return
-    import paper_2604_16613_b200 as gp  # generators only (host), no GPU use
+    from oracle.bindings import RefLib
+    ref = RefLib()
     threads = os.cpu_count() or 1
-    sample = args.ref_sample
-    texts = [gp.gen_bb72_branch(b).to_text() for b in range(sample)]
+    B = args.branches
+    t0 = time.time()
+    handles = ref.gen_bb72_branches(0, B, threads=threads)
+    gen_s = time.time() - t0
     times, edges = [], 0
     for i in range(args.warmup + args.steps):
-        e, wall = reference_pool(texts, args.level, threads)
+        e, ns = ref.compile_pool(handles, args.level, threads)
         if i >= args.warmup:
-            times.append(wall)
+            times.append(ns / 1e9)
             edges = e
     wall = statistics.mean(times)
     value = edges / wall
@@ -185,55 +196,147 @@ def run_reference(args, dist):
         "metric": METRIC, "value": value, "unit": UNIT, "impl": "reference", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": wall * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "u64+f64", "data": "synthetic",
-        "config": {"workload": "bb72_adaptive_branches_r6_L0", "branches_per_step": sample, "level": args.level,
-                   "note": "bounded sample of the GPU arm's workload (same generator, branch ids 0..sample-1)"},
+        "config": {"workload": WORKLOAD, "branches_per_gpu": B, "level": args.level,
+                   "hyperedges_per_step": int(edges), "generate_s": round(gen_s, 2),
+                   "note": "each step compiles the GPU arm's per-GPU branch set (ids 0..B-1) in full"},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
-                         "sample": f"{sample} BB72 r6 branch circuits per step, std::thread pool of {threads}",
-                         "cpu": model},
+                         "sample": f"all {B} BB72 r6 branch circuits per step, reference compile_circuit "
+                                   f"on a std::thread pool of {threads}", "cpu": model},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     emit_line(line)
 
 
-def single_circuit_block(compiler, ref_ok: bool, quick: bool):
-    """N=1 extras: p50 compile latency of single circuits (SURVEY 8d configs
-    1-4) through gp_compile (host circuit -> flat DEM in pinned memory), with
-    the reference CPU compiler's p50 on the same circuit."""
+def shim_lib():
+    """libgp_shimbench.so: timing harness of the C++ drop-in endpoint
+    (demc::compile_circuit -> owning demc::Dem, csrc/gp_shimbench.cpp)."""
+    import ctypes as C
+
+    from paper_2604_16613_b200 import _native as N
+    L = C.CDLL(str(N.LIB_PATH.parent / "libgp_shimbench.so"))
+    L.sb_time_shim.argtypes = [C.POINTER(N.CircuitView), C.c_int, C.c_uint32, C.c_uint32, C.POINTER(C.c_uint64)]
+    L.sb_time_shim.restype = C.c_int64
+    L.sb_shim_pool.argtypes = [C.POINTER(N.CircuitView), C.c_uint32, C.c_int, C.c_uint32, C.c_uint32,
+                               C.POINTER(C.c_uint64)]
+    L.sb_shim_pool.restype = C.c_int64
+    return L
+
+
+def pct(ts, q):
+    ts = sorted(ts)
+    return float(ts[min(len(ts) - 1, int(len(ts) * q))])
+
+
+def single_circuit_block(compiler, ref_ok: bool, quick: bool, gpu_iters: int, ref_iters: int):
+    """N=1 extras (SURVEY 8d timing protocol): p50 compile latency of the
+    single-circuit configs 1-4 at both GPU endpoints -- the flat pinned DEM
+    (gp_compile) and the owning demc::Dem of the reference signature (the C++
+    shim) -- over >= 1,000 compiles each after warm-up, with the reference
+    CPU compiler's p50 (1 thread, >= 20 compiles after 1 warm-up,
+    demc_main.cpp:126) on the same circuit."""
+    import ctypes as C
+
     import paper_2604_16613_b200 as gp
     cases = [("surface_d3_r3_paper", lambda: gp.gen_surface(3, 3, 1e-3), (0, 2)),
              ("surface_d11_r11_si1000", lambda: gp.gen_surface(11, 11, 1e-3, gp.NOISE_MODEL_SI1000), (0, 2)),
-             ("bb144_r12_uniform", lambda: gp.gen_bb144(12, 1e-3), (0, 2)),
+             ("bb144_r12_uniform_depth8", lambda: gp.gen_bb144(12, 1e-3), (0, 2)),
              ("surface_d25_r25_paper", lambda: gp.gen_surface(25, 25, 1e-3), (0,))]
     out = {}
     ref = None
     if ref_ok:
         from oracle.bindings import RefLib
         ref = RefLib()
+    shim = shim_lib()
     for name, make, levels in cases:
         g = make()
         text = g.to_text() if ref else None
+        view = g.view()[0]
         for lv in levels:
-            iters = 30 if "d25" in name else 200
-            for _ in range(5):
+            for _ in range(20):
                 dem = compiler.compile(g, lv)
             ts, ks = [], []
-            for _ in range(iters):
+            for _ in range(gpu_iters):
                 dem = compiler.compile(g, lv)
                 ts.append(compiler.last_stats["total_ns"])
                 ks.append(compiler.last_stats["kernel_ns"])
-            ts.sort()
-            p50 = ts[len(ts) // 2] / 1e6
-            entry = {"edges": dem.num_edges, "p50_ms": p50, "p99_ms": ts[int(len(ts) * 0.99) - 1] / 1e6,
-                     "kernel_p50_ms": sorted(ks)[len(ks) // 2] / 1e6, "hyperedges_per_s": dem.num_edges / (p50 / 1e3)}
+            p50 = pct(ts, 0.5) / 1e6
+            sns = (C.c_uint64 * gpu_iters)()
+            se = shim.sb_time_shim(C.byref(view), lv, 20, gpu_iters, sns)
+            s50 = pct(list(sns), 0.5) / 1e6
+            entry = {"edges": dem.num_edges, "iters": gpu_iters, "p50_ms": p50, "p99_ms": pct(ts, 0.99) / 1e6,
+                     "kernel_p50_ms": pct(ks, 0.5) / 1e6, "hyperedges_per_s": dem.num_edges / (p50 / 1e3),
+                     "dem_endpoint_p50_ms": s50, "dem_endpoint_p99_ms": pct(list(sns), 0.99) / 1e6,
+                     "dem_endpoint_ok": int(se) == dem.num_edges}
             if ref is not None and not (quick and "d25" in name):
-                riters = 1 if "d25" in name else (5 if "bb144" in name or "d11" in name else 20)
-                e, ns = ref.parse(text).time_compile(lv, riters)
-                rp50 = float(sorted(ns)[len(ns) // 2]) / 1e6
-                entry["ref_p50_ms"] = rp50
-                entry["ref_hyperedges_per_s"] = e / (rp50 / 1e3)
-                entry["speedup_p50"] = rp50 / p50
+                e, ns = ref.parse(text).time_compile(lv, ref_iters)
+                rp50 = pct(list(ns), 0.5) / 1e6
+                entry.update({"ref_iters": ref_iters, "ref_p50_ms": rp50, "ref_hyperedges_per_s": e / (rp50 / 1e3),
+                              "speedup_p50": rp50 / p50, "speedup_p50_dem_endpoint": rp50 / s50})
             out[f"{name}_L{lv}"] = entry
     return out
+
+
+def link_bandwidths(device: int) -> dict:
+    """Measured ceilings of the end-to-end path (GB/s): pinned H2D and D2H
+    copies (256 MiB, best of 5, CUDA events) and host memory copy bandwidth
+    (torch CPU copy on all threads, best of 3)."""
+    import torch
+    n = 256 << 20
+    h = torch.empty(n, dtype=torch.uint8, pin_memory=True)
+    d = torch.empty(n, dtype=torch.uint8, device=f"cuda:{device}")
+    h.fill_(1)
+    out = {}
+    for name, dst, src in (("h2d_gbs", d, h), ("d2h_gbs", h, d)):
+        best = 0.0
+        for _ in range(5):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            dst.copy_(src, non_blocking=True)
+            b.record()
+            b.synchronize()
+            best = max(best, n / (a.elapsed_time(b) * 1e6))
+        out[name] = best
+    x = torch.empty(1 << 30, dtype=torch.uint8)
+    y = torch.empty_like(x)
+    x.fill_(3)
+    best = 0.0
+    for _ in range(3):
+        t = time.perf_counter()
+        y.copy_(x)
+        best = max(best, 2 * x.numel() / ((time.perf_counter() - t) * 1e9))
+    out["host_copy_gbs"] = best
+    out["host_threads"] = torch.get_num_threads()
+    del h, d, x, y
+    return out
+
+
+def branch_parity(compiler, out, first: int, count: int, dist) -> dict:
+    """Every branch DEM of `out` against the reference's digests
+    (tests/golden/bb72_branches_r6_L0.npz: reference hyperedge count and
+    gp_dem_digest of its demc::Dem, per branch id); summed over ranks."""
+    import numpy as np
+    z = np.load(GOLDEN_BRANCHES)
+    got = compiler.batch_digests(out)
+    eoff = np.ctypeslib.as_array(out.edge_offsets, shape=(count + 1,))
+    checked = mism = 0
+    if first + count <= len(z["digests"]):
+        bad = (got != z["digests"][first:first + count]) | (np.diff(eoff) != z["edges"][first:first + count])
+        checked, mism = count, int(np.count_nonzero(bad))
+    return {"branches": int(dist.sum(checked)), "mismatches": int(dist.sum(mism)),
+            "distinct_dems": int(dist.sum(len(np.unique(got)))),
+            "how": "per-branch gp_dem_digest (ids + fp64 bits) == the reference's digest of its own demc::Dem"}
+
+
+def circuit_bytes(views) -> int:
+    """Bytes of the host circuit arrays the packer reads (gp_circuit_view)."""
+    total = 0
+    for v in views:
+        G = v.gate_offsets[v.num_layers]
+        Nn = v.noise_offsets[v.num_layers]
+        total += 21 * G + 17 * Nn + 8 * (v.num_layers + 1)
+        total += 4 * (v.num_detectors + 1 + v.det_offsets[v.num_detectors])
+        total += 4 * (v.num_observables + 1 + v.obs_offsets[v.num_observables])
+    return total
 
 
 def sharded_single_block(compiler, dist, reps: int = 10):
@@ -297,6 +400,8 @@ def run_gpu(args, dist):
     compiler.set_option(OPT_PIPELINE, 0)
     for _ in range(args.warmup):
         out, stats = compiler.compile_batch_raw(views, args.level)
+    first = shard(rank, ws, B).start
+    parity_value_path = branch_parity(compiler, out, first, B, dist) if args.level == 0 else None
     edges = int(out.num_edges)
     h2d = int(stats["h2d_bytes"])
     d2h = int(stats["d2h_bytes"])
@@ -336,6 +441,9 @@ def run_gpu(args, dist):
     clk = clocks.stop()
     e2e_s = dist.max(t1 - t0)
     e2e_value = total_edges * args.steps / e2e_s
+    # parity of the last e2e step's DEMs (the pipelined public-API output)
+    parity = branch_parity(compiler, out, first, B, dist) if args.level == 0 else None
+    e2e_h2d, e2e_d2h = int(stats["h2d_bytes"]), int(stats["d2h_bytes"])
 
     # --- optional final gather of per-rank DEM tables over NCCL -------------
     gather = None
@@ -395,13 +503,18 @@ def run_gpu(args, dist):
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "u64+f64", "data": "synthetic",
-        "config": {"workload": "bb72_adaptive_branches_r6_L0", "branches_per_gpu": B, "total_branches": B * ws,
+        "config": {"workload": WORKLOAD, "branches_per_gpu": B, "total_branches": B * ws,
+                   "code": "BB [[72,12,6]], Bravyi et al. depth-8 syndrome cycle (7 CX layers; X prep/measure "
+                           "as R/MR + H), paper noise NoiseModel{1e-3}, 6 rounds, checks of non-full rounds "
+                           "kept with probability 1/2 (mt19937_64 seed_seq{1,0,b,0})",
                    "level": args.level, "hyperedges_per_step": int(total_edges),
                    "parallelism": f"branch-sharded x{ws}, no collective",
                    "l2": "inputs larger than L2" if not flush else "L2 flushed between timed iterations",
                    "input_image_bytes_per_gpu": image_bytes, "generate_s": round(gen_s, 2)},
-        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": e2e_h2d, "d2h_bytes_per_step": e2e_d2h,
                 "ms_per_step": e2e_s / args.steps * 1e3, "breakdown": e2e_parts},
+        "parity": parity,
+        "parity_value_path": parity_value_path,
         "gpu_launches": launches_per_step * args.steps,
         "gather": gather,
         "roofline": roofline,
@@ -416,8 +529,33 @@ def run_gpu(args, dist):
         line["cpu_baseline"] = {"value": e / wall, "unit": UNIT, "cores": threads, "kind": "reference",
                                 "sample": f"{len(texts)} of the {B} branch circuits, reference compile_circuit "
                                           f"on a {threads}-thread pool ({wall:.2f} s wall)", "cpu": model}
+    # e2e roof: what the host <-> device path allows per step, from measured
+    # link and host-memory bandwidths (pipelined: the stages overlap, so the
+    # floor is the slowest of them)
+    bw = link_bandwidths(device)
+    in_bytes = circuit_bytes(views)
+    roof = {"h2d_ms": e2e_h2d / (bw["h2d_gbs"] * 1e6), "d2h_ms": e2e_d2h / (bw["d2h_gbs"] * 1e6),
+            "host_ms": (in_bytes + e2e_h2d + e2e_d2h) / (bw["host_copy_gbs"] * 1e6), "device_ms": ms_per_step,
+            "input_circuit_bytes": in_bytes, **bw}
+    roof["bound_ms"] = max(roof["h2d_ms"], roof["d2h_ms"], roof["host_ms"], roof["device_ms"])
+    roof["e2e_ms"] = e2e_s / args.steps * 1e3
+    roof["frac"] = roof["bound_ms"] / roof["e2e_ms"]
+    roof["how"] = ("host_ms = (circuit arrays read + staging image written + DEM written to pinned memory) / "
+                   "host copy bandwidth; h2d/d2h = bytes / pinned-copy bandwidth; device_ms = value's ms/step")
+    line["e2e"]["roof"] = roof
     if rank == 0 and ws == 1 and not args.no_single:
-        line["single_circuit"] = single_circuit_block(compiler, ref_ok=not args.no_cpu_baseline, quick=args.quick)
+        line["single_circuit"] = single_circuit_block(compiler, ref_ok=not args.no_cpu_baseline, quick=args.quick,
+                                                      gpu_iters=args.gpu_iters, ref_iters=args.ref_iters)
+    if rank == 0 and ws == 1 and not args.no_shim_pool:
+        import ctypes as C
+        wall = C.c_uint64()
+        thr = os.cpu_count() or 1
+        e = shim_lib().sb_shim_pool(views, B, args.level, thr, 3, C.byref(wall))
+        line["dem_endpoint_pool"] = {
+            "value": e / (wall.value / 1e9) if e > 0 else None, "unit": UNIT, "threads": thr, "circuits": B,
+            "ms_per_pass": wall.value / 1e6,
+            "how": "demc_main.cpp:184-195 pattern over the C++ drop-in: host threads, atomic counter, one "
+                   "demc::compile_circuit(c, L0, 1) per branch (one GPU context per thread, shared packing pool)"}
     if ws > 1 or args.sharded:
         try:
             blk = sharded_single_block(compiler, dist)
@@ -456,11 +594,13 @@ def main():
     ap.add_argument("--branches", type=int, default=4096, help="branch circuits per GPU")
     ap.add_argument("--level", type=int, default=0)
     ap.add_argument("--cpu-sample", type=int, default=1024)
-    ap.add_argument("--ref-sample", type=int, default=512)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-single", action="store_true")
     ap.add_argument("--sharded", action="store_true", help="also at N=1: fault-range sharded d25 block (over NCCL)")
     ap.add_argument("--quick", action="store_true")
+    ap.add_argument("--gpu-iters", type=int, default=1000, help="single-circuit GPU compiles per case")
+    ap.add_argument("--ref-iters", type=int, default=20, help="single-circuit reference compiles per case")
+    ap.add_argument("--no-shim-pool", action="store_true")
     ap.add_argument("--ncu-traffic", type=float, default=None)
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)

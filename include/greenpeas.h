@@ -214,6 +214,18 @@ gp_status gp_circuit_metrics(const gp_circuit_view *circuit, uint8_t level, gp_m
  * Returns a malloc'd NUL-terminated string; release with gp_free. */
 char *gp_serialize_dem(const gp_dem_view *dem, size_t *len);
 
+/* 64-bit digest of a DEM for bulk parity checks (host, no device work):
+ *   h = 0x6a09e667f3bcc909; absorb(D << 32 | O); absorb(E); per edge in order:
+ *   absorb(#dets << 32 | #obs), absorb(each detector id), absorb(each
+ *   observable id), absorb(probability bits); absorb(h, w) = splitmix64
+ *   finaliser of (h + w + 0x9e3779b97f4a7c15).
+ * Equal digests <=> identical serialize_dem text (dem.cpp:144-157) up to hash
+ * collisions: ids exact, fp64 bits exact. The reference-side restatement over
+ * demc::Dem is oracle/ref_capi.cpp dem_digest. gp_dem_batch_digest writes one
+ * digest per circuit of a batch view (out[num_circuits]), on host threads. */
+uint64_t gp_dem_digest(const gp_dem_view *dem);
+void gp_dem_batch_digest(const gp_dem_batch_view *batch, uint64_t *out);
+
 /* Pinned host allocation helpers (for zero-staging circuit uploads). */
 void *gp_host_alloc(size_t bytes);
 void gp_host_free(void *p);

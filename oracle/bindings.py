@@ -52,6 +52,14 @@ class RefLib:
         L.ref_time_compile.restype = C.c_int64
         L.ref_compile_pool.argtypes = [C.POINTER(vp), C.c_uint32, C.c_int, C.c_uint32, C.POINTER(C.c_uint64)]
         L.ref_compile_pool.restype = C.c_int64
+        L.ref_gen_bb72_branches.argtypes = [C.c_uint64, C.c_uint32, C.c_uint32, C.c_double, C.c_double,
+                                            C.c_uint64, C.c_uint32, C.POINTER(vp)]
+        L.ref_gen_bb72_branches.restype = C.c_int
+        L.ref_compile_digests.argtypes = [C.POINTER(vp), C.c_uint32, C.c_int, C.c_uint32, C.POINTER(C.c_uint64),
+                                          C.POINTER(C.c_uint64)]
+        L.ref_compile_digests.restype = C.c_int
+        L.ref_dem_text_digest.argtypes = [C.c_char_p, C.c_uint32, C.c_uint32]
+        L.ref_dem_text_digest.restype = C.c_uint64
         L.ref_sample_fired.argtypes = [vp, C.c_uint64, C.c_uint32]
         L.ref_sample_fired.restype = C.c_int64
         self.L = L
@@ -82,6 +90,36 @@ class RefLib:
         if not h:
             raise ValueError(self.L.ref_last_error().decode())
         return RefCircuit(self, h), self._str(txt.value, n)
+
+    def gen_bb72_branches(self, first: int, count: int, rounds: int = 6, p: float = 1e-3,
+                          check_prob: float = 0.5, seed: int = 1, threads: int = 0) -> list["RefCircuit"]:
+        """Branch circuits b = first .. first + count - 1 as
+        reference circuits: the repo's generator source compiled into this
+        library, handed over as text to the reference's parse_circuit."""
+        import os
+        arr = (C.c_void_p * max(count, 1))()
+        rc = self.L.ref_gen_bb72_branches(first, count, rounds, p, check_prob, seed, threads or os.cpu_count() or 1,
+                                          arr)
+        if rc:
+            raise ValueError("branch generation failed")
+        return [RefCircuit(self, arr[i]) for i in range(count)]
+
+    def compile_digests(self, circuits, level: int, threads: int = 0):
+        """Per circuit (hyperedges, DEM digest) of the reference compile_circuit."""
+        import os
+        n = len(circuits)
+        arr = (C.c_void_p * max(n, 1))(*[c.h for c in circuits])
+        e = np.zeros(max(n, 1), np.uint64)
+        d = np.zeros(max(n, 1), np.uint64)
+        rc = self.L.ref_compile_digests(arr, n, level, threads or os.cpu_count() or 1,
+                                        e.ctypes.data_as(C.POINTER(C.c_uint64)),
+                                        d.ctypes.data_as(C.POINTER(C.c_uint64)))
+        if rc:
+            raise ValueError("reference compile failed")
+        return e[:n], d[:n]
+
+    def dem_text_digest(self, text: str, num_detectors: int, num_observables: int) -> int:
+        return int(self.L.ref_dem_text_digest(text.encode(), num_detectors, num_observables))
 
     def compile_pool(self, circuits, level: int, threads: int):
         arr = (C.c_void_p * len(circuits))(*[c.h for c in circuits])

@@ -11,6 +11,13 @@
 //   gen_surface / gen_repetition  codes.cpp:149-333
 //   run_adaptive_shot    adaptive.cpp:382-391
 // Nothing in the product path (paper_2604_16613_b200/) links or loads this.
+//
+// Workload circuits the reference has no generator for (BB / SI1000 /
+// adaptive branches) come from this repo's host generator
+// source (paper_2604_16613_b200/csrc/gp_gen.cpp), compiled INTO this library
+// with hidden visibility by oracle/Makefile, and reach the reference only as
+// circuit text through its own parse_circuit -- so the --impl reference arm of
+// bench.py loads nothing but this library.
 
 #include <algorithm>
 #include <atomic>
@@ -27,6 +34,7 @@
 #include "demc/codes.hpp"
 #include "demc/compile.hpp"
 #include "demc/frame.hpp"
+#include "greenpeas.h"
 
 namespace {
 
@@ -38,6 +46,46 @@ char *dup_string(const std::string &s, size_t *len) {
     out[s.size()] = 0;
     if (len) *len = s.size();
     return out;
+}
+
+// DEM digest: the same 64-bit hash as gp_dem_digest (include/greenpeas.h),
+// restated over the reference's own demc::Dem. Equal digests <=> identical
+// serialize_dem text (ids exact, probability bits exact; shortest round-trip
+// formatting is injective on doubles).
+uint64_t dg_mix(uint64_t h, uint64_t w) {
+    uint64_t x = h + w + 0x9e3779b97f4a7c15ull;
+    x ^= x >> 30;
+    x *= 0xbf58476d1ce4e5b9ull;
+    x ^= x >> 27;
+    x *= 0x94d049bb133111ebull;
+    x ^= x >> 31;
+    return x;
+}
+
+uint64_t dem_digest(const demc::Dem &d) {
+    uint64_t h = 0x6a09e667f3bcc909ull;
+    h = dg_mix(h, (uint64_t)d.num_detectors << 32 | d.num_observables);
+    h = dg_mix(h, d.hyperedges.size());
+    for (const demc::Hyperedge &e : d.hyperedges) {
+        h = dg_mix(h, (uint64_t)e.detectors.size() << 32 | e.observables.size());
+        for (uint32_t x : e.detectors) h = dg_mix(h, x);
+        for (uint32_t x : e.observables) h = dg_mix(h, x);
+        uint64_t bits;
+        std::memcpy(&bits, &e.probability, 8);
+        h = dg_mix(h, bits);
+    }
+    return h;
+}
+
+template <class F>
+void parallel_for(uint32_t count, uint32_t threads, F &&f) {
+    std::atomic<uint32_t> next{0};
+    std::vector<std::thread> pool;
+    for (uint32_t t = 0; t < std::max<uint32_t>(1, threads); t++)
+        pool.emplace_back([&] {
+            for (uint32_t s = next++; s < count; s = next++) f(s);
+        });
+    for (auto &th : pool) th.join();
 }
 
 }  // namespace
@@ -186,6 +234,57 @@ int64_t ref_compile_pool(void **handles, uint32_t count, int level, uint32_t thr
     if (wall_ns)
         *wall_ns = (uint64_t)std::chrono::duration_cast<std::chrono::nanoseconds>(t1 - t0).count();
     return failed ? -1 : total.load();
+}
+
+// BB [[72,12,6]] adaptive branch circuits as
+// reference circuits: branch first + i -> handles[i], generated by the repo's
+// host generator (gp_gen_bb, hidden in this library) and parsed from text by
+// the reference's parse_circuit on `threads` workers. 0 on success.
+int ref_gen_bb72_branches(uint64_t first, uint32_t count, uint32_t rounds, double p, double check_prob,
+                          uint64_t seed, uint32_t threads, void **handles) {
+    static const uint32_t a[3] = {3, 1, 2}, b[3] = {3, 1, 2};
+    std::atomic<bool> failed{false};
+    parallel_for(count, threads, [&](uint32_t i) {
+        handles[i] = nullptr;
+        gp_circuit *g = gp_gen_bb(6, 6, a, b, rounds, p, GP_NOISE_MODEL_PAPER, check_prob,
+                                  std::max<uint32_t>(1, rounds / 2), seed, first + i);
+        if (!g) {
+            failed = true;
+            return;
+        }
+        size_t n = 0;
+        char *text = gp_circuit_serialize(g, &n);
+        gp_circuit_free(g);
+        try {
+            handles[i] = new demc::Circuit(demc::parse_circuit(std::string(text, n)));
+        } catch (...) {
+            failed = true;
+        }
+        std::free(text);
+    });
+    return failed ? -1 : 0;
+}
+
+// compile_circuit(c, level, 1) of every handle on `threads` workers (not
+// timed): per circuit, hyperedge count and DEM digest (dem_digest above).
+int ref_compile_digests(void **handles, uint32_t count, int level, uint32_t threads, uint64_t *edges,
+                        uint64_t *digests) {
+    std::atomic<bool> failed{false};
+    parallel_for(count, threads, [&](uint32_t s) {
+        try {
+            demc::Dem d = demc::compile_circuit(*(demc::Circuit *)handles[s], (demc::CorrelationLevel)level, 1);
+            edges[s] = d.hyperedges.size();
+            digests[s] = dem_digest(d);
+        } catch (...) {
+            failed = true;
+        }
+    });
+    return failed ? -1 : 0;
+}
+
+// Digest of a DEM given as text (parse_dem, dem.cpp:158-197).
+uint64_t ref_dem_text_digest(const char *text, uint32_t num_detectors, uint32_t num_observables) {
+    return dem_digest(demc::parse_dem(text, num_detectors, num_observables));
 }
 
 // Noiseless-soundness probe (frame.cpp:241-248, collapse randomisation on):

@@ -100,6 +100,9 @@ def lib() -> C.CDLL:
         L.gp_circuit_metrics.argtypes = [C.POINTER(CircuitView), C.c_uint8, C.POINTER(Metrics)]
         L.gp_serialize_dem.argtypes = [C.POINTER(DemView), C.POINTER(C.c_size_t)]
         L.gp_serialize_dem.restype = vp
+        L.gp_dem_digest.argtypes = [C.POINTER(DemView)]
+        L.gp_dem_digest.restype = C.c_uint64
+        L.gp_dem_batch_digest.argtypes = [C.POINTER(DemBatchView), _u64p]
         L.gp_free.argtypes = [vp]
         L.gp_host_alloc.argtypes = [C.c_size_t]
         L.gp_host_alloc.restype = vp

@@ -69,6 +69,11 @@ class Dem:
                       N.ptr(arrs[3], N._u32p), N.ptr(arrs[4], N._f64p))
         return v, arrs
 
+    def digest(self) -> int:
+        """gp_dem_digest: 64-bit hash of ids and probability bits (equal <=> same text)."""
+        v, keep = self.view()
+        return int(N.lib().gp_dem_digest(C.byref(v)))
+
     def to_text(self) -> str:
         """serialize_dem (dem.cpp:144-157), formatted natively with std::to_chars."""
         v, keep = self.view()
@@ -269,6 +274,13 @@ class Compiler:
                                                C.byref(st)))
         self.last_stats = st.as_dict()
         return out, self.last_stats
+
+    @staticmethod
+    def batch_digests(out) -> np.ndarray:
+        """Per-circuit gp_dem_digest of a DemBatchView (host threads)."""
+        d = np.zeros(max(int(out.num_circuits), 1), np.uint64)
+        N.lib().gp_dem_batch_digest(C.byref(out), N.ptr(d, N._u64p))
+        return d[:int(out.num_circuits)]
 
     def compile_batch(self, circuits, level=CorrelationLevel.L0) -> list[Dem]:
         keep = []

@@ -10,6 +10,8 @@
 
 #include <algorithm>
 #include <atomic>
+#include <memory>
+#include <mutex>
 #include <thread>
 #include <charconv>
 #include <chrono>
@@ -62,7 +64,6 @@ struct gp_ctx {
     gp::StageEvents stage_ev{};
 
     gp::PackPlan pack;
-    std::unique_ptr<gp::HostPool> pool;  // created on the first large job
     std::vector<uint32_t> out_ndet, out_nobs;
 
     // Last successful device plan (for gp_replay) and profiling state.
@@ -81,6 +82,7 @@ struct gp_ctx {
     // graph (repeated compiles of one circuit shape: the JIT case).
     struct {
         uint64_t key = 0, pending = 0;
+        gp::DevPlan plan{};  // the plan the graph was captured from (a key hit must match it byte for byte)
         cudaGraphExec_t exec = nullptr;
         int launches = 0;
         bool used = false;  // the last compile ran as the graph (no per-stage events)
@@ -97,6 +99,36 @@ uint64_t ns_since(clk::time_point t0) {
 }
 
 uint64_t align16(uint64_t x) { return (x + 15) & ~15ull; }
+
+// One host worker pool per process, shared by every context. A compile leases
+// it for its packing when it is free; when another context holds it (many
+// host threads compiling at once, the demc_main.cpp:184-195 pattern) the
+// caller packs on its own thread instead -- the callers already are the
+// parallelism, and no context ever starts a pool of its own.
+std::mutex g_pool_mu;
+
+gp::HostPool *shared_pool() {
+    static std::once_flag once;
+    static std::unique_ptr<gp::HostPool> pool;
+    std::call_once(once, [] {
+        pool = std::make_unique<gp::HostPool>(std::max(1u, std::thread::hardware_concurrency()) - 1);
+    });
+    return pool.get();
+}
+
+struct PoolLease {
+    gp::HostPool *pool = nullptr;
+    explicit PoolLease(bool want) {
+        if (want && g_pool_mu.try_lock()) pool = shared_pool();
+    }
+    ~PoolLease() { release(); }
+    void release() {
+        if (pool) g_pool_mu.unlock();
+        pool = nullptr;
+    }
+    PoolLease(const PoolLease &) = delete;
+    PoolLease &operator=(const PoolLease &) = delete;
+};
 
 gp_status fail(gp_ctx *ctx, gp_status st, const std::string &msg) {
     ctx->err = msg;
@@ -275,7 +307,7 @@ int launch_pipeline(gp_ctx *ctx, const DevPlan &p, cudaError_t *e) {
     auto &g = ctx->graph;
     const uint64_t key = p.dbg ? 0 : plan_key(p);
     g.used = false;
-    if (key && g.exec && g.key == key) {
+    if (key && g.exec && g.key == key && std::memcmp(&g.plan, &p, sizeof(DevPlan)) == 0) {
         *e = cudaGraphLaunch(g.exec, ctx->stream);
         cudaEventRecord(ctx->stage_ev.reduced, ctx->stream);  // stage events are not recorded inside the graph
         g.used = true;
@@ -314,6 +346,7 @@ int launch_pipeline(gp_ctx *ctx, const DevPlan &p, cudaError_t *e) {
         return 0;
     }
     g.key = key;
+    g.plan = p;
     g.launches = n;
     *e = cudaGraphLaunch(g.exec, ctx->stream);
     cudaEventRecord(ctx->stage_ev.reduced, ctx->stream);
@@ -343,9 +376,8 @@ gp_status run_batch(gp_ctx *ctx, const gp_circuit_view *cs, size_t count, uint8_
     for (size_t c = 0; c < count; c++)
         ops += (uint64_t)(cs[c].gate_offsets[cs[c].num_layers] - cs[c].gate_offsets[0]) +
                (cs[c].noise_offsets[cs[c].num_layers] - cs[c].noise_offsets[0]);
-    if (!ctx->pool && ops >= (1u << 14))
-        ctx->pool = std::make_unique<gp::HostPool>(std::max(1u, std::thread::hardware_concurrency()) - 1);
-    gp::HostPool *hpool = ops >= (1u << 14) ? ctx->pool.get() : nullptr;
+    PoolLease lease(ops >= (1u << 14));
+    gp::HostPool *hpool = lease.pool;
     pp.force_wide = false;
 repack:  // (again with per-op probabilities when the table overflowed)
     gp::pack_plan(hpool, cs, count, level, pp);
@@ -419,6 +451,7 @@ repack:  // (again with per-op probabilities when the table overflowed)
         slice(0, 1, 0, L.lay_gate);  // meta + cumulative tables (the image's head)
         slice(L.prob_table, 8, 0, t.prob_table_n);
     }
+    lease.release();  // packing done: the pool is free for other contexts
     const uint64_t pack_ns = ns_since(t0);
     if (e != cudaSuccess) return cuda_fail(ctx, e, "upload");
     cudaEventRecord(ctx->ev_h2d, ctx->stream);
@@ -501,7 +534,9 @@ repack:  // (again with per-op probabilities when the table overflowed)
         if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
         if (e != cudaSuccess) return cuda_fail(ctx, e, "device pipeline");
         hdr = p.out_mapped ? *p.hmap.hdr : *ctx->h_hdr;
-        if (attempt > 4) return fail(ctx, GP_ERR_CUDA, "capacity retry loop did not converge");
+        const bool retry = hdr.items_overflow || hdr.pool_overflow || hdr.record_overflow ||
+                           hdr.num_det_ids == 0xFFFFFFFFu;
+        if (retry && attempt >= 5) return fail(ctx, GP_ERR_CUDA, "capacity retry loop did not converge");
         if (hdr.items_overflow) {  // more nonempty signatures than items: use every source
             items_cap = t.sources + 16;
             ctx->items_hint = items_cap;
@@ -806,7 +841,8 @@ gp_status run_batch_pipelined(gp_ctx *ctx, const gp_circuit_view *cs, size_t cou
     hm.ids_cap = ids_cap;
     hm.c_cap = c_cap;
 
-    gp::HostPool *hpool = ctx->pool.get();
+    const PoolLease lease(true);
+    gp::HostPool *hpool = lease.pool;
     uint64_t h2d_bytes = 0, sources = 0;
     int launches = 0;
     auto drain = [&] {
@@ -1307,8 +1343,8 @@ gp_status gp_merge_partials(gp_ctx *ctx, const gp_partial_view *parts, size_t np
             return fail(ctx, GP_ERR_INVALID_ARGUMENT,
                         "malformed partial table: " + std::to_string(hdr.bad_input) +
                             " entries without records, wider than 16 words or outside the circuit");
-        if (attempt > 4) return fail(ctx, GP_ERR_CUDA, "capacity retry loop did not converge");
         if (hdr.num_det_ids == 0xFFFFFFFFu) {  // id capacity overflow
+            if (attempt >= 5) return fail(ctx, GP_ERR_CUDA, "capacity retry loop did not converge");
             ids_cap *= 4;
             ctx->ids_hint = ids_cap;
             continue;
@@ -1478,6 +1514,63 @@ char *gp_serialize_dem(const gp_dem_view *d, size_t *len) {
     out[s.size()] = 0;
     if (len) *len = s.size();
     return out;
+}
+
+}  // extern "C"
+
+namespace {
+
+uint64_t dg_mix(uint64_t h, uint64_t w) {
+    uint64_t x = h + w + 0x9e3779b97f4a7c15ull;
+    x ^= x >> 30;
+    x *= 0xbf58476d1ce4e5b9ull;
+    x ^= x >> 27;
+    x *= 0x94d049bb133111ebull;
+    x ^= x >> 31;
+    return x;
+}
+
+// Digest of edges [e0, e1) of flat DEM arrays (gp_dem_digest's definition).
+uint64_t digest_range(uint32_t D, uint32_t O, uint64_t e0, uint64_t e1, const uint64_t *doff, const uint32_t *dids,
+                      const uint64_t *ooff, const uint32_t *oids, const double *probs) {
+    uint64_t h = 0x6a09e667f3bcc909ull;
+    h = dg_mix(h, (uint64_t)D << 32 | O);
+    h = dg_mix(h, e1 - e0);
+    for (uint64_t e = e0; e < e1; e++) {
+        h = dg_mix(h, (doff[e + 1] - doff[e]) << 32 | (ooff[e + 1] - ooff[e]));
+        for (uint64_t k = doff[e]; k < doff[e + 1]; k++) h = dg_mix(h, dids[k]);
+        for (uint64_t k = ooff[e]; k < ooff[e + 1]; k++) h = dg_mix(h, oids[k]);
+        uint64_t bits;
+        std::memcpy(&bits, &probs[e], 8);
+        h = dg_mix(h, bits);
+    }
+    return h;
+}
+
+}  // namespace
+
+extern "C" {
+
+uint64_t gp_dem_digest(const gp_dem_view *d) {
+    return digest_range(d->num_detectors, d->num_observables, 0, d->num_edges, d->det_offsets, d->det_ids,
+                        d->obs_offsets, d->obs_ids, d->probs);
+}
+
+void gp_dem_batch_digest(const gp_dem_batch_view *b, uint64_t *out) {
+    const size_t n = b->num_circuits;
+    const unsigned nt = (unsigned)std::min<size_t>(std::max(1u, std::thread::hardware_concurrency()), (n + 63) / 64);
+    std::atomic<size_t> next{0};
+    auto work = [&] {
+        for (size_t c; (c = next.fetch_add(16)) < n;)
+            for (size_t i = c; i < std::min(n, c + 16); i++)
+                out[i] = digest_range(b->num_detectors[i], b->num_observables[i], b->edge_offsets[i],
+                                      b->edge_offsets[i + 1], b->det_offsets, b->det_ids, b->obs_offsets,
+                                      b->obs_ids, b->probs);
+    };
+    std::vector<std::thread> pool;
+    for (unsigned t = 1; t < nt; t++) pool.emplace_back(work);
+    work();
+    for (auto &t : pool) t.join();
 }
 
 void *gp_host_alloc(size_t bytes) {

@@ -333,43 +333,54 @@ gp_circuit *make_bb(uint32_t L, uint32_t Mm, const uint32_t a[3], const uint32_t
                 ex[k] = unif(rng) < check_prob;
                 ez[k] = unif(rng) < check_prob;
             }
-        for (uint32_t k = 0; k < lm; k++)
-            if (ex[k]) bld.h(nd + k);
-        bld.apply_noise(mdl, n);
-        bld.tick();
-        // 9 CX layers: Z checks over L (B^T), then Z over R (A^T) together with
-        // X over L (A), then X over R (B). Every X/Z pair meets Z-first on all
-        // shared data qubits, so the interleaving measures commuting checks.
-        for (int s = 0; s < 9; s++) {
-            if (s < 6) {
-                const int t = s % 3;
+        // The depth-8 syndrome cycle of Bravyi et al. (Nature 627, 778 (2024),
+        // Fig. 7): seven CX layers in which X and Z checks interleave, each
+        // check touching its six data qubits in the direction order sX / sZ
+        // (direction d < 3: the L-data neighbour through A_d (X) or B_d^T (Z);
+        // d >= 3: the R-data neighbour through B_{d-3} (X) or A_{d-3}^T (Z)).
+        // Its PrepX / MeasX steps are R/MR + H in this gate set, so a round is
+        //   t0  H(X anc)            | Z: CX dir sZ[0]
+        //   t1..t5  X: CX dir sX[t] | Z: CX dir sZ[t]
+        //   t6  X: CX dir sX[6]     | Z: MR (measure + re-prepare)
+        //   t7  H(X anc)
+        //   t8  MR(X anc)
+        static constexpr int kSX[7] = {-1, 1, 4, 3, 5, 0, 2};
+        static constexpr int kSZ[7] = {3, 5, 0, 1, 2, 4, -1};
+        auto xdata = [&](int d, uint32_t k) { return d < 3 ? fwd(A[d], k) : lm + fwd(B[d - 3], k); };
+        auto zdata = [&](int d, uint32_t k) { return d < 3 ? inv(B[d], k) : lm + inv(A[d - 3], k); };
+        std::vector<uint32_t> mx(lm), mz(lm);
+        for (int t = 0; t < 7; t++) {
+            if (t == 0) {
                 for (uint32_t k = 0; k < lm; k++)
-                    if (ez[k]) bld.cx(s < 3 ? inv(B[t], k) : lm + inv(A[t], k), nd + lm + k);
+                    if (ex[k]) bld.h(nd + k);
+            } else {
+                for (uint32_t k = 0; k < lm; k++)
+                    if (ex[k]) bld.cx(nd + k, xdata(kSX[t], k));
             }
-            if (s >= 3) {
-                const int t = (s - 3) % 3;
+            if (t < 6) {
                 for (uint32_t k = 0; k < lm; k++)
-                    if (ex[k]) bld.cx(nd + k, s < 6 ? fwd(A[t], k) : lm + fwd(B[t], k));
+                    if (ez[k]) bld.cx(zdata(kSZ[t], k), nd + lm + k);
+            } else {
+                for (uint32_t k = 0; k < lm; k++)
+                    if (ez[k]) mz[k] = bld.mr(nd + lm + k);
             }
             bld.apply_noise(mdl, n);
-            bld.tick();
+            if (t < 6) bld.tick();
         }
-        for (uint32_t k = 0; k < lm; k++)
-            if (ex[k]) bld.h(nd + k);
-        bld.apply_noise(mdl, n);
-        bld.tick();
-        std::vector<uint32_t> mx(lm), mz(lm);
-        for (uint32_t k = 0; k < lm; k++)
-            if (ez[k]) mz[k] = bld.mr(nd + lm + k);
-        for (uint32_t k = 0; k < lm; k++)
-            if (ex[k]) mx[k] = bld.mr(nd + k);
-        bld.apply_noise(mdl, n);
         for (uint32_t k = 0; k < lm; k++)
             if (ez[k]) {
                 if (last_z[k] < 0) bld.detector({mz[k]});
                 else bld.detector({(uint32_t)last_z[k], mz[k]});
                 last_z[k] = mz[k];
             }
+        bld.tick();
+        for (uint32_t k = 0; k < lm; k++)
+            if (ex[k]) bld.h(nd + k);
+        bld.apply_noise(mdl, n);
+        bld.tick();
+        for (uint32_t k = 0; k < lm; k++)
+            if (ex[k]) mx[k] = bld.mr(nd + k);
+        bld.apply_noise(mdl, n);
         for (uint32_t k = 0; k < lm; k++)
             if (ex[k]) {
                 if (last_x[k] >= 0) bld.detector({(uint32_t)last_x[k], mx[k]});

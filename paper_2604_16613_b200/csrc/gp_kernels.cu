@@ -463,7 +463,8 @@ __global__ void partial_kernel(__grid_constant__ const DevPlan p) {
 // Merge mode: the concatenated partial tables -> per-source counts,
 // probabilities and slot-major records (the emit stage's layout), one thread
 // per source. Malformed entries (no records, more than K, ids outside the
-// circuit) are dropped and counted in hdr->bad_input.
+// circuit -- words beyond W or bits beyond D + O in the last word -- or a
+// word repeated within an entry) are dropped and counted in hdr->bad_input.
 __global__ void unpack_kernel(__grid_constant__ const DevPlan p) {
     const uint64_t S = p.tot.sources;
     const uint64_t s = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -481,9 +482,15 @@ __global__ void unpack_kernel(__grid_constant__ const DevPlan p) {
     const uint32_t i = (uint32_t)s - d.x;
     const uint32_t base = p.p_roff[d.y], r0 = p.p_roff[d.y + i] - base, r1 = p.p_roff[d.y + i + 1] - base;
     const uint32_t W = (uint32_t)p.tot.tiles;
+    const uint32_t nb = p.tot.dets + p.tot.obss;  // valid bits: ids < D + O
+    const uint64_t last_mask = (nb & 63) ? (1ull << (nb & 63)) - 1 : ~0ull;
     bool ok = r1 > r0 && r1 - r0 <= p.K && r1 <= d.w;
-    for (uint32_t j = 0; ok && j < r1 - r0; j++)
-        ok = p.p_word[d.z + r0 + j] < W && p.p_bits[d.z + r0 + j] != 0;
+    for (uint32_t j = 0; ok && j < r1 - r0; j++) {
+        const uint32_t wd = p.p_word[d.z + r0 + j];
+        const uint64_t bits = p.p_bits[d.z + r0 + j];
+        ok = wd < W && bits != 0 && (wd + 1 < W || (bits & ~last_mask) == 0);
+        for (uint32_t i = 0; ok && i < j; i++) ok = p.p_word[d.z + r0 + i] != wd;  // one record per word
+    }
     if (!ok) {
         p.cnt[s] = 0;
         atomicAdd(&p.hdr->bad_input, 1u);
@@ -646,8 +653,12 @@ bool plan_traversal(const BatchTotals &t, int device, TravCfg *cfg, size_t *smem
         for (int o = 0; o < nopt; o++) {
             uint32_t R = opts[o][0], N = opts[o][1];
             if (force_r && force_n) R = force_r, N = force_n;
-            const trav::Dims d(T, R, N, t.max_n, t.max_layer_meas, t.max_layer_noise, t.max_l, c.max_comp);
+            // the layer source -> op map is used only by source-major emission
+            // (several words per CTA, every word of the circuit: TM > 1 && direct)
+            const uint32_t comp = (T > 1 && t.max_W <= T) ? c.max_comp : 0;
+            const trav::Dims d(T, R, N, t.max_n, t.max_layer_meas, t.max_layer_noise, t.max_l, comp);
             if (d.total_bytes() <= budget) {
+                c.max_comp = comp;
                 c.T = T;
                 c.R = R;
                 c.NST = N;

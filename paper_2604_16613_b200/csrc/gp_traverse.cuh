@@ -422,8 +422,10 @@ __global__ void __launch_bounds__(800, 1) traverse_kernel(__grid_constant__ cons
             if (TM > 1 && direct && nops) {
                 // Source-major: consecutive lanes take consecutive sources of
                 // the layer (an op's components are consecutive sources), so
-                // the signature stores of a warp are coalesced. Lane -> op by a
-                // binary search over the ops' first-source offsets.
+                // the signature stores of a warp are coalesced. Lane -> op
+                // through a per-boundary source -> op map in shared memory,
+                // built by the emit warps and ordered by the emit barrier
+                // before it is read (and after the previous boundary's reads).
                 const uint32_t sfirst = s_src[0];
                 const uint32_t klast = noise_kind(s_noise[nops - 1]);
                 const uint32_t ncl = klast <= 1 ? 1 : klast == 2 ? (level ? 3 : 2) : (level == 0 ? 6 : level == 1 ? 10 : 15);

@@ -13,6 +13,14 @@ is run and its serialize_dem text is recorded:
 * BASELINE.json configs at full size: sha256 + hyperedge count in
   tests/golden/full_size.json, so the GPU path can be checked byte-for-byte
   at the sizes it is benchmarked on without shipping megabytes of text.
+* the headline workload (config 5): every BB [[72,12,6]] r6 L0 branch
+  circuit b = 0 .. 8 * 4096 - 1 (what bench.py compiles at N = 1..8), its
+  hyperedge count and DEM digest (gp_dem_digest's definition, restated over
+  the reference's demc::Dem in oracle/ref_capi.cpp) in
+  tests/golden/bb72_branches_r6_L0.npz; plus a sha256 over the circuit text
+  of branches 0..255 to tell generator drift from compiler drift.
+
+    python tests/golden/make_goldens.py [small] [full] [branches]
 """
 
 from __future__ import annotations
@@ -21,6 +29,8 @@ import hashlib
 import json
 import sys
 import time
+
+import numpy as np
 from pathlib import Path
 
 ROOT = Path(__file__).resolve().parents[2]
@@ -54,8 +64,35 @@ def sha(s: str) -> str:
     return hashlib.sha256(s.encode()).hexdigest()
 
 
+BRANCH_TOTAL = 8 * 4096
+
+
+def make_branch_goldens(ref) -> None:
+    t0 = time.time()
+    edges, digests = [], []
+    chunk = 2048
+    for first in range(0, BRANCH_TOTAL, chunk):
+        hs = ref.gen_bb72_branches(first, chunk)
+        e, d = ref.compile_digests(hs, 0)
+        edges.append(e.astype(np.uint32))
+        digests.append(d)
+        print("branches", first + chunk, f"{time.time() - t0:.0f}s", flush=True)
+    h = hashlib.sha256()
+    for c in ref.gen_bb72_branches(0, 256):
+        h.update(c.text().encode())
+    np.savez_compressed(OUT / "bb72_branches_r6_L0.npz", edges=np.concatenate(edges),
+                        digests=np.concatenate(digests),
+                        circuits_0_255_sha256=np.frombuffer(bytes.fromhex(h.hexdigest()), np.uint8),
+                        seed=np.uint64(1), rounds=np.uint32(6), level=np.uint32(0))
+
+
 def main() -> None:
+    parts = set(sys.argv[1:]) or {"small", "full", "branches"}
     ref = RefLib()
+    if "branches" in parts:
+        make_branch_goldens(ref)
+    if "small" not in parts and "full" not in parts:
+        return
     gen_dir = OUT / "generated"
     gen_dir.mkdir(exist_ok=True)
     for name, make in SMALL.items():
