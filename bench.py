@@ -383,6 +383,8 @@ def sharded_single_block(compiler, dist, reps: int = 10):
 
 
 def run_gpu(args, dist):
+    import numpy as np
+
     import paper_2604_16613_b200 as gp
 
     ws, rank = dist.ws, dist.rank
@@ -450,7 +452,7 @@ def run_gpu(args, dist):
     if ws > 1:
         from paper_2604_16613_b200 import _native as N
         E_ = int(out.num_edges)
-        doff_ = N.copy_u64(out.det_offsets, E_ + 1)
+        doff_ = N.copy_u32(out.det_offsets, E_ + 1)
         arrays = {"edge_offsets": N.copy_u64(out.edge_offsets, len(circuits) + 1), "det_offsets": doff_,
                   "det_ids": N.copy_u32(out.det_ids, int(doff_[-1])), "probs": N.copy_f64(out.probs, E_)}
         dist.barrier()
@@ -465,8 +467,8 @@ def run_gpu(args, dist):
     from paper_2604_16613_b200 import _native as N
     E = int(out.num_edges)
     eoff = N.copy_u64(out.edge_offsets, len(circuits) + 1)
-    doff = N.copy_u64(out.det_offsets, E + 1)
-    ooff = N.copy_u64(out.obs_offsets, E + 1)
+    doff = N.copy_u32(out.det_offsets, E + 1).astype(np.int64)
+    ooff = N.copy_u32(out.obs_offsets, E + 1).astype(np.int64)
     ab = {"traverse": 0, "reduce": 0, "total": 0}
     for i, c in enumerate(circuits):  # B_alg is per circuit; sum over the batch
         e0, e1 = int(eoff[i]), int(eoff[i + 1])

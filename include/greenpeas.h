@@ -75,15 +75,17 @@ typedef struct gp_circuit_view {
 
 /* Flat view of demc::Dem (dem.hpp:38-52): hyperedges in the reference's
  * canonical order (dem.cpp:122-127), ids strictly ascending within an edge.
+ * Offsets are 32-bit (a compile or batch holds < 2^32 ids; larger batches
+ * fail with GP_ERR_UNSUPPORTED -- split them).
  * Memory is owned by the context (pinned host) and valid until the next
  * compile call on that context. */
 typedef struct gp_dem_view {
     uint32_t num_detectors;
     uint32_t num_observables;
     uint64_t num_edges;
-    const uint64_t *det_offsets; /* [num_edges + 1] */
+    const uint32_t *det_offsets; /* [num_edges + 1] */
     const uint32_t *det_ids;
-    const uint64_t *obs_offsets; /* [num_edges + 1] */
+    const uint32_t *obs_offsets; /* [num_edges + 1] */
     const uint32_t *obs_ids;
     const double *probs; /* [num_edges] */
 } gp_dem_view;
@@ -96,9 +98,9 @@ typedef struct gp_dem_batch_view {
     const uint32_t *num_detectors;   /* [num_circuits] */
     const uint32_t *num_observables; /* [num_circuits] */
     uint64_t num_edges;
-    const uint64_t *det_offsets; /* [num_edges + 1], global */
+    const uint32_t *det_offsets; /* [num_edges + 1], global */
     const uint32_t *det_ids;
-    const uint64_t *obs_offsets; /* [num_edges + 1], global */
+    const uint32_t *obs_offsets; /* [num_edges + 1], global */
     const uint32_t *obs_ids;
     const double *probs;
 } gp_dem_batch_view;

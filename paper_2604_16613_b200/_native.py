@@ -36,7 +36,7 @@ class CircuitView(C.Structure):
 class DemView(C.Structure):
     _fields_ = [
         ("num_detectors", C.c_uint32), ("num_observables", C.c_uint32), ("num_edges", C.c_uint64),
-        ("det_offsets", _u64p), ("det_ids", _u32p), ("obs_offsets", _u64p), ("obs_ids", _u32p),
+        ("det_offsets", _u32p), ("det_ids", _u32p), ("obs_offsets", _u32p), ("obs_ids", _u32p),
         ("probs", _f64p),
     ]
 
@@ -45,7 +45,7 @@ class DemBatchView(C.Structure):
     _fields_ = [
         ("num_circuits", C.c_uint64), ("edge_offsets", _u64p), ("num_detectors", _u32p),
         ("num_observables", _u32p), ("num_edges", C.c_uint64),
-        ("det_offsets", _u64p), ("det_ids", _u32p), ("obs_offsets", _u64p), ("obs_ids", _u32p),
+        ("det_offsets", _u32p), ("det_ids", _u32p), ("obs_offsets", _u32p), ("obs_ids", _u32p),
         ("probs", _f64p),
     ]
 

@@ -60,12 +60,12 @@ class Dem:
                 for e in range(self.num_edges)]
 
     def view(self):
-        arrs = (np.ascontiguousarray(self.det_offsets, np.uint64), np.ascontiguousarray(self.det_ids, np.uint32),
-                np.ascontiguousarray(self.obs_offsets, np.uint64), np.ascontiguousarray(self.obs_ids, np.uint32),
+        arrs = (np.ascontiguousarray(self.det_offsets, np.uint32), np.ascontiguousarray(self.det_ids, np.uint32),
+                np.ascontiguousarray(self.obs_offsets, np.uint32), np.ascontiguousarray(self.obs_ids, np.uint32),
                 np.ascontiguousarray(self.probs, np.float64))
         arrs = tuple(a if a.size else np.zeros(1, a.dtype) for a in arrs)
         v = N.DemView(self.num_detectors, self.num_observables, self.num_edges,
-                      N.ptr(arrs[0], N._u64p), N.ptr(arrs[1], N._u32p), N.ptr(arrs[2], N._u64p),
+                      N.ptr(arrs[0], N._u32p), N.ptr(arrs[1], N._u32p), N.ptr(arrs[2], N._u32p),
                       N.ptr(arrs[3], N._u32p), N.ptr(arrs[4], N._f64p))
         return v, arrs
 
@@ -149,15 +149,20 @@ class DevicePartialTable:
         return v, ts
 
 
-def _dem_from_view(v, lo: int, hi: int, nd: int, no: int) -> Dem:
+def _dem_slice(v, doff: np.ndarray, ooff: np.ndarray, lo: int, hi: int, nd: int, no: int) -> Dem:
+    """Edges [lo, hi) of a flat DEM view (offset arrays already copied)."""
     E = hi - lo
-    doff = N.copy_u64(v.det_offsets, v.num_edges + 1) if v.num_edges else np.zeros(1, np.uint64)
-    ooff = N.copy_u64(v.obs_offsets, v.num_edges + 1) if v.num_edges else np.zeros(1, np.uint64)
     d0, d1, o0, o1 = int(doff[lo]), int(doff[hi]), int(ooff[lo]), int(ooff[hi])
     dids = np.ctypeslib.as_array(v.det_ids, shape=(d1,))[d0:d1].copy() if d1 > d0 else np.zeros(0, np.uint32)
     oids = np.ctypeslib.as_array(v.obs_ids, shape=(o1,))[o0:o1].copy() if o1 > o0 else np.zeros(0, np.uint32)
     probs = np.ctypeslib.as_array(v.probs, shape=(hi,))[lo:hi].copy() if E else np.zeros(0, np.float64)
-    return Dem(nd, no, doff[lo:hi + 1] - d0, dids, ooff[lo:hi + 1] - o0, oids, probs)
+    return Dem(nd, no, doff[lo:hi + 1] - np.uint32(d0), dids, ooff[lo:hi + 1] - np.uint32(o0), oids, probs)
+
+
+def _dem_from_view(v, lo: int, hi: int, nd: int, no: int) -> Dem:
+    doff = N.copy_u32(v.det_offsets, v.num_edges + 1) if v.num_edges else np.zeros(1, np.uint32)
+    ooff = N.copy_u32(v.obs_offsets, v.num_edges + 1) if v.num_edges else np.zeros(1, np.uint32)
+    return _dem_slice(v, doff, ooff, lo, hi, nd, no)
 
 
 class Compiler:
@@ -291,10 +296,11 @@ class Compiler:
             keep.append(k)
         out, _ = self.compile_batch_raw(arr, level)
         eo = N.copy_u64(out.edge_offsets, len(circuits) + 1)
-        flat = N.DemView(0, 0, out.num_edges, out.det_offsets, out.det_ids, out.obs_offsets, out.obs_ids,
-                         out.probs)
-        return [_dem_from_view(flat, int(eo[i]), int(eo[i + 1]), int(out.num_detectors[i]),
-                               int(out.num_observables[i])) for i in range(len(circuits))]
+        E = int(out.num_edges)
+        doff = N.copy_u32(out.det_offsets, E + 1) if E else np.zeros(1, np.uint32)
+        ooff = N.copy_u32(out.obs_offsets, E + 1) if E else np.zeros(1, np.uint32)
+        return [_dem_slice(out, doff, ooff, int(eo[i]), int(eo[i + 1]), int(out.num_detectors[i]),
+                           int(out.num_observables[i])) for i in range(len(circuits))]
 
 
 _tls = threading.local()

@@ -131,14 +131,14 @@ Dem compile_circuit(const Circuit &c, CorrelationLevel level, uint32_t threads, 
 
 std::string serialize_dem(const Dem &d) {
     // Flatten and reuse the C-ABI formatter (dem.cpp:144-157 semantics).
-    std::vector<uint64_t> doff{0}, ooff{0};
+    std::vector<uint32_t> doff{0}, ooff{0};
     std::vector<uint32_t> dids, oids;
     std::vector<double> probs;
     for (const Hyperedge &h : d.hyperedges) {
         dids.insert(dids.end(), h.detectors.begin(), h.detectors.end());
         oids.insert(oids.end(), h.observables.begin(), h.observables.end());
-        doff.push_back(dids.size());
-        ooff.push_back(oids.size());
+        doff.push_back((uint32_t)dids.size());
+        ooff.push_back((uint32_t)oids.size());
         probs.push_back(h.probability);
     }
     gp_dem_view v{d.num_detectors, d.num_observables, d.hyperedges.size(), doff.data(), dids.data(),

@@ -166,8 +166,8 @@ size_t carve_out(DevPlan &p, uint8_t *base, uint64_t e_cap, uint64_t ids_cap, ui
         return base ? base + at : nullptr;
     };
     p.e_cap = e_cap;
-    p.o_det_off = (uint64_t *)take(e_cap * 8 + 8);
-    p.o_obs_off = (uint64_t *)take(e_cap * 8 + 8);
+    p.o_det_off = (uint32_t *)take(e_cap * 4 + 4);
+    p.o_obs_off = (uint32_t *)take(e_cap * 4 + 4);
     p.o_prob = (double *)take(e_cap * 8);
     p.o_det = (uint32_t *)take(ids_cap * 4);
     p.o_obs = (uint32_t *)take(ids_cap * 4);
@@ -190,6 +190,7 @@ size_t carve(gp_ctx *ctx, DevPlan &p, const BatchTotals &t, uint8_t *base, uint3
     p.leaf = (uint64_t *)take(t.leaf * 8);
     p.prob = (double *)take(S * 8);
     p.nsrc = (uint32_t *)take(t.noise * 4 + 16);
+    p.noise_w = t.narrow ? (uint64_t *)take(t.noise * 8) : nullptr;  // widened by lower_kernel
     p.cnt = (uint32_t *)take(S * 4 + 4);
     p.rbits = (uint64_t *)take(S * K * 8);
     p.rtile = (uint32_t *)take(S * K * 4);
@@ -210,7 +211,6 @@ size_t carve(gp_ctx *ctx, DevPlan &p, const BatchTotals &t, uint8_t *base, uint3
     p.ecount = (uint32_t *)take(NB * 4);
     p.eids = (uint2 *)take(NB * 8);
     p.oscan = (uint4 *)take((NB + 1) * 16);
-    p.e_src = (uint32_t *)take(items_cap * 4);
     p.e_ndno = (uint32_t *)take(items_cap * 4);
     p.e_item = (uint32_t *)take(items_cap * 4);
     p.e_prob = (double *)take(items_cap * 8);
@@ -289,7 +289,8 @@ float elapsed_ms(cudaEvent_t a, cudaEvent_t b) {
 }
 
 struct HostOut {
-    uint64_t *det_off, *obs_off, *edge_off;
+    uint32_t *det_off, *obs_off;
+    uint64_t *edge_off;
     double *probs;
     uint32_t *det_ids, *obs_ids;
 };
@@ -379,6 +380,7 @@ gp_status run_batch(gp_ctx *ctx, const gp_circuit_view *cs, size_t count, uint8_
     PoolLease lease(ops >= (1u << 14));
     gp::HostPool *hpool = lease.pool;
     pp.force_wide = false;
+    pp.no_narrow = false;
 repack:  // (again with per-op probabilities when the table overflowed)
     gp::pack_plan(hpool, cs, count, level, pp);
     if (pp.err == gp::kPackIndexSpace || pp.err == gp::kPackTooWide) {
@@ -414,8 +416,8 @@ repack:  // (again with per-op probabilities when the table overflowed)
         const BatchTotals &tt = pp.t;
         slice(L.lay_gate, 4, a.layer_base, last ? tt.layer_slots : b->layer_base);
         slice(L.lay_noise, 4, a.layer_base, last ? tt.layer_slots : b->layer_base);
-        slice(L.gates, 8, a.gate_base, last ? tt.gates : b->gate_base);
-        slice(L.noise, 8, a.noise_base, last ? tt.noise : b->noise_base);
+        slice(L.gates, tt.narrow ? 4 : 8, a.gate_base, last ? tt.gates : b->gate_base);
+        slice(L.noise, tt.narrow ? 4 : 8, a.noise_base, last ? tt.noise : b->noise_base);
         if (tt.wide_prob) slice(L.noise_prob, 8, a.noise_base, last ? tt.noise : b->noise_base);
         slice(L.meas_flip, 8, a.meas_base, last ? tt.meas : b->meas_base);
         slice(L.det_off, 4, a.det_base, last ? tt.det_slots : b->det_base);
@@ -424,9 +426,10 @@ repack:  // (again with per-op probabilities when the table overflowed)
         slice(L.obs_meas, 4, a.obs_entry_base, last ? tt.obs_entries : b->obs_entry_base);
     }
     if (pp.err) return fail_pack(ctx, pp.err);
-    if (pp.need_wide.load() && !pp.force_wide) {
+    if ((pp.need_wide.load() && !pp.force_wide) || (pp.need_wide_words.load() && !pp.no_narrow)) {
         cudaStreamSynchronize(ctx->stream);  // chunk uploads read the staging image
-        pp.force_wide = true;
+        if (pp.need_wide.load()) pp.force_wide = true;
+        pp.no_narrow = true;
         goto repack;
     }
     gp::pack_finish(pp, ctx->h_stage);
@@ -496,8 +499,8 @@ repack:  // (again with per-op probabilities when the table overflowed)
                 mo = (size_t)align16(mo + bytes);
                 return at;
             };
-            const size_t m_hdr = mtake(sizeof(DeviceHeader)), m_det_off = mtake((p.e_cap + 1) * 8),
-                         m_obs_off = mtake((p.e_cap + 1) * 8), m_prob = mtake(p.e_cap * 8),
+            const size_t m_hdr = mtake(sizeof(DeviceHeader)), m_det_off = mtake((p.e_cap + 1) * 4),
+                         m_obs_off = mtake((p.e_cap + 1) * 4), m_prob = mtake(p.e_cap * 8),
                          m_det = mtake(p.ids_cap * 4), m_obs = mtake(p.ids_cap * 4), m_edge = mtake((t.C + 1) * 8);
             p.out_mapped = mode == gp::kModeFull && mo <= (size_t(128) << 20);
             if (p.out_mapped && ctx->h_map_cap < mo) {
@@ -513,8 +516,8 @@ repack:  // (again with per-op probabilities when the table overflowed)
             }
             if (p.out_mapped) {
                 p.hmap.hdr = (DeviceHeader *)(ctx->h_map + m_hdr);
-                p.hmap.det_off = (uint64_t *)(ctx->h_map + m_det_off);
-                p.hmap.obs_off = (uint64_t *)(ctx->h_map + m_obs_off);
+                p.hmap.det_off = (uint32_t *)(ctx->h_map + m_det_off);
+                p.hmap.obs_off = (uint32_t *)(ctx->h_map + m_obs_off);
                 p.hmap.probs = (double *)(ctx->h_map + m_prob);
                 p.hmap.det_ids = (uint32_t *)(ctx->h_map + m_det);
                 p.hmap.obs_ids = (uint32_t *)(ctx->h_map + m_obs);
@@ -645,7 +648,7 @@ repack:  // (again with per-op probabilities when the table overflowed)
             stats->d2h_ns = (uint64_t)(out_ms * 1e6);
             stats->num_sources = t.sources;
             stats->h2d_bytes = pp.image_bytes();
-            stats->d2h_bytes = sizeof(DeviceHeader) + (E + 1) * 16 + E * 8 + (nd + no) * 4 + (count + 1) * 8;
+            stats->d2h_bytes = sizeof(DeviceHeader) + (E + 1) * 8 + E * 8 + (nd + no) * 4 + (count + 1) * 8;
             stats->kernel_launches = (uint64_t)launches;
             stats->total_ns = ns_since(t0);
         }
@@ -657,15 +660,15 @@ repack:  // (again with per-op probabilities when the table overflowed)
         o = (size_t)align16(o + bytes);
         return at;
     };
-    const size_t o_det_off = take((E + 1) * 8), o_obs_off = take((E + 1) * 8), o_prob = take(E * 8),
+    const size_t o_det_off = take((E + 1) * 4), o_obs_off = take((E + 1) * 4), o_prob = take(E * 8),
                  o_det = take(nd * 4), o_obs = take(no * 4), o_edge = take((count + 1) * 8);
     if ((st = ensure_host(ctx, &ctx->h_out, &ctx->h_out_cap, o)) != GP_OK) return st;
     auto d2h = [&](size_t off, const void *src, size_t bytes) {
         if (bytes && e == cudaSuccess)
             e = cudaMemcpyAsync(ctx->h_out + off, src, bytes, cudaMemcpyDeviceToHost, ctx->stream);
     };
-    d2h(o_det_off, p.o_det_off, (E + 1) * 8);
-    d2h(o_obs_off, p.o_obs_off, (E + 1) * 8);
+    d2h(o_det_off, p.o_det_off, (E + 1) * 4);
+    d2h(o_obs_off, p.o_obs_off, (E + 1) * 4);
     d2h(o_prob, p.o_prob, E * 8);
     d2h(o_det, p.o_det, nd * 4);
     d2h(o_obs, p.o_obs, no * 4);
@@ -673,8 +676,8 @@ repack:  // (again with per-op probabilities when the table overflowed)
     cudaEventRecord(ctx->ev_end, ctx->stream);
     if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
     if (e != cudaSuccess) return cuda_fail(ctx, e, "download");
-    ho.det_off = (uint64_t *)(ctx->h_out + o_det_off);
-    ho.obs_off = (uint64_t *)(ctx->h_out + o_obs_off);
+    ho.det_off = (uint32_t *)(ctx->h_out + o_det_off);
+    ho.obs_off = (uint32_t *)(ctx->h_out + o_obs_off);
     ho.probs = (double *)(ctx->h_out + o_prob);
     ho.det_ids = (uint32_t *)(ctx->h_out + o_det);
     ho.obs_ids = (uint32_t *)(ctx->h_out + o_obs);
@@ -808,7 +811,7 @@ gp_status run_batch_pipelined(gp_ctx *ctx, const gp_circuit_view *cs, size_t cou
         o = (size_t)align16(o + bytes);
         return at;
     };
-    const size_t o_det_off = take(e_cap * 8), o_obs_off = take(e_cap * 8), o_prob = take(e_cap * 8),
+    const size_t o_det_off = take(e_cap * 4), o_obs_off = take(e_cap * 4), o_prob = take(e_cap * 8),
                  o_det = take(ids_cap * 4), o_obs = take(ids_cap * 4), o_edge = take(c_cap * 8);
     if (ps.h_map_cap < o) {
         if (ps.h_map) cudaFreeHost(ps.h_map);
@@ -826,13 +829,14 @@ gp_status run_batch_pipelined(gp_ctx *ctx, const gp_circuit_view *cs, size_t cou
     std::fill(bases, bases + 4, 0);
     *status = 0;
     struct {
-        uint64_t *det_off, *obs_off, *edge_off;
+        uint32_t *det_off, *obs_off;
+        uint64_t *edge_off;
         double *probs;
         uint32_t *det_ids, *obs_ids;
         uint64_t e_cap, ids_cap, c_cap;
     } hm{};
-    hm.det_off = (uint64_t *)(ps.h_map + o_det_off);
-    hm.obs_off = (uint64_t *)(ps.h_map + o_obs_off);
+    hm.det_off = (uint32_t *)(ps.h_map + o_det_off);
+    hm.obs_off = (uint32_t *)(ps.h_map + o_obs_off);
     hm.probs = (double *)(ps.h_map + o_prob);
     hm.det_ids = (uint32_t *)(ps.h_map + o_det);
     hm.obs_ids = (uint32_t *)(ps.h_map + o_obs);
@@ -866,11 +870,14 @@ gp_status run_batch_pipelined(gp_ctx *ctx, const gp_circuit_view *cs, size_t cou
         } else {
             const uint64_t bE = bases[4 * j], bD = bases[4 * j + 1], bO = bases[4 * j + 2], bC = bases[4 * j + 3];
             const uint64_t E = h.num_edges, nd = h.num_det_ids, no = h.num_obs_ids, C = pj.tot.C;
-            if (bE + E + 1 > hm.e_cap || bD + nd > hm.ids_cap || bO + no > hm.ids_cap || bC + C + 1 > hm.c_cap) {
+            if (bD + nd >= 0xFFFFFFFFull || bO + no >= 0xFFFFFFFFull) {
+                *status |= 4;  // 32-bit id offsets of the batch view exceeded
+            } else if (bE + E + 1 > hm.e_cap || bD + nd > hm.ids_cap || bO + no > hm.ids_cap ||
+                       bC + C + 1 > hm.c_cap) {
                 *status |= 1;
             } else {
-                cudaMemcpyAsync(hm.det_off + bE, pj.o_det_off, (E + 1) * 8, cudaMemcpyDeviceToHost, ps.s_out);
-                cudaMemcpyAsync(hm.obs_off + bE, pj.o_obs_off, (E + 1) * 8, cudaMemcpyDeviceToHost, ps.s_out);
+                cudaMemcpyAsync(hm.det_off + bE, pj.o_det_off, (E + 1) * 4, cudaMemcpyDeviceToHost, ps.s_out);
+                cudaMemcpyAsync(hm.obs_off + bE, pj.o_obs_off, (E + 1) * 4, cudaMemcpyDeviceToHost, ps.s_out);
                 if (E) cudaMemcpyAsync(hm.probs + bE, pj.o_prob, E * 8, cudaMemcpyDeviceToHost, ps.s_out);
                 if (nd) cudaMemcpyAsync(hm.det_ids + bD, pj.o_det, nd * 4, cudaMemcpyDeviceToHost, ps.s_out);
                 if (no) cudaMemcpyAsync(hm.obs_ids + bO, pj.o_obs, no * 4, cudaMemcpyDeviceToHost, ps.s_out);
@@ -894,6 +901,7 @@ gp_status run_batch_pipelined(gp_ctx *ctx, const gp_circuit_view *cs, size_t cou
         if (ln.used) cudaEventSynchronize(ln.ev_in);  // the lane's previous staging was uploaded
         gp::PackPlan &pp = ln.pp;
         pp.force_wide = false;
+        pp.no_narrow = false;
     repack:
         gp::pack_plan(hpool, cs + c0, n, level, pp);
         if (pp.err == gp::kPackIndexSpace || pp.err == gp::kPackTooWide) {
@@ -905,8 +913,9 @@ gp_status run_batch_pipelined(gp_ctx *ctx, const gp_circuit_view *cs, size_t cou
             return drain(), fail(ctx, st, "pinned host allocation failed");
         gp::pack_range(hpool, cs + c0, pp, ln.h_stage, 0, n);
         if (pp.err) return drain(), fail_pack(ctx, pp.err);
-        if (pp.need_wide.load() && !pp.force_wide) {
-            pp.force_wide = true;
+        if ((pp.need_wide.load() && !pp.force_wide) || (pp.need_wide_words.load() && !pp.no_narrow)) {
+            if (pp.need_wide.load()) pp.force_wide = true;
+            pp.no_narrow = true;
             goto repack;
         }
         gp::pack_finish(pp, ln.h_stage);
@@ -995,6 +1004,7 @@ gp_status run_batch_pipelined(gp_ctx *ctx, const gp_circuit_view *cs, size_t cou
         }
         for (cudaEvent_t ev : tev) cudaEventDestroy(ev);
     }
+    if (*status & 4) return fail(ctx, GP_ERR_UNSUPPORTED, "batch exceeds 2^32 detector or observable ids; split it");
     if (*status) {  // capacity: let the unpipelined path learn larger hints
         ps.e_hint = 0;
         return GP_ERR_UNSUPPORTED;  // caller falls back
@@ -1019,7 +1029,7 @@ gp_status run_batch_pipelined(gp_ctx *ctx, const gp_circuit_view *cs, size_t cou
         stats->kernel_ns = (uint64_t)(all * 1e6);
         stats->num_sources = sources;
         stats->h2d_bytes = h2d_bytes;
-        stats->d2h_bytes = (E + 1) * 16 + E * 8 + (nd + no) * 4 + (count + 1) * 8;
+        stats->d2h_bytes = (E + 1) * 8 + E * 8 + (nd + no) * 4 + (count + 1) * 8;
         stats->kernel_launches = (uint64_t)launches;
         stats->total_ns = ns_since(t0);
     }
@@ -1358,15 +1368,15 @@ gp_status gp_merge_partials(gp_ctx *ctx, const gp_partial_view *parts, size_t np
         q = (size_t)align16(q + bytes);
         return at;
     };
-    const size_t o_det_off = otake((E + 1) * 8), o_obs_off = otake((E + 1) * 8), o_prob = otake(E * 8),
+    const size_t o_det_off = otake((E + 1) * 4), o_obs_off = otake((E + 1) * 4), o_prob = otake(E * 8),
                  o_det = otake(nd * 4), o_obs = otake(no * 4);
     if ((st = ensure_host(ctx, &ctx->h_out, &ctx->h_out_cap, q)) != GP_OK) return st;
     auto d2h = [&](size_t off, const void *src, size_t bytes) {
         if (bytes && e == cudaSuccess)
             e = cudaMemcpyAsync(ctx->h_out + off, src, bytes, cudaMemcpyDeviceToHost, ctx->stream);
     };
-    d2h(o_det_off, p.o_det_off, (E + 1) * 8);
-    d2h(o_obs_off, p.o_obs_off, (E + 1) * 8);
+    d2h(o_det_off, p.o_det_off, (E + 1) * 4);
+    d2h(o_obs_off, p.o_obs_off, (E + 1) * 4);
     d2h(o_prob, p.o_prob, E * 8);
     d2h(o_det, p.o_det, nd * 4);
     d2h(o_obs, p.o_obs, no * 4);
@@ -1376,8 +1386,8 @@ gp_status gp_merge_partials(gp_ctx *ctx, const gp_partial_view *parts, size_t np
     out->num_detectors = D;
     out->num_observables = O;
     out->num_edges = E;
-    out->det_offsets = (uint64_t *)(ctx->h_out + o_det_off);
-    out->obs_offsets = (uint64_t *)(ctx->h_out + o_obs_off);
+    out->det_offsets = (uint32_t *)(ctx->h_out + o_det_off);
+    out->obs_offsets = (uint32_t *)(ctx->h_out + o_obs_off);
     out->probs = (double *)(ctx->h_out + o_prob);
     out->det_ids = (uint32_t *)(ctx->h_out + o_det);
     out->obs_ids = (uint32_t *)(ctx->h_out + o_obs);
@@ -1531,13 +1541,13 @@ uint64_t dg_mix(uint64_t h, uint64_t w) {
 }
 
 // Digest of edges [e0, e1) of flat DEM arrays (gp_dem_digest's definition).
-uint64_t digest_range(uint32_t D, uint32_t O, uint64_t e0, uint64_t e1, const uint64_t *doff, const uint32_t *dids,
-                      const uint64_t *ooff, const uint32_t *oids, const double *probs) {
+uint64_t digest_range(uint32_t D, uint32_t O, uint64_t e0, uint64_t e1, const uint32_t *doff, const uint32_t *dids,
+                      const uint32_t *ooff, const uint32_t *oids, const double *probs) {
     uint64_t h = 0x6a09e667f3bcc909ull;
     h = dg_mix(h, (uint64_t)D << 32 | O);
     h = dg_mix(h, e1 - e0);
     for (uint64_t e = e0; e < e1; e++) {
-        h = dg_mix(h, (doff[e + 1] - doff[e]) << 32 | (ooff[e + 1] - ooff[e]));
+        h = dg_mix(h, (uint64_t)(doff[e + 1] - doff[e]) << 32 | (ooff[e + 1] - ooff[e]));
         for (uint64_t k = doff[e]; k < doff[e + 1]; k++) h = dg_mix(h, dids[k]);
         for (uint64_t k = ooff[e]; k < ooff[e + 1]; k++) h = dg_mix(h, oids[k]);
         uint64_t bits;

@@ -23,6 +23,7 @@ struct TravCfg {
     uint32_t walk_threads, walk_npt;  // walk CTA size; base nodes per node thread (0: generic)
     uint32_t G;          // boundaries per staged group (walk_kernel)
     uint32_t max_comp;   // sources per noise op at this level (6 / 10 / 15): the layer source map
+    uint32_t fuse_key;   // direct traversal files each source's reduce bucket (red::key_kernel skipped)
     uint32_t debug;      // experiments only: bit0 skip emission work, bit1 skip node work
 };
 
@@ -39,6 +40,13 @@ struct DevPlan {
     // STEPG IR built on device.
     uint32_t *ell;   // [tot.ell] base-slot ELLPACK (node words, gp_layout.h)
     uint64_t *leaf;  // [tot.leaf] leaf rows, tile-major per circuit (Eq. 3)
+
+    // Noise words as the traversal reads them (8 bytes per op): the image's
+    // own array, or -- narrow uploads -- widened into the workspace by lower_kernel.
+    uint64_t *noise_w;  // [N] narrow batches only
+    __host__ __device__ const uint64_t *noise_words() const {
+        return tot.narrow ? noise_w : reinterpret_cast<const uint64_t *>(img + lay.noise);
+    }
 
     // Per source.
     double *prob;      // [S]
@@ -64,15 +72,15 @@ struct DevPlan {
     // groups (edges) and their id counts, output offsets (scan).
     uint32_t *bcount;  // [NB + 1]
     uint4 *boff;       // [NB + 1]
-    struct ItemStub { uint32_t w[14]; };  // red::Item (56 bytes), sources in bucket order
+    struct alignas(16) ItemStub { uint64_t w[4]; };  // red::Item (32 bytes), sources in bucket order
     ItemStub *items;   // [items_cap]
     uint64_t items_cap;
     uint32_t *ecount;  // [NB]
     uint2 *eids;       // [NB]
     uint4 *oscan;      // [NB + 1]
-    // Per group (edge), at the bucket's slots: representative, probability, ids.
-    uint32_t *e_src, *e_ndno;
-    uint32_t *e_item;  // representative's sort item (complete keys), or ~0: ids from the records
+    // Per group (edge), at the bucket's slots: representative item, probability, id counts.
+    uint32_t *e_ndno;
+    uint32_t *e_item;  // representative's sort item (its key, or its source's records when incomplete)
     double *e_prob;
     uint32_t *huge;    // [NB] buckets too large for a warp
     uint64_t ids_cap;
@@ -86,7 +94,7 @@ struct DevPlan {
     // Offsets are global: this compile's edges / ids / circuits start at
     // base_in[0..3] of the whole batch (a pipelined batch is compiled in
     // sub-batches); write_kernel publishes base_out = base_in + totals.
-    uint64_t *o_det_off, *o_obs_off;  // [E_cap + 1] (values global)
+    uint32_t *o_det_off, *o_obs_off;  // [E_cap + 1] (values global, < 2^32)
     uint32_t *o_det, *o_obs;          // [ids_cap] (local positions)
     double *o_prob;                   // [E_cap]
     uint64_t *o_edge_off;             // [C + 1] (values global)
@@ -98,7 +106,8 @@ struct DevPlan {
     // and the header straight into mapped pinned host memory, so the host
     // waits once and reads everything there (no header round trip).
     struct {
-        uint64_t *det_off, *obs_off, *edge_off;
+        uint32_t *det_off, *obs_off;
+        uint64_t *edge_off;
         double *probs;
         uint32_t *det_ids, *obs_ids;
         DeviceHeader *hdr;

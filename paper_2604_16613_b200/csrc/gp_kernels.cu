@@ -171,10 +171,12 @@ __global__ void lower_kernel(__grid_constant__ const DevPlan p, uint32_t blocks_
         const uint32_t *lay_gate = arr<uint32_t>(p, p.lay.lay_gate);
         const uint32_t *lay_noise = arr<uint32_t>(p, p.lay.lay_noise);
         const uint64_t *gates = arr<uint64_t>(p, p.lay.gates);
+        const uint32_t *gates32 = arr<uint32_t>(p, p.lay.gates);
+        const bool narrow = p.tot.narrow != 0;
         const double *flip = arr<double>(p, p.lay.meas_flip);
         const uint64_t src_flip = m.src_base + m.src_noise;
         for (uint32_t g = lay_gate[li] + lane; g < lay_gate[li + 1]; g += 32) {
-            const uint64_t w = gates[g];
+            const uint64_t w = narrow ? widen_gate(gates32[g]) : gates[g];
             const uint32_t lo = (uint32_t)w, hi = (uint32_t)(w >> 32);
             const uint32_t q = lo & ((1u << kGateKindShift) - 1), kind = lo >> kGateKindShift;
             if (kind == 3 || kind == 4) p.prob[src_flip + hi] = flip[m.meas_base + hi];
@@ -211,13 +213,15 @@ __global__ void lower_kernel(__grid_constant__ const DevPlan p, uint32_t blocks_
         // Noise ops: component counts -> warp scan -> source offsets (from the
         // layer's base) and per-component probabilities.
         const uint64_t *noise = arr<uint64_t>(p, p.lay.noise);
+        const uint32_t *noise32 = arr<uint32_t>(p, p.lay.noise);
         const double *nprob = arr<double>(p, p.lay.noise_prob);
         const double *ptab = arr<double>(p, p.lay.prob_table);
         uint32_t base = arr<uint32_t>(p, p.lay.lay_src)[li];
         for (uint32_t o0 = lay_noise[li]; o0 < lay_noise[li + 1]; o0 += 32) {
             const uint32_t o = o0 + lane;
             const bool act = o < lay_noise[li + 1];
-            const uint64_t w = act ? noise[o] : 0;
+            const uint64_t w = act ? (narrow ? widen_noise(noise32[o]) : noise[o]) : 0;
+            if (act && narrow) p.noise_w[o] = w;  // the traversal's 8-byte words
             const uint32_t kind = noise_kind(w);
             const uint32_t k = act ? noise_components(kind, p.tot.level) : 0;
             uint32_t incl = k;
@@ -656,9 +660,12 @@ bool plan_traversal(const BatchTotals &t, int device, TravCfg *cfg, size_t *smem
             // the layer source -> op map is used only by source-major emission
             // (several words per CTA, every word of the circuit: TM > 1 && direct)
             const uint32_t comp = (T > 1 && t.max_W <= T) ? c.max_comp : 0;
-            const trav::Dims d(T, R, N, t.max_n, t.max_layer_meas, t.max_layer_noise, t.max_l, comp);
+            // a direct CTA owns its circuit's buckets: the key pass is fused
+            const bool fuse = T > 1 && t.max_W <= T && !std::getenv("GP_NO_FUSED_KEY");
+            const trav::Dims d(T, R, N, t.max_n, t.max_layer_meas, t.max_layer_noise, t.max_l, comp, fuse);
             if (d.total_bytes() <= budget) {
                 c.max_comp = comp;
+                c.fuse_key = fuse;
                 c.T = T;
                 c.R = R;
                 c.NST = N;
@@ -767,7 +774,8 @@ reduce:
     const uint32_t tpb = 256;
     uint4 *totals = p.bsum + p.bsum_cap - 4;  // scan totals live at the end of bsum
     const uint32_t sgrid = (uint32_t)std::min<uint64_t>(std::max<uint64_t>(blocks_for(S, tpb), 1), 148 * 32);
-    red::key_kernel<<<sgrid, tpb, 0, st>>>(p), launches++;
+    if (!(p.mode == kModeFull && p.trav.fuse_key && !p.trav.split))  // (else filed by the traversal)
+        red::key_kernel<<<sgrid, tpb, 0, st>>>(p), launches++;
     mark(kProfKey);
     launch_scan(BucketScanF{p.bcount}, NB + 1, p.bsum, p.boff, &totals[0], st, &launches);
     mark(kProfScanBucket);
@@ -781,8 +789,8 @@ reduce:
         red::bucket_kernel<<<(uint32_t)std::min<uint64_t>(std::max<uint64_t>(ctas, 1), 148 * 256),
                              red::kBucketThreads, 0, st>>>(p);
         smem_optin(red::huge_kernel);
-        // (a bucket over kWarpItems sources: at most S / (kWarpItems + 1) of them)
-        const uint32_t hgrid = (uint32_t)std::min<uint64_t>(kHugeCtas, std::max<uint64_t>(1, S / (red::kWarpItems + 1)));
+        // (listed buckets: over kWarpItems sources, or holding an incomplete key)
+        const uint32_t hgrid = (uint32_t)std::min<uint64_t>(kHugeCtas, std::max<uint64_t>(1, S / 64));
         red::huge_kernel<<<hgrid, 256, red::kHugeSmem, st>>>(p);
         launches += 2;
     }

@@ -54,6 +54,28 @@ __host__ __device__ inline uint32_t noise_q1(uint64_t w) { return (uint32_t)(w >
 __host__ __device__ inline uint32_t noise_kind(uint64_t w) { return (uint32_t)(w >> kNoiseKindShift & 3); }
 __host__ __device__ inline uint32_t noise_pidx(uint64_t w) { return (uint32_t)(w >> kNoisePidxShift); }
 
+// Narrow upload (BatchTotals.narrow: every circuit of the batch has at most
+// 4096 qubits and 32768 measurements, and the batch at most 64 distinct noise
+// probabilities): 4-byte op words halve the staging image -- the end-to-end
+// path is bound by host memory traffic -- and lower_kernel widens the noise
+// words into the workspace for the traversal.
+//   gate  : q0 [0,14) | kind [14,17) | hi [17,32) (CX target / local measurement)
+//   noise : q0 [0,12) | q1 [12,24) | kind [24,26) | probability index [26,32)
+constexpr uint32_t kNarrowMaxQubits = 4096, kNarrowMaxMeas = 32768, kNarrowMaxProbs = 64;
+__host__ __device__ inline uint32_t narrow_gate(uint32_t q0, uint32_t kind, uint32_t hi) {
+    return q0 | kind << 14 | hi << 17;
+}
+__host__ __device__ inline uint64_t widen_gate(uint32_t w) {
+    return (uint64_t)(w >> 17) << 32 | ((w & 0x3FFFu) | ((w >> 14) & 7u) << kGateKindShift);
+}
+__host__ __device__ inline uint32_t narrow_noise(uint32_t q0, uint32_t q1, uint32_t kind, uint32_t pidx) {
+    return q0 | q1 << 12 | kind << 24 | pidx << 26;
+}
+__host__ __device__ inline uint64_t widen_noise(uint32_t w) {
+    return (uint64_t)(w & 0xFFFu) | (uint64_t)(w >> 12 & 0xFFFu) << kNoiseQubitBits |
+           (uint64_t)(w >> 24 & 3u) << kNoiseKindShift | (uint64_t)(w >> 26) << kNoisePidxShift;
+}
+
 struct CircuitMeta {
     uint32_t n, l, M, D, O, W;
     uint32_t layer_base;   // index of layer 0 in the layer arrays (l + 1 entries per circuit)
@@ -90,8 +112,8 @@ struct StageLayout {
     uint64_t lay_gate;    // u32[sum(l + 1)] global gate index of each layer start
     uint64_t lay_noise;   // u32[sum(l + 1)] global noise index
     uint64_t lay_meas;    // u32[sum(l + 1)] local measurement index
-    uint64_t gates;       // u64[G]
-    uint64_t noise;       // u64[N] noise words
+    uint64_t gates;       // u64[G] gate words (u32 when narrow)
+    uint64_t noise;       // u64[N] noise words (u32 when narrow)
     uint64_t noise_prob;  // f64[N] (wide-probability mode only, else empty)
     uint64_t prob_table;  // f64[P] distinct noise probabilities of the batch
     uint64_t lay_src;     // u32[sum(l + 1)] local source offset of each layer's first op
@@ -124,6 +146,8 @@ struct BatchTotals {
     uint32_t max_layer_meas;
     uint32_t wide_prob;   // 1: per-op fp64 probabilities (table would exceed 14 bits)
     uint32_t prob_table_n;
+    uint32_t narrow;      // 1: 4-byte gate / noise words in the image (see narrow_gate)
+    uint32_t pad_;
 };
 
 // Header written by the device at the end of a compile (read back first).

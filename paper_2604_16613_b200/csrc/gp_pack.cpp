@@ -106,6 +106,13 @@ inline void put64(uint64_t *dst, uint64_t v) {
     *dst = v;
 #endif
 }
+inline void put32(uint32_t *dst, uint32_t v) {
+#if defined(__x86_64__)
+    _mm_stream_si32(reinterpret_cast<int *>(dst), (int)v);
+#else
+    *dst = v;
+#endif
+}
 inline void put_fence() {
 #if defined(__x86_64__)
     _mm_sfence();
@@ -133,8 +140,8 @@ StageLayout stage_layout(const BatchTotals &t) {
     L.lay_gate = put(t.layer_slots * 4);
     L.lay_noise = put(t.layer_slots * 4);
     L.lay_meas = put(t.layer_slots * 4);
-    L.gates = put(t.gates * 8);
-    L.noise = put(t.noise * 8);
+    L.gates = put(t.gates * (t.narrow ? 4 : 8));
+    L.noise = put(t.noise * (t.narrow ? 4 : 8));
     L.noise_prob = put(t.wide_prob ? t.noise * 8 : 0);
     L.lay_src = put(t.layer_slots * 4);
     L.meas_flip = put(t.meas * 8);
@@ -306,8 +313,12 @@ void pack_plan(HostPool *pool, const gp_circuit_view *cs, size_t C, uint8_t leve
     // at the end of the image (image_bytes() uploads the part used).
     t.wide_prob = pp.force_wide;
     t.prob_table_n = t.wide_prob ? 0 : kNoisePidxMax + 1;
+    uint32_t max_m = 0;
+    for (const CircuitMeta &m : pp.metas) max_m = std::max(max_m, m.M);
+    t.narrow = !t.wide_prob && !pp.no_narrow && t.max_n <= kNarrowMaxQubits && max_m <= kNarrowMaxMeas;
     pp.dict.clear();
     pp.need_wide.store(false);
+    pp.need_wide_words.store(false);
     pp.prob_table.clear();
     pp.L = stage_layout(t);
 }
@@ -322,6 +333,9 @@ void pack_range(HostPool *pool, const gp_circuit_view *cs, PackPlan &pp, uint8_t
     auto *lay_meas = (uint32_t *)at(L.lay_meas);
     auto *gates = (uint64_t *)at(L.gates);
     auto *noise = (uint64_t *)at(L.noise);
+    auto *gates32 = (uint32_t *)at(L.gates);
+    auto *noise32 = (uint32_t *)at(L.noise);
+    const bool narrow = t.narrow != 0;
     auto *nprob = (double *)at(L.noise_prob);
     auto *lay_src = (uint32_t *)at(L.lay_src);
     auto *flip = (double *)at(L.meas_flip);
@@ -373,7 +387,8 @@ void pack_range(HostPool *pool, const gp_circuit_view *cs, PackPlan &pp, uint8_t
                         flip[m.meas_base + hi] = v.gate_flip[g];
                         meas++;
                     }
-                    put64(&gates[m.gate_base + g - g0], (uint64_t)hi << 32 | (v.gate_q0[g] | (uint32_t)kd << kGateKindShift));
+                    if (narrow) put32(&gates32[m.gate_base + g - g0], narrow_gate(v.gate_q0[g], kd, hi));
+                    else put64(&gates[m.gate_base + g - g0], (uint64_t)hi << 32 | (v.gate_q0[g] | (uint32_t)kd << kGateKindShift));
                 }
                 lay_meas[li] = meas;  // count; prefix in pack_finish
                 uint32_t src = 0;
@@ -390,9 +405,17 @@ void pack_range(HostPool *pool, const gp_circuit_view *cs, PackPlan &pp, uint8_t
                             pi = 0;
                         }
                     }
-                    put64(&noise[idx], (uint64_t)v.noise_q0[o] |
-                                           (uint64_t)(kd == GP_NOISE_DEPOLARIZE2 ? v.noise_q1[o] : 0) << kNoiseQubitBits |
-                                           (uint64_t)kd << kNoiseKindShift | pi << kNoisePidxShift);
+                    const uint32_t q1 = kd == GP_NOISE_DEPOLARIZE2 ? v.noise_q1[o] : 0;
+                    if (narrow) {
+                        if (pi >= kNarrowMaxProbs) {  // a 65th probability: repack with 8-byte words
+                            pp.need_wide_words.store(true, std::memory_order_relaxed);
+                            pi = 0;
+                        }
+                        put32(&noise32[idx], narrow_noise(v.noise_q0[o], q1, kd, (uint32_t)pi));
+                    } else {
+                        put64(&noise[idx], (uint64_t)v.noise_q0[o] | (uint64_t)q1 << kNoiseQubitBits |
+                                               (uint64_t)kd << kNoiseKindShift | pi << kNoisePidxShift);
+                    }
                     src += comp_tab[kd & 7];
                 }
                 lay_src[li] = src;  // count; prefix in pack_finish

@@ -83,6 +83,8 @@ struct PackPlan {
     ProbDict dict;
     bool force_wide = false;            // in: per-op fp64 probabilities
     std::atomic<bool> need_wide{false};  // out: more distinct probabilities than the table holds
+    bool no_narrow = false;                    // in: 8-byte op words even where narrow ones fit
+    std::atomic<bool> need_wide_words{false};  // out: a narrow batch met a 65th probability
     int err = kPackOk;               // first failing circuit's error
     size_t err_circuit = 0;
     // Bytes of the packed image to upload (the probability table is last and

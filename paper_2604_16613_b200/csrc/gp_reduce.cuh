@@ -17,10 +17,16 @@
 // observable ids o0<o1<... is the sequence  d0+1, d1+1, ..., 0, o0+1, ..., 0
 // (then 0 forever). std::vector's lexicographic (dets, obs) compare -- a
 // prefix sorts first -- is exactly the lexicographic compare of these
-// sequences. seq[0] picks the bucket; seq[1..4] form a 128-bit sort key that
-// decides almost every compare; the rest is compared exactly (full records)
-// only when two keys tie, so distinct signatures never merge
-// (dem.cpp:73-78, test_dem.cpp:94-101).
+// sequences. seq[0] picks the bucket. Within a bucket (d0 equal), the
+// detector part compares like the CONSECUTIVE differences d1-d0, d2-d1, ...
+// (each >= 1; a list that ends scores 0, so a prefix sorts first): equal
+// prefixes of ids are equal prefixes of differences. Those differences,
+// 12 bits each, ten of them, are the 128-bit sort key of a 32-byte sort item;
+// the observables follow as a 64-bit mask (obs_cmp). A signature that does not
+// fit (more than 11 detectors, a difference over 4095, an observable id over
+// 63) keeps its source id instead and its bucket is compared exactly over the
+// full records, so distinct signatures never merge (dem.cpp:73-78,
+// test_dem.cpp:94-101).
 
 #include <type_traits>
 
@@ -105,38 +111,55 @@ struct SeqIt {
     }
 };
 
-// Exact canonical compare of two signatures (-1, 0, 1).
-__device__ __forceinline__ int seq_cmp(const DevPlan &p, uint64_t a, uint64_t b, uint32_t D) {
-    SeqIt x, y;
-    x.init(p, a, D);
-    y.init(p, b, D);
-    while (true) {
-        const uint32_t u = x.next(), v = y.next();
-        if (u != v) return u < v ? -1 : 1;
-        if (x.phase == 2 && y.phase == 2) return 0;
-    }
-}
-
-// Sort item. Key: the detector part of the sequence after d0 as sixteen
-// 16-bit slots, most significant first, relative to the bucket (d - d0 >= 1;
-// the separator and everything after it 0), plus the observables as a 64-bit
-// mask -- built from the source's records when the bucket is loaded.
-// "complete": every detector fits the slots (<= 16 after d0, deltas < 2^16)
-// and every observable id is < 64 (always true for the codes here). Within
-// one bucket, complete keys compare exactly like the canonical sequences:
-// slot-wise for the detectors (a prefix has its separator 0 first), then the
-// observable lists via their masks (obs_less). A bucket holding any
-// incomplete key is sorted with the exact comparator over the full records.
+// Sort item (32 bytes, two 16-byte stores / loads).
+//   k0: differences 1..5, k1: differences 6..10 -- 12 bits each, most
+//       significant first (bits 63..52 hold the first), 0 after the last;
+//       k1 bit 0: INCOMPLETE (the key did not fit; obs then holds the source)
+//       k1 bit 1: the signature has detectors (the bucket's q0 != 0; equal
+//       for every item of a bucket, so it never changes an order)
+//   obs: observable mask (complete items)
+//   prob: the source's probability (members of a group fold in its order)
+// No source id: complete items decode their ids from the key (write_kernel),
+// and order ties inside a bucket break by position.
 struct Item {
-    uint32_t k[8];   // sixteen 16-bit detector slots, most significant first
-    uint64_t obs;    // observable mask
-    double prob;     // members of a group sort by probability: the fold order
-    uint32_t src;
-    uint32_t ndno;   // detector ids | observable ids << 16 | complete << 31
-    __device__ bool complete() const { return ndno >> 31; }
+    uint64_t k0, k1, obs;
+    double prob;
+    __device__ bool complete() const { return !(k1 & 1); }
+    __device__ uint32_t src() const { return (uint32_t)obs; }
 };
 static_assert(sizeof(Item) == sizeof(DevPlan::ItemStub), "DevPlan::ItemStub mirrors Item");
 __device__ __forceinline__ Item *items_of(const DevPlan &p) { return reinterpret_cast<Item *>(p.items); }
+
+constexpr uint32_t kKeyFields = 10, kKeyDeltaMax = 4095;
+
+__device__ __forceinline__ void key_put(uint64_t &k0, uint64_t &k1, uint32_t f, uint64_t v) {
+    const uint32_t sh = 52 - 12 * (f % 5);
+    if (f < 5) k0 |= v << sh;
+    else k1 |= v << sh;
+}
+
+__device__ __forceinline__ uint32_t key_get(const Item &it, uint32_t f) {
+    return (uint32_t)(((f < 5 ? it.k0 : it.k1) >> (52 - 12 * (f % 5))) & 0xFFF);
+}
+
+// Detectors after d0 in a complete key (its nonzero fields form a prefix).
+__device__ __forceinline__ uint32_t key_len(const Item &it) {
+    uint32_t n = 0;
+#pragma unroll
+    for (uint32_t f = 0; f < kKeyFields; f++) n += key_get(it, f) != 0;
+    return n;
+}
+
+constexpr uint64_t kItemIncomplete = 1, kItemHasDet = 2;
+
+__device__ __forceinline__ Item incomplete_item(uint32_t s, double prob) {
+    Item it;
+    it.k0 = 0;
+    it.k1 = kItemIncomplete;
+    it.obs = s;
+    it.prob = prob;
+    return it;
+}
 
 // Word mask of the detector bits (ids < D) of word t.
 __device__ __forceinline__ uint64_t det_mask(uint32_t t, uint32_t D) {
@@ -169,107 +192,76 @@ __device__ __forceinline__ Item make_item_small(const DevPlan &p, uint32_t s, ui
     cs(1, 3);
     cs(1, 2);
     // Detector ids in order (records sorted by word, bits ascending): the
-    // first is the bucket (q0), the next ones go to 16-bit slots relative to
-    // it, four per 64-bit word, most significant first. Observables: a mask.
-    uint64_t kw[4] = {0, 0, 0, 0};
-    uint32_t q0 = 0, cnt = 0, nobs = 0;
+    // first is the bucket, the next ones go to the key as differences.
+    uint64_t k0 = 0, k1 = 0, obs = 0;
+    uint32_t prev = 0, cnt = 0;
     bool fits = true;
-    uint64_t obs = 0;
 #pragma unroll
     for (int j = 0; j < 4; j++) {
         if (t[j] == 0xFFFFFFFFu) continue;
         const uint64_t dm = det_mask(t[j], D);
         for (uint64_t m = w[j] & dm; m; m &= m - 1) {
-            const uint32_t id1 = t[j] * 64 + (uint32_t)__ffsll((long long)m);  // id + 1
-            if (cnt == 0) {
-                q0 = id1;
-            } else {
-                const uint32_t slot = cnt - 1, v = id1 - q0;
-                if (slot >= 15 || v >= 0xFFFFu) fits = false;  // no room for the separator / delta too wide
-                if (slot < 16) {
-                    const uint64_t add = (uint64_t)(v & 0xFFFF) << (48 - 16 * (slot & 3));
-                    const uint32_t wi = slot >> 2;
-                    kw[0] |= wi == 0 ? add : 0;
-                    kw[1] |= wi == 1 ? add : 0;
-                    kw[2] |= wi == 2 ? add : 0;
-                    kw[3] |= wi == 3 ? add : 0;
-                }
+            const uint32_t id = t[j] * 64 + (uint32_t)__ffsll((long long)m) - 1;
+            if (cnt) {
+                const uint32_t dv = id - prev;
+                if (cnt > kKeyFields || dv > kKeyDeltaMax) fits = false;
+                else key_put(k0, k1, cnt - 1, dv);
             }
+            prev = id;
             cnt++;
         }
         for (uint64_t ob = w[j] & ~dm; ob; ob &= ob - 1) {
             const uint32_t o = t[j] * 64 + (uint32_t)__ffsll((long long)ob) - 1 - D;
             if (o < 64) obs |= 1ull << o;
             else fits = false;
-            nobs++;
         }
     }
-    const uint32_t ndno = cnt | nobs << 16;  // id counts (the DEM's offsets)
+    const double prob = p.prob[s];
+    if (!fits || p.force_collisions) return incomplete_item(s, prob);
     Item it;
-#pragma unroll
-    for (int x = 0; x < 4; x++) {
-        it.k[2 * x] = (uint32_t)(kw[x] >> 32);
-        it.k[2 * x + 1] = (uint32_t)kw[x];
-    }
+    it.k0 = k0;
+    it.k1 = k1 | (cnt ? kItemHasDet : 0);
     it.obs = obs;
-    it.prob = p.prob[s];
-    it.src = s;
-    it.ndno = ndno | ((fits && !p.force_collisions) ? 1u << 31 : 0u);
+    it.prob = prob;
     return it;
 }
 
 // Sources with more than four records (rare): the generic path, out of line
 // so that the hot path keeps its registers.
-__device__ __noinline__ Item make_item_large(const DevPlan &p, uint32_t s, uint32_t D, uint32_t nrec) {
-    uint32_t nd = 0, no = 0;
-    for (uint32_t x = 0; x < nrec; x++) {
-        const uint64_t b = p.rbits[rec_at(p, s, x)], dm = det_mask(p.rtile[rec_at(p, s, x)], D);
-        nd += __popcll(b & dm);
-        no += __popcll(b & ~dm);
-    }
-    const uint32_t ndno = nd | no << 16;
-    Item it;
+__device__ __noinline__ Item make_item_large(const DevPlan &p, uint32_t s, uint32_t D) {
     SeqIt q;
     q.init(p, s, D);
-    const uint32_t q0 = q.next();  // first detector + 1, or 0 (no detectors): the bucket
-    bool sep = q0 == 0, fits = true;
-    uint32_t sl[16];
-#pragma unroll
-    for (int x = 0; x < 16; x++) {
-        uint32_t v = 0;
-        if (!sep) {
-            const uint32_t e = q.next();
-            if (e == 0) sep = true;  // detector separator
-            else {
-                v = e - q0;
-                if (v >= 0xFFFFu) fits = false;
-            }
-        }
-        sl[x] = v & 0xFFFF;
-    }
-    if (!sep) fits = false;  // more than 16 detectors after d0
-    uint64_t obs = 0;
-    if (fits) {  // remaining: observables (o + 1) then the terminator
-        for (uint32_t e; (e = q.next()) != 0;) {
-            if (e > 64) {
-                fits = false;
-                break;
-            }
-            obs |= 1ull << (e - 1);
+    uint32_t prev = q.next();  // first detector + 1, or 0 (no detectors): the bucket
+    const bool has_det = prev != 0;
+    bool sep = prev == 0, fits = true;
+    uint64_t k0 = 0, k1 = 0, obs = 0;
+    for (uint32_t f = 0; !sep; f++) {
+        const uint32_t e = q.next();
+        if (e == 0) {
+            sep = true;  // detector separator
+        } else {
+            if (f >= kKeyFields || e - prev > kKeyDeltaMax) fits = false;
+            else key_put(k0, k1, f, e - prev);
+            prev = e;
         }
     }
-#pragma unroll
-    for (int w = 0; w < 8; w++) it.k[w] = sl[2 * w] << 16 | sl[2 * w + 1];
+    for (uint32_t e; (e = q.next()) != 0;) {  // observables (o + 1), then the terminator
+        if (e > 64) fits = false;
+        else obs |= 1ull << (e - 1);
+    }
+    const double prob = p.prob[s];
+    if (!fits || p.force_collisions) return incomplete_item(s, prob);
+    Item it;
+    it.k0 = k0;
+    it.k1 = k1 | (has_det ? kItemHasDet : 0);
     it.obs = obs;
-    it.prob = p.prob[s];
-    it.src = s;
-    it.ndno = ndno | ((fits && !p.force_collisions) ? 1u << 31 : 0u);
+    it.prob = prob;
     return it;
 }
 
 __device__ __forceinline__ Item make_item(const DevPlan &p, uint32_t s, uint32_t D) {
     const uint32_t nrec = p.cnt[s];
-    return nrec <= 4 ? make_item_small(p, s, nrec, D) : make_item_large(p, s, D, nrec);
+    return nrec <= 4 ? make_item_small(p, s, nrec, D) : make_item_large(p, s, D);
 }
 
 // Lexicographic compare of two sorted id lists given as masks (a != b): at
@@ -284,28 +276,115 @@ __device__ __forceinline__ int obs_cmp(uint64_t a, uint64_t b) {
 }
 
 __device__ __forceinline__ int key_cmp(const Item &a, const Item &b) {
-#pragma unroll
-    for (int w = 0; w < 8; w++)
-        if (a.k[w] != b.k[w]) return a.k[w] < b.k[w] ? -1 : 1;
+    if (a.k0 != b.k0) return a.k0 < b.k0 ? -1 : 1;
+    if (a.k1 != b.k1) return a.k1 < b.k1 ? -1 : 1;
     return obs_cmp(a.obs, b.obs);
 }
 
+// The bucket an item is compared in: D of its circuit and q0 = first
+// detector + 1 (0: a bucket of observable-only signatures).
+struct BucketCtx {
+    uint32_t D, q0;
+};
+
+// Lazy canonical sequence of one item: decoded from a complete key, or
+// generated from the source's records (SeqIt) for an incomplete one.
+struct ItemSeq {
+    SeqIt r;
+    uint64_t k0, k1, obs;
+    uint32_t f, prev, state;  // state 0: d0, 1: differences, 2: observables, 3: done
+    bool rec;
+    __device__ void init(const DevPlan &p, const Item &it, BucketCtx c) {
+        rec = !it.complete();
+        if (rec) {
+            r.init(p, it.src(), c.D);
+            return;
+        }
+        k0 = it.k0;
+        k1 = it.k1;
+        obs = it.obs;
+        f = 0;
+        prev = c.q0;
+        state = 0;
+    }
+    __device__ bool done() const { return rec ? r.phase == 2 : state == 3; }
+    __device__ uint32_t next() {
+        if (rec) return r.next();
+        switch (state) {
+            case 0:
+                state = prev ? 1 : 2;  // no detectors: the separator comes first
+                return prev;
+            case 1: {
+                const uint32_t dv = f < kKeyFields ? key_get(Item{k0, k1, 0, 0}, f) : 0;
+                f++;
+                if (dv == 0) {
+                    state = 2;
+                    return 0;
+                }
+                prev += dv;
+                return prev;
+            }
+            case 2:
+                if (obs) {
+                    const uint32_t x = (uint32_t)__ffsll((long long)obs);
+                    obs &= obs - 1;
+                    return x;
+                }
+                state = 3;
+                return 0;
+            default:
+                return 0;
+        }
+    }
+};
+
+// Exact canonical compare of two items of one bucket (-1, 0, 1).
+__device__ __forceinline__ int seq_cmp(const DevPlan &p, const Item &a, const Item &b, BucketCtx c) {
+    ItemSeq x, y;
+    x.init(p, a, c);
+    y.init(p, b, c);
+    while (true) {
+        const uint32_t u = x.next(), v = y.next();
+        if (u != v) return u < v ? -1 : 1;
+        if (x.done() && y.done()) return 0;
+    }
+}
+
 // Canonical compare of two items of one bucket (0: identical signatures).
-// EXACT: some key of the bucket is incomplete -- compare the full records.
+// EXACT: some key of the bucket is incomplete -- compare the sequences.
 template <bool EXACT>
-__device__ __forceinline__ int sig_cmp(const DevPlan &p, const Item &a, const Item &b, uint32_t D) {
-    if (EXACT) return seq_cmp(p, a.src, b.src, D);
+__device__ __forceinline__ int sig_cmp(const DevPlan &p, const Item &a, const Item &b, BucketCtx c) {
+    if (EXACT) return seq_cmp(p, a, b, c);
     return key_cmp(a, b);
 }
 
 // Sort order: signature, then ascending probability -- the order the
-// reference folds a group in (dem.cpp:97-106) -- then source id.
+// reference folds a group in (dem.cpp:97-106) -- then position (ia, ib).
 template <bool EXACT>
-__device__ __forceinline__ bool item_less(const DevPlan &p, const Item &a, const Item &b, uint32_t D) {
-    const int c = sig_cmp<EXACT>(p, a, b, D);
-    if (c) return c < 0;
+__device__ __forceinline__ bool item_less(const DevPlan &p, const Item &a, uint32_t ia, const Item &b, uint32_t ib,
+                                          BucketCtx c) {
+    const int s = sig_cmp<EXACT>(p, a, b, c);
+    if (s) return s < 0;
     if (a.prob != b.prob) return a.prob < b.prob;
-    return a.src < b.src;
+    return ia < ib;
+}
+
+// Id counts (detectors | observables << 16) of a complete key.
+__device__ __forceinline__ uint32_t key_ndno(const Item &it) {
+    return ((uint32_t)(it.k1 >> 1 & 1) + key_len(it)) | (uint32_t)__popcll(it.obs) << 16;
+}
+
+// Id counts of any item's signature (an incomplete one: from its records).
+__device__ __forceinline__ uint32_t item_ndno(const DevPlan &p, const Item &it, BucketCtx c) {
+    if (it.complete()) return key_ndno(it);
+    const uint32_t s = it.src(), n = min(p.cnt[s], 16u);
+    uint32_t nd = 0, no = 0;
+    for (uint32_t x = 0; x < n; x++) {
+        const uint64_t b = p.rbits[rec_at(p, s, x)], dm = det_mask(p.rtile[rec_at(p, s, x)], c.D);
+        nd += __popcll(b & dm);
+        no += __popcll(b & ~dm);
+    }
+    return nd | no << 16;
 }
 
 // ---------------------------------------------------------------- R1 keys
@@ -366,9 +445,9 @@ __global__ void key_kernel(__grid_constant__ const DevPlan p) {
     });
 }
 
-// R3: counting-sort scatter. Each source's sort item (key built from its
-// records, probability, id counts) is written to its bucket slot, so the
-// bucket kernel reads every bucket as one contiguous run -- random gathers
+// R3: counting-sort scatter. Each source's 32-byte sort item (key built from
+// its records, probability) is written to its bucket slot, so the bucket
+// kernel reads every bucket as one contiguous run -- random gathers
 // (latency) become scattered stores (bandwidth).
 __global__ void __launch_bounds__(512, 3) scatter_kernel(__grid_constant__ const DevPlan p) {
     for_sources(p, [&](uint64_t s, CircCache &cc) {
@@ -385,98 +464,49 @@ __global__ void __launch_bounds__(512, 3) scatter_kernel(__grid_constant__ const
             atomicOr(&p.hdr->items_overflow, 1u);
             return;
         }
-        // 16-byte stores where the 56-byte item allows (every other slot is 16-byte aligned)
-        const uint64_t *w = reinterpret_cast<const uint64_t *>(&it);
-        uint64_t *d = reinterpret_cast<uint64_t *>(items_of(p) + at);
-        if ((at & 1) == 0) {
-            reinterpret_cast<ulonglong2 *>(d)[0] = make_ulonglong2(w[0], w[1]);
-            reinterpret_cast<ulonglong2 *>(d)[1] = make_ulonglong2(w[2], w[3]);
-            reinterpret_cast<ulonglong2 *>(d)[2] = make_ulonglong2(w[4], w[5]);
-            d[6] = w[6];
-        } else {
-            d[0] = w[0];
-            reinterpret_cast<ulonglong2 *>(d + 1)[0] = make_ulonglong2(w[1], w[2]);
-            reinterpret_cast<ulonglong2 *>(d + 1)[1] = make_ulonglong2(w[3], w[4]);
-            reinterpret_cast<ulonglong2 *>(d + 1)[2] = make_ulonglong2(w[5], w[6]);
-        }
+        ulonglong2 *d = reinterpret_cast<ulonglong2 *>(items_of(p) + at);
+        d[0] = make_ulonglong2(it.k0, it.k1);
+        d[1] = make_ulonglong2(it.obs, (unsigned long long)__double_as_longlong(it.prob));
     });
+}
+
+__device__ __forceinline__ Item load_item(const Item *it) {
+    const ulonglong2 a = reinterpret_cast<const ulonglong2 *>(it)[0], b = reinterpret_cast<const ulonglong2 *>(it)[1];
+    return Item{a.x, a.y, b.x, __longlong_as_double((long long)b.y)};
 }
 
 __device__ __forceinline__ uint32_t bucket_circuit(const DevPlan &p, uint64_t b) {
     return find_u32(arr<uint32_t>(p, p.lay.circ_bkt), p.tot.C, (uint32_t)b);
 }
 
-// Group starting at sorted position i0 of a bucket (slot base; at(x) is the
-// item at sorted position x): walks to the group's end, folding the members'
-// probabilities -- already ascending -- from 0 (merge_prob, dem.cpp:97-106),
-// and files edge g: representative source, probability, id counts (returned).
+__device__ __forceinline__ BucketCtx bucket_ctx(const DevPlan &p, uint64_t b) {
+    const CircuitMeta &m = arr<CircuitMeta>(p, p.lay.meta)[bucket_circuit(p, b)];
+    return BucketCtx{m.D, (uint32_t)b - m.bucket_base};
+}
+
+// Group starting at sorted position i0 of a bucket (at(x): the bucket index
+// of the item at sorted position x): walks to the group's end, folding the
+// members' probabilities -- already ascending -- from 0 (merge_prob,
+// dem.cpp:97-106), and files edge g: representative item, probability, id
+// counts (returned).
 template <bool EXACT, class At>
 __device__ __forceinline__ uint32_t emit_group(const DevPlan &p, uint32_t base, uint32_t g, const At &at, uint32_t i0,
-                                               uint32_t n, uint32_t D) {
-    double acc = merge_prob(0.0, at(i0).prob);
-    uint32_t e = i0 + 1;
-    while (e < n && sig_cmp<EXACT>(p, at(e - 1), at(e), D) == 0) acc = merge_prob(acc, at(e++).prob);
-    const uint32_t rep = at(i0).src;
-    const uint32_t ndno = at(i0).ndno & 0x7FFFFFFFu;
-    p.e_src[base + g] = rep;
-    p.e_item[base + g] = 0xFFFFFFFFu;  // (exact path: ids from the records)
+                                               uint32_t n, BucketCtx c) {
+    const Item *items = items_of(p) + base;
+    Item prev = load_item(items + at(i0));
+    double acc = merge_prob(0.0, prev.prob);
+    for (uint32_t e = i0 + 1; e < n; e++) {
+        const Item cur = load_item(items + at(e));
+        if (sig_cmp<EXACT>(p, prev, cur, c) != 0) break;
+        acc = merge_prob(acc, cur.prob);
+        prev = cur;
+    }
+    const uint32_t rep = at(i0);
+    const uint32_t ndno = item_ndno(p, load_item(items + rep), c);
+    p.e_item[base + g] = base + rep;
     p.e_prob[base + g] = acc;
     p.e_ndno[base + g] = ndno;
     return ndno;
-}
-
-// Groups of a sorted bucket, one warp: start flags by chunks of 32, group
-// ids by ballot prefix, one edge per group.
-template <bool EXACT, class At>
-__device__ __forceinline__ void groups_warp(const DevPlan &p, uint32_t b, uint32_t base, uint32_t n, uint32_t D,
-                                            const At &at) {
-    const uint32_t lane = threadIdx.x & 31;
-    uint32_t ng = 0, nd = 0, no = 0;
-    for (uint32_t c0 = 0; c0 < n; c0 += 32) {
-        const uint32_t i = c0 + lane;
-        const bool start = i < n && (i == 0 || sig_cmp<EXACT>(p, at(i - 1), at(i), D) != 0);
-        const uint32_t starts = __ballot_sync(0xffffffffu, start);
-        if (start) {
-            const uint32_t v = emit_group<EXACT>(p, base, ng + __popc(starts & ((1u << lane) - 1)), at, i, n, D);
-            nd += v & 0xFFFF;
-            no += v >> 16;
-        }
-        ng += __popc(starts);
-    }
-#pragma unroll
-    for (int d = 16; d > 0; d >>= 1) {
-        nd += __shfl_xor_sync(0xffffffffu, nd, d);
-        no += __shfl_xor_sync(0xffffffffu, no, d);
-    }
-    if (lane == 0) {
-        p.ecount[b] = ng;
-        p.eids[b] = make_uint2(nd, no);
-    }
-}
-
-// Branch-free "o sorts before m" for complete keys: key words, then the
-// observable lists (obs_cmp rule), then probability bits (nonnegative
-// doubles order like their bits), then source id. No divergence: every
-// lane of a warp compares against the same broadcast item.
-__device__ __forceinline__ uint32_t item_lt(const Item &o, const Item &m) {
-    bool lt = false, eq = true;
-#pragma unroll
-    for (int w = 0; w < 8; w++) {
-        lt |= eq && o.k[w] < m.k[w];
-        eq &= o.k[w] == m.k[w];
-    }
-    const uint64_t d = o.obs ^ m.obs;
-    const uint32_t x = (uint32_t)__ffsll((long long)d) - 1;  // valid when d != 0
-    const uint64_t above = x >= 63 ? 0 : ~0ull << (x + 1);
-    const bool x_in_o = (o.obs >> (x & 63)) & 1;
-    const bool obs_lt = d != 0 && (x_in_o ? (m.obs & above) != 0 : (o.obs & above) == 0);
-    lt |= eq && obs_lt;
-    eq &= d == 0;
-    const uint64_t po = (uint64_t)__double_as_longlong(o.prob), pm = (uint64_t)__double_as_longlong(m.prob);
-    lt |= eq && po < pm;
-    eq &= po == pm;
-    lt |= eq && o.src < m.src;
-    return lt ? 1u : 0u;
 }
 
 // ---------------------------------------------------------------- grouping
@@ -493,17 +523,14 @@ __device__ __forceinline__ uint32_t item_lt(const Item &o, const Item &m) {
 // Items stay in global memory (the bucket's contiguous run; L1-resident).
 
 __device__ __forceinline__ uint32_t item_hash(const Item &it) {
-    uint64_t h = 0x9e3779b97f4a7c15ull ^ it.obs;
-#pragma unroll
-    for (int w = 0; w < 8; w += 2) h = mix64(h ^ ((uint64_t)it.k[w] << 32 | it.k[w + 1]));
+    uint64_t h = mix64(0x9e3779b97f4a7c15ull ^ it.obs);
+    h = mix64(h ^ it.k0);
+    h = mix64(h ^ it.k1);
     return (uint32_t)(h >> 32);
 }
 
 __device__ __forceinline__ bool key_eq(const Item &a, const Item &b) {
-    bool eq = a.obs == b.obs;
-#pragma unroll
-    for (int w = 0; w < 8; w++) eq &= a.k[w] == b.k[w];
-    return eq;
+    return a.k0 == b.k0 && a.k1 == b.k1 && a.obs == b.obs;
 }
 
 struct WarpTeam {
@@ -605,7 +632,7 @@ __device__ bool group_bucket(const DevPlan &p, const Team &tm, uint32_t b, uint3
     // 1. representatives: hash + full key compare
     bool inc = false;
     for (uint32_t i = t0; i < n; i += nt) {
-        const Item me = it[i];
+        const Item me = load_item(it + i);
         inc |= !me.complete();
         uint32_t h = item_hash(me) & (w.tcap - 1), r = i;
         while (true) {
@@ -614,7 +641,7 @@ __device__ bool group_bucket(const DevPlan &p, const Team &tm, uint32_t b, uint3
                 cur = atomicCAS(&w.tab[h], (unsigned short)0xFFFF, (unsigned short)i);
                 if (cur == 0xFFFF) break;  // this item founds the group
             }
-            if (key_eq(it[cur], me)) {
+            if (key_eq(load_item(it + cur), me)) {
                 r = cur;
                 break;
             }
@@ -628,7 +655,6 @@ __device__ bool group_bucket(const DevPlan &p, const Team &tm, uint32_t b, uint3
     // 2. members grouped by representative; sorted ascending fold per group
     const uint32_t G = scan_groups(tm, w, n);
     constexpr bool kWarp = std::is_same<Team, WarpTeam>::value;
-    {
     for (uint32_t i = t0; i < n; i += nt) {
         const uint32_t r = w.rep[i];
         w.mp[w.off[r] + atomicSub(&w.cnt[r], 1u) - 1] = it[i].prob;
@@ -652,7 +678,6 @@ __device__ bool group_bucket(const DevPlan &p, const Team &tm, uint32_t b, uint3
         v[0] = acc;
     }
     tm.sync();
-    }
     // 3. groups in canonical order. A warp with at most 32 groups ranks them
     // (one group per lane, keys distinct); otherwise bitonic ("flip" form).
     if (kWarp && G <= 32) {
@@ -660,11 +685,11 @@ __device__ bool group_bucket(const DevPlan &p, const Team &tm, uint32_t b, uint3
         const uint32_t mine = lane < G ? w.grp[lane] : 0;
         uint32_t rank = 0;
         Item me{};
-        if (lane < G) me = it[mine];
+        if (lane < G) me = load_item(it + mine);
         for (uint32_t h = 0; h < G; h++) {  // the others' keys by shuffle (all lanes take part)
             Item o;
-#pragma unroll
-            for (int x = 0; x < 8; x++) o.k[x] = __shfl_sync(0xffffffffu, me.k[x], h);
+            o.k0 = __shfl_sync(0xffffffffu, me.k0, h);
+            o.k1 = __shfl_sync(0xffffffffu, me.k1, h);
             o.obs = __shfl_sync(0xffffffffu, me.obs, h);
             rank += (lane < G && h != lane && key_cmp(o, me) < 0) ? 1u : 0u;
         }
@@ -672,36 +697,35 @@ __device__ bool group_bucket(const DevPlan &p, const Team &tm, uint32_t b, uint3
         if (lane < G) w.grp[rank] = (uint16_t)mine;
         __syncwarp();
     } else {
-    uint32_t np = 1;
-    while (np < G) np <<= 1;
-    auto cas = [&](uint32_t x, uint32_t y) {
-        const uint32_t u = w.grp[x], v = w.grp[y];
-        if (key_cmp(it[v], it[u]) < 0) {
-            w.grp[x] = (uint16_t)v;
-            w.grp[y] = (uint16_t)u;
-        }
-    };
-    for (uint32_t k = 2; k <= np; k <<= 1) {
-        for (uint32_t x = t0; x < G; x += nt) {
-            const uint32_t y = x ^ (k - 1);
-            if (y > x && y < G) cas(x, y);
-        }
-        tm.sync();
-        for (uint32_t j = k >> 2; j > 0; j >>= 1) {
+        uint32_t np = 1;
+        while (np < G) np <<= 1;
+        auto cas = [&](uint32_t x, uint32_t y) {
+            const uint32_t u = w.grp[x], v = w.grp[y];
+            if (key_cmp(load_item(it + v), load_item(it + u)) < 0) {
+                w.grp[x] = (uint16_t)v;
+                w.grp[y] = (uint16_t)u;
+            }
+        };
+        for (uint32_t k = 2; k <= np; k <<= 1) {
             for (uint32_t x = t0; x < G; x += nt) {
-                const uint32_t y = x ^ j;
+                const uint32_t y = x ^ (k - 1);
                 if (y > x && y < G) cas(x, y);
             }
             tm.sync();
+            for (uint32_t j = k >> 2; j > 0; j >>= 1) {
+                for (uint32_t x = t0; x < G; x += nt) {
+                    const uint32_t y = x ^ j;
+                    if (y > x && y < G) cas(x, y);
+                }
+                tm.sync();
+            }
         }
-    }
     }
     // 4. edges
     uint32_t nd = 0, no = 0;
     for (uint32_t g = t0; g < G; g += nt) {
         const uint32_t r = w.grp[g];
-        const uint32_t v = it[r].ndno & 0x7FFFFFFFu;
-        p.e_src[base + g] = it[r].src;
+        const uint32_t v = key_ndno(load_item(it + r));  // (every key complete here)
         p.e_item[base + g] = base + r;  // complete key: write_kernel decodes the ids from the item
         p.e_prob[base + g] = w.mp[w.off[r]];
         p.e_ndno[base + g] = v;
@@ -728,36 +752,18 @@ __device__ bool group_bucket(const DevPlan &p, const Team &tm, uint32_t b, uint3
     return true;
 }
 
-// Exact fallback for a bucket holding an incomplete key (pathological
-// weights): rank every item with the exact comparator, then groups in order.
-__device__ void bucket_exact_warp(const DevPlan &p, uint32_t b, uint32_t base, uint32_t n, uint32_t D,
-                                  uint16_t *order) {
-    const uint32_t lane = threadIdx.x & 31;
-    const Item *it = items_of(p) + base;
-    for (uint32_t i = lane; i < n; i += 32) {
-        const Item m = it[i];
-        uint32_t rank = 0;
-        for (uint32_t j = 0; j < n; j++) rank += (j != i && item_less<true>(p, it[j], m, D)) ? 1 : 0;
-        order[rank] = (uint16_t)i;
-    }
-    __syncwarp();
-    auto at = [&](uint32_t x) -> const Item & { return it[order[x]]; };
-    groups_warp<true>(p, b, base, n, D, at);
-    __syncwarp();
-}
-
 // Bitonic network in its "flip" form: every comparator puts the smaller item
 // first, so indices >= n act as +infinity and are skipped (no padding).
-// `sync` is __syncwarp for one warp, __syncthreads for a CTA.
+// Items move (in place in the bucket's run), so ties keep their order.
 template <bool EXACT, class Sync>
-__device__ __forceinline__ void bitonic(const DevPlan &p, Item *it, uint32_t n, uint32_t D, uint32_t t0,
+__device__ __forceinline__ void bitonic(const DevPlan &p, Item *it, uint32_t n, BucketCtx c, uint32_t t0,
                                         uint32_t nt, Sync sync) {
     uint32_t np = 1;
     while (np < n) np <<= 1;
     auto cas = [&](uint32_t i, uint32_t l) {
-        const Item a = it[i], c = it[l];
-        if (item_less<EXACT>(p, c, a, D)) {
-            it[i] = c;
+        const Item a = load_item(it + i), d = load_item(it + l);
+        if (item_less<EXACT>(p, d, 1, a, 0, c)) {  // strictly smaller: swap
+            it[i] = d;
             it[l] = a;
         }
     };
@@ -779,14 +785,14 @@ __device__ __forceinline__ void bitonic(const DevPlan &p, Item *it, uint32_t n, 
 
 // One CTA, larger buckets (huge_kernel): bitonic sort, then groups.
 template <bool EXACT>
-__device__ void groups_cta(const DevPlan &p, uint32_t b, uint32_t base, uint32_t n, uint32_t D, const Item *it) {
+__device__ void groups_cta(const DevPlan &p, uint32_t b, uint32_t base, uint32_t n, BucketCtx c, const Item *it) {
     __shared__ uint32_t s_cnt[33], s_ids[2];
     if (threadIdx.x == 0) s_ids[0] = s_ids[1] = 0;
     uint32_t total = 0;
     const uint32_t w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     for (uint32_t c0 = 0; c0 < n; c0 += blockDim.x) {
         const uint32_t i = c0 + threadIdx.x;
-        const bool start = i < n && (i == 0 || sig_cmp<EXACT>(p, it[i - 1], it[i], D) != 0);
+        const bool start = i < n && (i == 0 || sig_cmp<EXACT>(p, load_item(it + i - 1), load_item(it + i), c) != 0);
         const uint32_t bal = __ballot_sync(0xffffffffu, start);
         if (lane == 0) s_cnt[w] = __popc(bal);
         __syncthreads();
@@ -801,9 +807,9 @@ __device__ void groups_cta(const DevPlan &p, uint32_t b, uint32_t base, uint32_t
         }
         __syncthreads();
         if (start) {
-            auto at = [&](uint32_t x) -> const Item & { return it[x]; };
+            auto at = [](uint32_t x) -> uint32_t { return x; };
             const uint32_t v =
-                emit_group<EXACT>(p, base, total + s_cnt[w] + __popc(bal & ((1u << lane) - 1)), at, i, n, D);
+                emit_group<EXACT>(p, base, total + s_cnt[w] + __popc(bal & ((1u << lane) - 1)), at, i, n, c);
             atomicAdd(&s_ids[0], v & 0xFFFF);
             atomicAdd(&s_ids[1], v >> 16);
         }
@@ -817,7 +823,7 @@ __device__ void groups_cta(const DevPlan &p, uint32_t b, uint32_t base, uint32_t
     __syncthreads();
 }
 
-__device__ void bucket_cta(const DevPlan &p, uint32_t b, uint32_t n, uint32_t D, Item *it) {
+__device__ void bucket_cta(const DevPlan &p, uint32_t b, uint32_t n, BucketCtx c, Item *it) {
     const uint32_t base = p.boff[b].x;
     __shared__ uint32_t s_inc;
     if (threadIdx.x == 0) s_inc = 0;
@@ -826,11 +832,11 @@ __device__ void bucket_cta(const DevPlan &p, uint32_t b, uint32_t n, uint32_t D,
         if (!it[i].complete()) s_inc = 1;
     __syncthreads();
     if (s_inc) {
-        bitonic<true>(p, it, n, D, threadIdx.x, blockDim.x, [] { __syncthreads(); });
-        groups_cta<true>(p, b, base, n, D, it);
+        bitonic<true>(p, it, n, c, threadIdx.x, blockDim.x, [] { __syncthreads(); });
+        groups_cta<true>(p, b, base, n, c, it);
     } else {
-        bitonic<false>(p, it, n, D, threadIdx.x, blockDim.x, [] { __syncthreads(); });
-        groups_cta<false>(p, b, base, n, D, it);
+        bitonic<false>(p, it, n, c, threadIdx.x, blockDim.x, [] { __syncthreads(); });
+        groups_cta<false>(p, b, base, n, c, it);
     }
 }
 
@@ -839,15 +845,14 @@ constexpr uint32_t kWarpWs = (256 * 18 + 16 + 512 * 2 + 15) & ~15u;  // GroupWs:
 constexpr uint32_t kHugeSmem = 196 * 1024;                            // huge_kernel dynamic smem
 
 // One warp per bucket, no CTA synchronisation: empty buckets, buckets of up
-// to kWarpItems sources (group_bucket in the warp's workspace, or the exact
-// fallback); larger ones are listed for huge_kernel.
+// to kWarpItems sources (group_bucket in the warp's workspace); larger ones
+// and those holding an incomplete key are listed for huge_kernel.
 __global__ void __launch_bounds__(kBucketThreads) bucket_kernel(__grid_constant__ const DevPlan p) {
     __shared__ __align__(16) uint8_t ws[(kBucketThreads / 32) * kWarpWs];
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     GroupWs w;
     w.carve(ws + warp * kWarpWs, kWarpItems, kWarpTab);
     const uint64_t NB = p.tot.buckets;
-    const CircuitMeta *meta = arr<CircuitMeta>(p, p.lay.meta);
     const uint64_t warps = (uint64_t)gridDim.x * (kBucketThreads / 32);
     if (p.hdr->items_overflow) return;  // re-run with a larger item array
     for (uint64_t b = ((uint64_t)blockIdx.x * kBucketThreads + threadIdx.x) >> 5; b < NB; b += warps) {
@@ -864,25 +869,30 @@ __global__ void __launch_bounds__(kBucketThreads) bucket_kernel(__grid_constant_
             continue;
         }
         const Item *it = items_of(p) + base;
-        if (!group_bucket(p, WarpTeam{}, (uint32_t)b, base, n, it, w))  // (an incomplete key: exact ranks)
-            bucket_exact_warp(p, (uint32_t)b, base, n, meta[bucket_circuit(p, b)].D,
-                              reinterpret_cast<uint16_t *>(w.tab));
+        uint32_t tc = 64;  // hash table: a power of two >= 2n
+        while (tc < 2 * n) tc <<= 1;
+        w.tcap = tc;
+        // an incomplete key: the bucket goes to huge_kernel's exact CTA sort
+        // (kept out of this kernel: its comparator's state costs registers)
+        if (!group_bucket(p, WarpTeam{}, (uint32_t)b, base, n, it, w) && lane == 0)
+            p.huge[atomicAdd(&p.hdr->huge_count, 1u)] = (uint32_t)b;
     }
 }
 
-// Buckets too large for a warp: one CTA each, group_bucket in up to 196 KB
-// of dynamic shared memory; the exact CTA sort (in place in the bucket's own
-// run of the item array) for incomplete keys or buckets beyond that.
+// Buckets too large for a warp, or holding an incomplete key: one CTA each,
+// group_bucket in up to 196 KB of dynamic shared memory; the exact CTA sort
+// (in place in the bucket's own run of the item array) for incomplete keys or
+// buckets beyond that.
 __global__ void __launch_bounds__(256) huge_kernel(__grid_constant__ const DevPlan p) {
     extern __shared__ __align__(16) uint8_t hsm[];
     if (p.hdr->items_overflow) return;
     const uint32_t nh = p.hdr->huge_count;
-    const CircuitMeta *meta = arr<CircuitMeta>(p, p.lay.meta);
     __shared__ uint32_t s_inc;
     for (uint32_t i = blockIdx.x; i < nh; i += gridDim.x) {
         const uint32_t b = p.huge[i];
         const uint32_t base = p.boff[b].x, n = p.boff[b + 1].x - base;
         Item *it = items_of(p) + base;
+        const BucketCtx c = bucket_ctx(p, b);
         if (threadIdx.x == 0) s_inc = 0;
         __syncthreads();
         for (uint32_t x = threadIdx.x; x < n; x += blockDim.x)
@@ -895,7 +905,7 @@ __global__ void __launch_bounds__(256) huge_kernel(__grid_constant__ const DevPl
             w.carve(hsm, n, tc);
             group_bucket(p, CtaTeam{}, b, base, n, it, w);
         } else {
-            bucket_cta(p, b, n, meta[bucket_circuit(p, b)].D, it);
+            bucket_cta(p, b, n, c, it);
         }
         __syncthreads();
     }
@@ -903,8 +913,8 @@ __global__ void __launch_bounds__(256) huge_kernel(__grid_constant__ const DevPl
 
 // ---------------------------------------------------------------- R6 output
 // Bucket b's groups become edges [eoff, eoff + ecount) of the flat DEM, ids
-// expanded from the representative's records in word order (bit b < D ->
-// detector b, else observable b - D; dem.cpp:108-116).
+// decoded from the representative's key (or expanded from its records, in
+// word order: bit b < D -> detector b, else observable b - D; dem.cpp:108-116).
 __global__ void write_kernel(__grid_constant__ const DevPlan p, const uint4 *out_total) {
     const uint64_t NB = p.tot.buckets;
     const uint32_t lane = threadIdx.x & 31;
@@ -921,8 +931,8 @@ __global__ void write_kernel(__grid_constant__ const DevPlan p, const uint4 *out
             h.num_edges = tot.x;
             h.num_det_ids = tot.y;
             h.num_obs_ids = tot.z;
-            p.o_det_off[tot.x] = bD + tot.y;
-            p.o_obs_off[tot.x] = bO + tot.z;
+            p.o_det_off[tot.x] = (uint32_t)(bD + tot.y);
+            p.o_obs_off[tot.x] = (uint32_t)(bO + tot.z);
         }
         *p.hdr = h;
         *p.hdr_out = h;
@@ -941,8 +951,7 @@ __global__ void write_kernel(__grid_constant__ const DevPlan p, const uint4 *out
         if (ne == 0) continue;
         const uint4 o = p.oscan[b];  // (edges, det ids, obs ids) before this bucket
         const uint32_t base = p.boff[b].x;
-        const CircuitMeta &cm = meta[bucket_circuit(p, b)];
-        const uint32_t D = cm.D, q0 = (uint32_t)b - cm.bucket_base;  // first detector + 1 (0: none)
+        const BucketCtx c = bucket_ctx(p, b);
         const Item *items = items_of(p);
         uint32_t dcar = 0, ocar = 0;
         for (uint32_t k0 = 0; k0 < ne; k0 += 32) {
@@ -956,45 +965,45 @@ __global__ void write_kernel(__grid_constant__ const DevPlan p, const uint4 *out
             uint32_t di = nd, oi = no;  // inclusive warp scans
 #pragma unroll
             for (int d = 1; d < 32; d <<= 1) {
-                const uint32_t a = __shfl_up_sync(0xffffffffu, di, d), c = __shfl_up_sync(0xffffffffu, oi, d);
+                const uint32_t a = __shfl_up_sync(0xffffffffu, di, d), cc = __shfl_up_sync(0xffffffffu, oi, d);
                 if (lane >= (uint32_t)d) {
                     di += a;
-                    oi += c;
+                    oi += cc;
                 }
             }
             if (k < ne) {
                 const uint64_t e = (uint64_t)o.x + k;
                 const uint32_t d0 = o.y + dcar + di - nd, o0 = o.z + ocar + oi - no;
-                p.o_det_off[e] = bD + d0;
-                p.o_obs_off[e] = bO + o0;
+                p.o_det_off[e] = (uint32_t)(bD + d0);
+                p.o_obs_off[e] = (uint32_t)(bO + o0);
                 p.o_prob[e] = p.e_prob[base + k];
-                const uint32_t ii = p.e_item[base + k];
-                if (ii != 0xFFFFFFFFu) {  // complete key: detectors q0 - 1 + slot deltas, observables by mask
-                    const Item q = items[ii];
-                    uint32_t wd = d0, wo = o0;
-                    if (q0) {
-                        p.o_det[wd++] = q0 - 1;
-                        for (uint32_t x = 0; x < 16; x++) {
-                            const uint32_t v = (q.k[x >> 1] >> ((x & 1) ? 0 : 16)) & 0xFFFF;
-                            if (v == 0) break;
-                            p.o_det[wd++] = q0 - 1 + v;
+                const Item q = load_item(items + p.e_item[base + k]);
+                uint32_t wd = d0, wo = o0;
+                if (q.complete()) {  // detectors q0 - 1, then the differences; observables by mask
+                    if (c.q0) {
+                        uint32_t id = c.q0 - 1;
+                        p.o_det[wd++] = id;
+                        for (uint32_t f = 0; f < kKeyFields; f++) {
+                            const uint32_t dv = key_get(q, f);
+                            if (dv == 0) break;
+                            id += dv;
+                            p.o_det[wd++] = id;
                         }
                     }
                     for (uint64_t ob = q.obs; ob; ob &= ob - 1) p.o_obs[wo++] = (uint32_t)__ffsll((long long)ob) - 1;
                 } else {  // ids from the representative's records, in word order
-                    const uint32_t r = p.e_src[base + k];
+                    const uint32_t r = q.src();
                     uint8_t ord[16];
                     const uint32_t n = min(p.cnt[r], 16u);
                     sig_order(p, r, n, ord);
-                    uint32_t wd = d0, wo = o0;
                     for (uint32_t x = 0; x < n; x++) {
                         const uint32_t t = p.rtile[rec_at(p, r, ord[x])];
                         uint64_t bits = p.rbits[rec_at(p, r, ord[x])];
                         while (bits) {
                             const uint32_t id = t * 64 + (uint32_t)__ffsll((long long)bits) - 1;
                             bits &= bits - 1;
-                            if (id < D) p.o_det[wd++] = id;
-                            else p.o_obs[wo++] = id - D;
+                            if (id < c.D) p.o_det[wd++] = id;
+                            else p.o_obs[wo++] = id - c.D;
                         }
                     }
                 }

@@ -42,9 +42,9 @@ struct StageHdr {  // written by the producer into each stage
 static_assert(sizeof(StageHdr) % 16 == 0, "bulk-copy destinations must stay 16-byte aligned");
 
 struct Dims {
-    uint32_t T, R, NST, n2, ell_w, leaf_w, noise_w, src_w, lay_w, map_w;
+    uint32_t T, R, NST, n2, ell_w, leaf_w, noise_w, src_w, lay_w, map_w, bkt_w;
     __host__ __device__ Dims(uint32_t t, uint32_t r, uint32_t nst, uint32_t max_n, uint32_t max_meas,
-                             uint32_t max_noise, uint32_t max_l, uint32_t max_comp = 15)
+                             uint32_t max_noise, uint32_t max_l, uint32_t max_comp = 15, bool fuse_key = false)
         : T(t),
           R(r),
           NST(nst),
@@ -54,13 +54,15 @@ struct Dims {
           noise_w((max_noise + 3) & ~1u),
           src_w((max_noise + 9) & ~3u),
           lay_w((max_l + 4) & ~3u),
-          map_w((max_noise * max_comp + 8) & ~7u) {}
+          map_w((max_noise * max_comp + 8) & ~7u),
+          bkt_w(fuse_key ? (64 * t + 4) & ~3u : 0) {}
     __host__ __device__ size_t ring_bytes() const { return (size_t)R * T * n2 * 8; }
     __host__ __device__ size_t stage_bytes() const {
         return sizeof(StageHdr) + (size_t)ell_w * 4 + ((size_t)T * leaf_w + noise_w) * 8 + (size_t)src_w * 4;
     }
     __host__ __device__ size_t total_bytes() const {
-        return ring_bytes() + NST * stage_bytes() + (2 * NST + 2 * R) * 8 + (size_t)2 * lay_w * 4 + (size_t)map_w * 2 + 64;
+        return ring_bytes() + NST * stage_bytes() + (2 * NST + 2 * R) * 8 + (size_t)2 * lay_w * 4 + (size_t)bkt_w * 4 +
+               (size_t)map_w * 2 + 64;
     }
     __device__ uint64_t *slot(uint8_t *base, uint32_t r) const {
         return reinterpret_cast<uint64_t *>(base) + (size_t)r * T * n2;
@@ -82,8 +84,10 @@ struct Dims {
     }
     // Per-layer tables of the CTA's circuit (measurement / noise-op offsets).
     __device__ uint32_t *lay(uint8_t *base) const { return reinterpret_cast<uint32_t *>(bars(base) + 2 * NST + 2 * R); }
+    // per-bucket source counts of the CTA's circuit (fused bucket keys)
+    __device__ uint32_t *bkt(uint8_t *base) const { return lay(base) + 2 * lay_w; }
     // layer source -> op (source-major emission)
-    __device__ uint16_t *map(uint8_t *base) const { return reinterpret_cast<uint16_t *>(lay(base) + 2 * lay_w); }
+    __device__ uint16_t *map(uint8_t *base) const { return reinterpret_cast<uint16_t *>(bkt(base) + bkt_w); }
 };
 
 __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
@@ -107,11 +111,22 @@ __device__ __forceinline__ bool named_or(int id, int nthreads, bool pred) {
     return out != 0;
 }
 
+// Fused bucket keys (direct traversal: the CTA owns its circuit's every
+// word): each nonempty source's reduce bucket -- (circuit, first detector),
+// gp_reduce.cuh -- is found here from the words in registers and its slot in
+// the bucket claimed on a shared-memory counter; the CTA publishes the
+// circuit's bucket counts at its end. This is the reduce's key pass
+// (red::key_kernel) without re-reading the records.
+struct KeyCtx {
+    uint32_t *sbkt;  // shared per-bucket counters (D + 1), or null: no fusion
+    uint32_t bucket_base, D;
+};
+
 // Writes one source's sparse signature words. `direct`: this CTA owns every
 // word of the source (T == W), so the signature is written without atomics.
 template <int TM>
 __device__ __forceinline__ void emit_source(const DevPlan &p, uint64_t src, uint32_t t0, uint32_t tw,
-                                            const uint64_t (&v)[TM], bool direct) {
+                                            const uint64_t (&v)[TM], bool direct, const KeyCtx &kc) {
     uint32_t nz = 0;
 #pragma unroll
     for (int w = 0; w < TM; w++) nz += ((uint32_t)w < tw && v[w] != 0);
@@ -122,13 +137,22 @@ __device__ __forceinline__ void emit_source(const DevPlan &p, uint64_t src, uint
         atomicMax(&p.hdr->record_overflow, j + nz);
         return;
     }
+    uint32_t first = 0xFFFFFFFFu;
 #pragma unroll
     for (int w = 0; w < TM; w++)
         if ((uint32_t)w < tw && v[w]) {
             p.rbits[rec_at(p, src, j)] = v[w];
             p.rtile[rec_at(p, src, j)] = t0 + w;
             j++;
+            const uint32_t b0 = (t0 + w) * 64;
+            const uint64_t dm = b0 + 64 <= kc.D ? ~0ull : b0 >= kc.D ? 0 : (1ull << (kc.D - b0)) - 1;
+            if (first == 0xFFFFFFFFu && (v[w] & dm)) first = b0 + (uint32_t)__ffsll((long long)(v[w] & dm)) - 1;
         }
+    if (kc.sbkt) {
+        const uint32_t local = first == 0xFFFFFFFFu ? 0 : first + 1;
+        p.s_bkt[src] = kc.bucket_base + local;
+        p.s_pos[src] = atomicAdd(&kc.sbkt[local], 1u);
+    }
 }
 
 // Warp-cooperative append into the record pool: lane-uniform chunk state,
@@ -207,7 +231,8 @@ __global__ void __launch_bounds__(800, 1) traverse_kernel(__grid_constant__ cons
     __shared__ int s_issued_lo;      // lowest boundary the producer staged
     __shared__ uint32_t s_grp;
 
-    const Dims L(cfg.T, cfg.R, cfg.NST, cfg.max_n, cfg.max_layer_meas, cfg.max_layer_noise, cfg.max_l, cfg.max_comp);
+    const Dims L(cfg.T, cfg.R, cfg.NST, cfg.max_n, cfg.max_layer_meas, cfg.max_layer_noise, cfg.max_l, cfg.max_comp,
+                 cfg.fuse_key != 0);
     const uint32_t tid = threadIdx.x;
     const uint32_t warp = tid >> 5, lane = tid & 31;
     const uint32_t node_threads = cfg.node_warps * 32, emit_threads = cfg.emit_warps * 32;
@@ -297,11 +322,14 @@ __global__ void __launch_bounds__(800, 1) traverse_kernel(__grid_constant__ cons
         uint64_t *z = L.slot(smem, L.R - 1);
         for (uint32_t x = tid; x < L.T * n2; x += blockDim.x) z[x] = 0;
     }
+    const KeyCtx kc{cfg.fuse_key ? L.bkt(smem) : nullptr, m.bucket_base, m.D};
+    if (kc.sbkt)
+        for (uint32_t x = tid; x <= m.D; x += blockDim.x) kc.sbkt[x] = 0;
     __syncthreads();
 
     const uint32_t *ell = p.ell + m.ell_base;
     const uint32_t estride = ell_stride(m.n);
-    const uint64_t *noise = arr<uint64_t>(p, p.lay.noise);
+    const uint64_t *noise = p.noise_words();
     const uint32_t *nsrc = p.nsrc;
 
     if (warp == 0) {
@@ -404,7 +432,7 @@ __global__ void __launch_bounds__(800, 1) traverse_kernel(__grid_constant__ cons
                 uint64_t v[TM];
 #pragma unroll
                 for (int w = 0; w < TM; w++) v[w] = (uint32_t)w < tw ? leaf[(uint64_t)(t0 + w) * leaf_stride(m.M) + mm] : 0;
-                emit_source<TM>(p, src_flip + mm, t0, tw, v, direct);
+                emit_source<TM>(p, src_flip + mm, t0, tw, v, direct, kc);
             }
         }
         constexpr uint8_t kMask[15] = {4, 8, 1, 5, 2, 10, 12, 9, 3, 6, 13, 7, 15, 11, 14};
@@ -459,7 +487,7 @@ __global__ void __launch_bounds__(800, 1) traverse_kernel(__grid_constant__ cons
                         }
                         v[w] = x;
                     }
-                    emit_source<TM>(p, m.src_base + ls, t0, tw, v, direct);
+                    emit_source<TM>(p, m.src_base + ls, t0, tw, v, direct, kc);
                 }
             } else
             // Warp-uniform trip count (the pool path needs whole-warp rounds).
@@ -513,15 +541,15 @@ __global__ void __launch_bounds__(800, 1) traverse_kernel(__grid_constant__ cons
                     anyw |= x0[w] | z0[w];
                 }
                 if (kind <= 1) {
-                    if (anyw) emit_source<TM>(p, src, t0, tw, kind == 0 ? x0 : z0, direct);
+                    if (anyw) emit_source<TM>(p, src, t0, tw, kind == 0 ? x0 : z0, direct, kc);
                 } else if (kind == 2) {
                     if (!anyw) continue;
                     uint64_t y[TM];
 #pragma unroll
                     for (int w = 0; w < TM; w++) y[w] = x0[w] ^ z0[w];
-                    emit_source<TM>(p, src, t0, tw, x0, direct);  // X, Z, then Y at L1+ (stepg.cpp:75-83)
-                    emit_source<TM>(p, src + 1, t0, tw, z0, direct);
-                    if (level) emit_source<TM>(p, src + 2, t0, tw, y, direct);
+                    emit_source<TM>(p, src, t0, tw, x0, direct, kc);  // X, Z, then Y at L1+ (stepg.cpp:75-83)
+                    emit_source<TM>(p, src + 1, t0, tw, z0, direct, kc);
+                    if (level) emit_source<TM>(p, src + 2, t0, tw, y, direct, kc);
                 } else {
                     // Component words are re-read from the on-chip state slot per
                     // component: keeps only T words live in registers.
@@ -542,7 +570,7 @@ __global__ void __launch_bounds__(800, 1) traverse_kernel(__grid_constant__ cons
                                                      : ((mk & 1) ? rx0[o2] : 0) ^ ((mk & 2) ? rz0[o2] : 0) ^
                                                            ((mk & 4) ? rx1[o2] : 0) ^ ((mk & 8) ? rz1[o2] : 0);
                         }
-                        emit_source<TM>(p, src + c, t0, tw, v, direct);
+                        emit_source<TM>(p, src + c, t0, tw, v, direct, kc);
                     }
                 }
             }
@@ -556,6 +584,8 @@ __global__ void __launch_bounds__(800, 1) traverse_kernel(__grid_constant__ cons
         pool_close(p, pw, lane);
     }
     __syncthreads();
+    if (kc.sbkt)  // the circuit's bucket counts (the CTA owns all of them)
+        for (uint32_t x = tid; x <= m.D; x += blockDim.x) p.bcount[m.bucket_base + x] = kc.sbkt[x];
     // Drain bulk copies staged below the stopping boundary (never consumed;
     // each is the latest use of its stage, so its phase parity is unambiguous).
     if (tid == 0)

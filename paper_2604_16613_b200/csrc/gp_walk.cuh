@@ -318,7 +318,7 @@ __global__ void __launch_bounds__(256) emit_kernel(__grid_constant__ const DevPl
     const uint32_t level = p.tot.level;
     const CircuitMeta *meta = arr<CircuitMeta>(p, p.lay.meta);
     const uint32_t *lay_noise = arr<uint32_t>(p, p.lay.lay_noise);
-    const uint64_t *noise = arr<uint64_t>(p, p.lay.noise);
+    const uint64_t *noise = p.noise_words();
     constexpr uint8_t kMask[15] = {4, 8, 1, 5, 2, 10, 12, 9, 3, 6, 13, 7, 15, 11, 14};
     // Noise ops at live boundaries: one CTA per slab.
     for (uint64_t sl = blockIdx.x; sl < used; sl += gridDim.x) {
