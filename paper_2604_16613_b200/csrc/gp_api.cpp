@@ -206,15 +206,29 @@ size_t carve(gp_ctx *ctx, DevPlan &p, const BatchTotals &t, uint8_t *base, uint3
     p.force_collisions = ctx->force_collisions;
     p.bcount = (uint32_t *)take(NB * 4 + 4);
     p.boff = (uint4 *)take((NB + 1) * 16);
-    p.items = (DevPlan::ItemStub *)take(items_cap * sizeof(DevPlan::ItemStub));
-    p.items_cap = items_cap;
+    // Fused items: positions are circuit regions of S slots (every source may emit).
+    p.fused = p.trav.fuse_key && !p.trav.split && p.mode == gp::kModeFull;
+    const uint64_t icap = p.fused ? S + 16 : items_cap;
+    p.items = (DevPlan::ItemStub *)take(icap * sizeof(DevPlan::ItemStub));
+    p.items_cap = icap;
     p.ecount = (uint32_t *)take(NB * 4);
     p.eids = (uint2 *)take(NB * 8);
     p.oscan = (uint4 *)take((NB + 1) * 16);
-    p.e_ndno = (uint32_t *)take(items_cap * 4);
-    p.e_item = (uint32_t *)take(items_cap * 4);
-    p.e_prob = (double *)take(items_cap * 8);
+    p.e_ndno = (uint32_t *)take(icap * 4);
+    p.e_item = (uint32_t *)take(icap * 4);
+    p.e_prob = (double *)take(icap * 8);
     p.huge = (uint32_t *)take(NB * 4);
+    if (p.fused) {
+        // items moved into bucket order (contiguous runs for the bucket warps)
+        // unless GP_FUSED_MOVE=0 (index lists; measured 0.45 ms slower per
+        // 4,096 branches in the bucket stage)
+        const char *mv = std::getenv("GP_FUSED_MOVE");
+        p.fused_move = mv ? (uint32_t)std::atoi(mv) : 1;
+        p.items2 = (DevPlan::ItemStub *)take(icap * sizeof(DevPlan::ItemStub));
+        p.ibkt = (uint16_t *)take(S * 2);
+        p.iidx = (uint32_t *)take(S * 4);
+        p.ptab3 = (double *)take((size_t)t.prob_table_n * 32 + 32);
+    }
     if (p.mode == gp::kModeShard) {  // compact partial table of the shard
         p.p_prob = (double *)take(S * 8);
         p.p_roff = (uint32_t *)take(S * 4 + 4);
@@ -557,8 +571,9 @@ repack:  // (again with per-op probabilities when the table overflowed)
             ctx->record_slots = K;
             continue;
         }
-        if (hdr.num_det_ids == 0xFFFFFFFFu) {  // id capacity overflow
+        if (hdr.num_det_ids == 0xFFFFFFFFu) {  // id (or, fused items: edge) capacity overflow
             ids_cap *= 4;
+            if (p.fused) items_cap = std::max<uint64_t>(items_cap, t.sources + 16);
             ctx->ids_hint = ids_cap;
             continue;
         }

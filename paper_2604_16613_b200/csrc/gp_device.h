@@ -23,7 +23,7 @@ struct TravCfg {
     uint32_t walk_threads, walk_npt;  // walk CTA size; base nodes per node thread (0: generic)
     uint32_t G;          // boundaries per staged group (walk_kernel)
     uint32_t max_comp;   // sources per noise op at this level (6 / 10 / 15): the layer source map
-    uint32_t fuse_key;   // direct traversal files each source's reduce bucket (red::key_kernel skipped)
+    uint32_t fuse_key;   // direct traversal builds the reduce's sort items (red::key_kernel / scatter_kernel skipped)
     uint32_t debug;      // experiments only: bit0 skip emission work, bit1 skip node work
 };
 
@@ -83,6 +83,18 @@ struct DevPlan {
     uint32_t *e_item;  // representative's sort item (its key, or its source's records when incomplete)
     double *e_prob;
     uint32_t *huge;    // [NB] buckets too large for a warp
+    // Fused items (trav.fuse_key, full mode): the direct traversal writes each
+    // nonempty source's sort item into its circuit's region of `items` (from
+    // src_base, in emission order) with its circuit-local bucket in `ibkt`,
+    // then lists every bucket's items in `iidx` (boff[b] = {first, count});
+    // huge_kernel gathers a listed bucket into `items2` (same positions) and
+    // marks its e_item entries with kItem2.
+    uint32_t fused;
+    uint32_t fused_move;  // the CTA moves the items into bucket order in items2 (no index list)
+    ItemStub *items2;  // [S + 16]
+    uint16_t *ibkt;    // [S]
+    uint32_t *iidx;    // [S]
+    double *ptab3;     // [P * 4] noise probability table: p, p / 3, p / 15 (IEEE division)
     uint64_t ids_cap;
 
     // Scan scratch.

@@ -114,14 +114,19 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t *bar, uint32_t by
                  : "memory");
 }
 
-__device__ __forceinline__ bool mbar_try_wait(uint64_t *bar, uint32_t parity) {
+constexpr uint32_t kMbarSleepNs = 20000;
+
+// try_wait with a suspend-time hint: the waiting warp sleeps until the phase
+// completes (or the hint expires) instead of re-polling, so waiting roles do
+// not take issue slots from the working ones.
+__device__ __forceinline__ bool mbar_try_wait_sleep(uint64_t *bar, uint32_t parity, uint32_t ns = kMbarSleepNs) {
     uint32_t ok;
     asm volatile(
         "{\n\t.reg .pred p;\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
         "selp.u32 %0, 1, 0, p;\n\t}"
         : "=r"(ok)
-        : "r"(smem_u32(bar)), "r"(parity)
+        : "r"(smem_u32(bar)), "r"(parity), "r"(ns)
         : "memory");
     return ok != 0;
 }
@@ -130,8 +135,8 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t *bar, uint32_t parity) {
 // of hanging the device (a few seconds of suspended try_waits).
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
     uint32_t spins = 0;
-    while (!mbar_try_wait(bar, parity))
-        if (++spins > 20000000u) __trap();
+    while (!mbar_try_wait_sleep(bar, parity))
+        if (++spins > 200000u) __trap();
 }
 
 __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
@@ -175,11 +180,14 @@ __global__ void lower_kernel(__grid_constant__ const DevPlan p, uint32_t blocks_
         const bool narrow = p.tot.narrow != 0;
         const double *flip = arr<double>(p, p.lay.meas_flip);
         const uint64_t src_flip = m.src_base + m.src_noise;
+        // fused items: the traversal takes each source's probability from the
+        // flips / ptab3 itself (no per-source array)
+        const bool fused_prob = p.fused && !p.tot.wide_prob;
         for (uint32_t g = lay_gate[li] + lane; g < lay_gate[li + 1]; g += 32) {
             const uint64_t w = narrow ? widen_gate(gates32[g]) : gates[g];
             const uint32_t lo = (uint32_t)w, hi = (uint32_t)(w >> 32);
             const uint32_t q = lo & ((1u << kGateKindShift) - 1), kind = lo >> kGateKindShift;
-            if (kind == 3 || kind == 4) p.prob[src_flip + hi] = flip[m.meas_base + hi];
+            if ((kind == 3 || kind == 4) && !fused_prob) p.prob[src_flip + hi] = flip[m.meas_base + hi];
             if (i == 0) continue;  // no boundary before layer 0
             uint32_t *e = p.ell + m.ell_base + (uint64_t)(i - 1) * ell_stride(m.n);
             const uint32_t x = 2 * q, z = 2 * q + 1;
@@ -236,7 +244,8 @@ __global__ void lower_kernel(__grid_constant__ const DevPlan p, uint32_t blocks_
                 const double pr = p.tot.wide_prob ? nprob[o] : ptab[noise_pidx(w)];
                 const double pe = kind == 2 ? __ddiv_rn(pr, 3.0) : kind == 3 ? __ddiv_rn(pr, 15.0) : pr;
                 double *dst = p.prob + m.src_base + off;
-                for (uint32_t j = 0; j < k; j++) dst[j] = pe;
+                if (!fused_prob)
+                    for (uint32_t j = 0; j < k; j++) dst[j] = pe;
             }
             base += __shfl_sync(0xffffffffu, incl, 31);
         }
@@ -244,6 +253,16 @@ __global__ void lower_kernel(__grid_constant__ const DevPlan p, uint32_t blocks_
     }
     // Part B.
     const uint64_t t = (uint64_t)(blockIdx.x - blocks_a) * blockDim.x + threadIdx.x;
+    if (t >= p.tot.dets + p.tot.obss) {  // Part C (fused items): component probabilities per table entry
+        const uint64_t x = t - p.tot.dets - p.tot.obss;
+        if (p.fused && x < p.tot.prob_table_n) {
+            const double pr = arr<double>(p, p.lay.prob_table)[x];
+            p.ptab3[4 * x] = pr;
+            p.ptab3[4 * x + 1] = __ddiv_rn(pr, 3.0);
+            p.ptab3[4 * x + 2] = __ddiv_rn(pr, 15.0);
+        }
+        return;
+    }
     if (t < p.tot.dets) {
         const uint32_t c = find_u32(arr<uint32_t>(p, p.lay.circ_det), C, (uint32_t)t);
         const CircuitMeta m = meta[c];
@@ -253,7 +272,7 @@ __global__ void lower_kernel(__grid_constant__ const DevPlan p, uint32_t blocks_
         uint64_t *row = p.leaf + m.leaf_base + (uint64_t)(d >> 6) * leaf_stride(m.M);
         for (uint32_t k = off[d]; k < off[d + 1]; k++)
             atomicXor((unsigned long long *)&row[ms[k]], 1ull << (d & 63));
-    } else if (t < p.tot.dets + p.tot.obss) {
+    } else {
         const uint32_t to = (uint32_t)(t - p.tot.dets);
         const uint32_t c = find_u32(arr<uint32_t>(p, p.lay.circ_obs), C, to);
         const CircuitMeta m = meta[c];
@@ -269,6 +288,7 @@ __global__ void lower_kernel(__grid_constant__ const DevPlan p, uint32_t blocks_
 
 // ---------------------------------------------------------------- K2 traversal
 }  // namespace
+#include "gp_reduce.cuh"
 #include "gp_traverse.cuh"
 #include "gp_walk.cuh"
 namespace {
@@ -516,7 +536,6 @@ __global__ void zero_kernel(ZeroRanges z) {
 }
 
 }  // namespace
-#include "gp_reduce.cuh"
 namespace {
 
 template <class F>
@@ -599,11 +618,13 @@ bool plan_traversal(const BatchTotals &t, int device, TravCfg *cfg, size_t *smem
     c.node_warps = n2 <= 512 ? 4 : n2 <= 2048 ? 8 : 12;
     c.emit_warps = c.node_warps;
     if (t.C >= 2u * (uint32_t)sms && t.max_W <= 8 && n2 <= 512) {
-        // wide-group batches of small circuits: emission (source expansion) is
-        // the heavier role; 224 threads and a 2-deep state ring fit four CTAs
-        // per SM (registers and shared memory), which beats deeper rings
-        c.node_warps = 2;
-        c.emit_warps = 4;
+        // wide-group batches of small circuits: emission (source expansion and
+        // the sort items) is the heavier role; 224 threads and a 2-deep state
+        // ring fit four CTAs per SM (registers and shared memory), which beats
+        // deeper rings (measured: 1 + 5 warps 4.37 ms, 2 + 4 4.41, 1 + 7 with
+        // a 3-deep ring 4.48 per 4,096 branches)
+        c.node_warps = 1;
+        c.emit_warps = 5;
     }
     if (const char *o = std::getenv("GP_TRAV_WARPS")) {  // tuning: "node,emit"
         unsigned a = 0, b = 0;
@@ -661,7 +682,7 @@ bool plan_traversal(const BatchTotals &t, int device, TravCfg *cfg, size_t *smem
             // (several words per CTA, every word of the circuit: TM > 1 && direct)
             const uint32_t comp = (T > 1 && t.max_W <= T) ? c.max_comp : 0;
             // a direct CTA owns its circuit's buckets: the key pass is fused
-            const bool fuse = T > 1 && t.max_W <= T && !std::getenv("GP_NO_FUSED_KEY");
+            const bool fuse = T > 1 && t.max_W <= T && t.sources < (1ull << 31) && !std::getenv("GP_NO_FUSED_KEY");
             const trav::Dims d(T, R, N, t.max_n, t.max_layer_meas, t.max_layer_noise, t.max_l, comp, fuse);
             if (d.total_bytes() <= budget) {
                 c.max_comp = comp;
@@ -700,9 +721,12 @@ int enqueue_pipeline(const DevPlan &p, cudaStream_t st, const StageEvents *ev, c
         if (p.mode != kModeMerge) {  // (merge: counts and records are uploaded)
             add(p.ell, p.tot.ell * 4);
             add(p.leaf, p.tot.leaf * 8);
-            add(p.cnt, S * 4 + 4);
+            // fused items: records are written (and read) only for incomplete keys
+            if (!p.fused) add(p.cnt, S * 4 + 4);
         }
-        add(p.bcount, NB * 4 + 4);
+        // fused items: the traversal files every bucket it sees ({first, count}); the rest stay empty
+        if (p.fused) add(p.boff, (NB + 1) * 16);
+        else add(p.bcount, NB * 4 + 4);
         add(p.hdr, sizeof(DeviceHeader));
         uint64_t units = 0;
         for (int r = 0; r < z.count; r++) units = std::max(units, z.n16[r]);
@@ -720,7 +744,7 @@ int enqueue_pipeline(const DevPlan &p, cudaStream_t st, const StageEvents *ev, c
     {
         const uint32_t tpb = 256;
         const uint32_t ba = blocks_for(p.tot.layers, tpb / 32);
-        const uint32_t bb = blocks_for(p.tot.dets + p.tot.obss, tpb);
+        const uint32_t bb = blocks_for(p.tot.dets + p.tot.obss + (p.fused ? p.tot.prob_table_n : 0), tpb);
         if (ba + bb) lower_kernel<<<ba + bb, tpb, 0, st>>>(p, ba), launches++;
     }
     mark(kProfLower);
@@ -774,14 +798,17 @@ reduce:
     const uint32_t tpb = 256;
     uint4 *totals = p.bsum + p.bsum_cap - 4;  // scan totals live at the end of bsum
     const uint32_t sgrid = (uint32_t)std::min<uint64_t>(std::max<uint64_t>(blocks_for(S, tpb), 1), 148 * 32);
-    if (!(p.mode == kModeFull && p.trav.fuse_key && !p.trav.split))  // (else filed by the traversal)
+    if (!p.fused) {  // (fused items: keys, bucket lists and items come from the traversal)
         red::key_kernel<<<sgrid, tpb, 0, st>>>(p), launches++;
-    mark(kProfKey);
-    launch_scan(BucketScanF{p.bcount}, NB + 1, p.bsum, p.boff, &totals[0], st, &launches);
-    mark(kProfScanBucket);
-    {  // (512-thread CTAs measure best for the scatter, 128 for the write)
+        mark(kProfKey);
+        launch_scan(BucketScanF{p.bcount}, NB + 1, p.bsum, p.boff, &totals[0], st, &launches);
+        mark(kProfScanBucket);
+        // (512-thread CTAs measure best for the scatter, 128 for the write)
         const uint32_t g512 = (uint32_t)std::min<uint64_t>(std::max<uint64_t>(blocks_for(S, 512), 1), 148 * 16);
         red::scatter_kernel<<<g512, 512, 0, st>>>(p), launches++;
+    } else {
+        mark(kProfKey);
+        mark(kProfScanBucket);
     }
     mark(kProfScatter);
     {

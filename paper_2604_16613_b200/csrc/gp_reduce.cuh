@@ -264,6 +264,78 @@ __device__ __forceinline__ Item make_item(const DevPlan &p, uint32_t s, uint32_t
     return nrec <= 4 ? make_item_small(p, s, nrec, D) : make_item_large(p, s, D);
 }
 
+// Item of a signature held in registers (fused items: the direct traversal
+// owns all TM words of its circuit, word w = ids [64 w, 64 w + 64)). Ids come
+// out ascending, word by word, bit by bit; each detector id pushes its
+// difference into a 128-bit shift register (branch-free: the first id's
+// "difference" is pushed too and shifted out at the end), observables are
+// shifted into their mask a word at a time. *local = the circuit-local bucket
+// (first detector + 1, or 0 without detectors).
+template <int TM>
+__device__ __forceinline__ Item item_of_words(const uint64_t (&v)[TM], uint32_t tw, uint32_t D, double prob,
+                                              uint32_t src, bool force, uint32_t *local) {
+    uint64_t hi = 0, lo = 0, obs = 0;
+    uint32_t prev = 0, cnt = 0, first = 0;
+    bool fits = true;
+    const uint32_t wD = D >> 6;
+    const uint64_t lowD = (1ull << (D & 63)) - 1;
+#pragma unroll
+    for (int w = 0; w < TM; w++) {
+        if ((uint32_t)w >= tw || !v[w]) continue;
+        const uint64_t dm = (uint32_t)w < wD ? ~0ull : (uint32_t)w == wD ? lowD : 0ull;
+        for (uint64_t m = v[w] & dm; m; m &= m - 1) {
+            const uint32_t id = (uint32_t)w * 64 + (uint32_t)__ffsll((long long)m) - 1;
+            const uint32_t dv = id - prev;
+            fits &= dv <= kKeyDeltaMax || cnt == 0;
+            first = cnt == 0 ? id : first;
+            hi = hi << 12 | lo >> 52;
+            lo = lo << 12 | dv;
+            prev = id;
+            cnt++;
+        }
+        const uint64_t ob = v[w] & ~dm;  // observable o = 64 w + bit - D
+        if (ob) {
+            const int sh = w * 64 - (int)D;
+            if (sh >= 64) fits = false;
+            else if (sh >= 0) {
+                if (sh > 0 && (ob >> (64 - sh))) fits = false;
+                obs |= ob << sh;
+            } else {
+                obs |= ob >> -sh;
+            }
+        }
+    }
+    *local = cnt ? first + 1 : 0;
+    if (cnt > kKeyFields + 1 || !fits || force) return incomplete_item(src, prob);
+    // n = cnt - 1 differences in the low 12 n bits: align field 0 at bit 119
+    // (k0 = bits 119..60 << 4, k1 = bits 59..0 << 4, as key_put lays them out)
+    uint64_t k0 = 0, k1 = 0;
+    if (cnt > 1) {
+        const uint32_t s = 12 * (kKeyFields + 1 - cnt);
+        if (s >= 64) {
+            hi = lo << (s - 64);
+            lo = 0;
+        } else if (s > 0) {
+            hi = hi << s | lo >> (64 - s);
+            lo <<= s;
+        }
+        k0 = (hi << 4 | lo >> 60) << 4;
+        k1 = lo << 4;
+    }
+    Item it;
+    it.k0 = k0;
+    it.k1 = k1 | (cnt ? kItemHasDet : 0);
+    it.obs = obs;
+    it.prob = prob;
+    return it;
+}
+
+__device__ __forceinline__ void store_item(Item *dst, const Item &it) {
+    ulonglong2 *d = reinterpret_cast<ulonglong2 *>(dst);
+    d[0] = make_ulonglong2(it.k0, it.k1);
+    d[1] = make_ulonglong2(it.obs, (unsigned long long)__double_as_longlong(it.prob));
+}
+
 // Lexicographic compare of two sorted id lists given as masks (a != b): at
 // the smallest id x in exactly one list, the list holding x is smaller iff
 // the other list continues past x (a list that ends there is a prefix).
@@ -464,15 +536,37 @@ __global__ void __launch_bounds__(512, 3) scatter_kernel(__grid_constant__ const
             atomicOr(&p.hdr->items_overflow, 1u);
             return;
         }
-        ulonglong2 *d = reinterpret_cast<ulonglong2 *>(items_of(p) + at);
-        d[0] = make_ulonglong2(it.k0, it.k1);
-        d[1] = make_ulonglong2(it.obs, (unsigned long long)__double_as_longlong(it.prob));
+        store_item(items_of(p) + at, it);
     });
 }
 
 __device__ __forceinline__ Item load_item(const Item *it) {
     const ulonglong2 a = reinterpret_cast<const ulonglong2 *>(it)[0], b = reinterpret_cast<const ulonglong2 *>(it)[1];
     return Item{a.x, a.y, b.x, __longlong_as_double((long long)b.y)};
+}
+
+// e_item entries of buckets gathered into items2 (fused items, huge_kernel).
+constexpr uint32_t kItem2 = 0x80000000u;
+
+// The items of one bucket as the grouping sees them: i in [0, n).
+struct RunAcc {  // a contiguous run (bucket order); e_item = position | flag
+    const Item *it;
+    uint32_t base, flag;
+    __device__ Item load(uint32_t i) const { return load_item(it + i); }
+    __device__ double prob(uint32_t i) const { return it[i].prob; }
+    __device__ uint32_t gidx(uint32_t i) const { return (base + i) | flag; }
+};
+struct IdxAcc {  // fused items: through the bucket's index list
+    const Item *items;
+    const uint32_t *idx;
+    __device__ Item load(uint32_t i) const { return load_item(items + idx[i]); }
+    __device__ double prob(uint32_t i) const { return items[idx[i]].prob; }
+    __device__ uint32_t gidx(uint32_t i) const { return idx[i]; }
+};
+
+// Items and item count of bucket b.
+__device__ __forceinline__ uint32_t bucket_size(const DevPlan &p, uint64_t b) {
+    return p.fused ? p.boff[b].y : p.boff[b + 1].x - p.boff[b].x;
 }
 
 __device__ __forceinline__ uint32_t bucket_circuit(const DevPlan &p, uint64_t b) {
@@ -490,9 +584,8 @@ __device__ __forceinline__ BucketCtx bucket_ctx(const DevPlan &p, uint64_t b) {
 // dem.cpp:97-106), and files edge g: representative item, probability, id
 // counts (returned).
 template <bool EXACT, class At>
-__device__ __forceinline__ uint32_t emit_group(const DevPlan &p, uint32_t base, uint32_t g, const At &at, uint32_t i0,
-                                               uint32_t n, BucketCtx c) {
-    const Item *items = items_of(p) + base;
+__device__ __forceinline__ uint32_t emit_group(const DevPlan &p, const Item *items, uint32_t base, uint32_t flag,
+                                               uint32_t g, const At &at, uint32_t i0, uint32_t n, BucketCtx c) {
     Item prev = load_item(items + at(i0));
     double acc = merge_prob(0.0, prev.prob);
     for (uint32_t e = i0 + 1; e < n; e++) {
@@ -503,7 +596,7 @@ __device__ __forceinline__ uint32_t emit_group(const DevPlan &p, uint32_t base, 
     }
     const uint32_t rep = at(i0);
     const uint32_t ndno = item_ndno(p, load_item(items + rep), c);
-    p.e_item[base + g] = base + rep;
+    p.e_item[base + g] = (base + rep) | flag;
     p.e_prob[base + g] = acc;
     p.e_ndno[base + g] = ndno;
     return ndno;
@@ -572,6 +665,51 @@ struct GroupWs {
     }
 };
 
+// The group's member probabilities mp[o, e) folded from 0 in ascending order
+// (merge_prob, dem.cpp:97-106). A group holds few distinct values (the noise
+// model's p, p/3, p/15, flips), so it is folded one distinct value at a time:
+// the smallest value above the last one and its multiplicity, O(k d) reads
+// instead of an O(k^2) sort. Values that do not order (NaN) fall back to an
+// insertion sort (mp[o, e) is scratch either way).
+__device__ __forceinline__ double fold_sorted(double *mp, uint32_t o, uint32_t e) {
+    double acc = 0.0, last = -INFINITY;
+    uint32_t done = 0;
+    bool first = true;
+    while (done < e - o) {
+        double x = INFINITY;
+        uint32_t c = 0;
+        for (uint32_t a = o; a < e; a++) {
+            const double y = mp[a];
+            if (y > last || (first && y == last)) {
+                if (y < x) {
+                    x = y;
+                    c = 1;
+                } else if (y == x) {
+                    c++;
+                }
+            }
+        }
+        if (c == 0) break;  // unordered values remain
+        for (uint32_t j = 0; j < c; j++) acc = merge_prob(acc, x);
+        done += c;
+        last = x;
+        first = false;
+    }
+    if (done == e - o) return acc;
+    for (uint32_t a = o + 1; a < e; a++) {  // insertion sort of the group's probabilities
+        const double x = mp[a];
+        uint32_t z = a;
+        while (z > o && mp[z - 1] > x) {
+            mp[z] = mp[z - 1];
+            z--;
+        }
+        mp[z] = x;
+    }
+    acc = 0.0;
+    for (uint32_t a = o; a < e; a++) acc = merge_prob(acc, mp[a]);
+    return acc;
+}
+
 // Exclusive prefix of cnt[0..n) into off[], listing representatives (cnt > 0)
 // in grp[] (ascending item order); returns the group count. Team-wide.
 template <class Team>
@@ -622,9 +760,9 @@ __device__ __forceinline__ uint32_t scan_groups(const Team &tm, const GroupWs &w
 
 // Returns false, having written nothing, when some key of the bucket is
 // incomplete (found while hashing): the caller takes the exact path.
-template <class Team>
+template <class Team, class Acc>
 __device__ bool group_bucket(const DevPlan &p, const Team &tm, uint32_t b, uint32_t base, uint32_t n,
-                             const Item *it, GroupWs &w) {
+                             const Acc &it, GroupWs &w) {
     const uint32_t t0 = tm.t0(), nt = tm.nt();
     for (uint32_t x = t0; x < w.tcap; x += nt) w.tab[x] = 0xFFFF;
     for (uint32_t x = t0; x < n; x += nt) w.cnt[x] = 0;
@@ -632,7 +770,7 @@ __device__ bool group_bucket(const DevPlan &p, const Team &tm, uint32_t b, uint3
     // 1. representatives: hash + full key compare
     bool inc = false;
     for (uint32_t i = t0; i < n; i += nt) {
-        const Item me = load_item(it + i);
+        const Item me = it.load(i);
         inc |= !me.complete();
         uint32_t h = item_hash(me) & (w.tcap - 1), r = i;
         while (true) {
@@ -641,7 +779,7 @@ __device__ bool group_bucket(const DevPlan &p, const Team &tm, uint32_t b, uint3
                 cur = atomicCAS(&w.tab[h], (unsigned short)0xFFFF, (unsigned short)i);
                 if (cur == 0xFFFF) break;  // this item founds the group
             }
-            if (key_eq(load_item(it + cur), me)) {
+            if (key_eq(it.load(cur), me)) {
                 r = cur;
                 break;
             }
@@ -657,25 +795,13 @@ __device__ bool group_bucket(const DevPlan &p, const Team &tm, uint32_t b, uint3
     constexpr bool kWarp = std::is_same<Team, WarpTeam>::value;
     for (uint32_t i = t0; i < n; i += nt) {
         const uint32_t r = w.rep[i];
-        w.mp[w.off[r] + atomicSub(&w.cnt[r], 1u) - 1] = it[i].prob;
+        w.mp[w.off[r] + atomicSub(&w.cnt[r], 1u) - 1] = it.prob(i);
     }
     tm.sync();
     for (uint32_t g = t0; g < G; g += nt) {
         const uint32_t r = w.grp[g];
         const uint32_t o = w.off[r], e = g + 1 < G ? w.off[w.grp[g + 1]] : n;
-        double *v = w.mp + o;
-        for (uint32_t a = o + 1; a < e; a++) {  // insertion sort of the group's probabilities
-            const double x = w.mp[a];
-            uint32_t z = a;
-            while (z > o && w.mp[z - 1] > x) {
-                w.mp[z] = w.mp[z - 1];
-                z--;
-            }
-            w.mp[z] = x;
-        }
-        double acc = 0;
-        for (uint32_t a = o; a < e; a++) acc = merge_prob(acc, w.mp[a]);
-        v[0] = acc;
+        w.mp[o] = fold_sorted(w.mp, o, e);
     }
     tm.sync();
     // 3. groups in canonical order. A warp with at most 32 groups ranks them
@@ -685,7 +811,7 @@ __device__ bool group_bucket(const DevPlan &p, const Team &tm, uint32_t b, uint3
         const uint32_t mine = lane < G ? w.grp[lane] : 0;
         uint32_t rank = 0;
         Item me{};
-        if (lane < G) me = load_item(it + mine);
+        if (lane < G) me = it.load(mine);
         for (uint32_t h = 0; h < G; h++) {  // the others' keys by shuffle (all lanes take part)
             Item o;
             o.k0 = __shfl_sync(0xffffffffu, me.k0, h);
@@ -701,7 +827,7 @@ __device__ bool group_bucket(const DevPlan &p, const Team &tm, uint32_t b, uint3
         while (np < G) np <<= 1;
         auto cas = [&](uint32_t x, uint32_t y) {
             const uint32_t u = w.grp[x], v = w.grp[y];
-            if (key_cmp(load_item(it + v), load_item(it + u)) < 0) {
+            if (key_cmp(it.load(v), it.load(u)) < 0) {
                 w.grp[x] = (uint16_t)v;
                 w.grp[y] = (uint16_t)u;
             }
@@ -725,8 +851,8 @@ __device__ bool group_bucket(const DevPlan &p, const Team &tm, uint32_t b, uint3
     uint32_t nd = 0, no = 0;
     for (uint32_t g = t0; g < G; g += nt) {
         const uint32_t r = w.grp[g];
-        const uint32_t v = key_ndno(load_item(it + r));  // (every key complete here)
-        p.e_item[base + g] = base + r;  // complete key: write_kernel decodes the ids from the item
+        const uint32_t v = key_ndno(it.load(r));  // (every key complete here)
+        p.e_item[base + g] = it.gidx(r);  // complete key: write_kernel decodes the ids from the item
         p.e_prob[base + g] = w.mp[w.off[r]];
         p.e_ndno[base + g] = v;
         nd += v & 0xFFFF;
@@ -785,7 +911,8 @@ __device__ __forceinline__ void bitonic(const DevPlan &p, Item *it, uint32_t n, 
 
 // One CTA, larger buckets (huge_kernel): bitonic sort, then groups.
 template <bool EXACT>
-__device__ void groups_cta(const DevPlan &p, uint32_t b, uint32_t base, uint32_t n, BucketCtx c, const Item *it) {
+__device__ void groups_cta(const DevPlan &p, uint32_t b, uint32_t base, uint32_t flag, uint32_t n, BucketCtx c,
+                           const Item *it) {
     __shared__ uint32_t s_cnt[33], s_ids[2];
     if (threadIdx.x == 0) s_ids[0] = s_ids[1] = 0;
     uint32_t total = 0;
@@ -809,7 +936,7 @@ __device__ void groups_cta(const DevPlan &p, uint32_t b, uint32_t base, uint32_t
         if (start) {
             auto at = [](uint32_t x) -> uint32_t { return x; };
             const uint32_t v =
-                emit_group<EXACT>(p, base, total + s_cnt[w] + __popc(bal & ((1u << lane) - 1)), at, i, n, c);
+                emit_group<EXACT>(p, it, base, flag, total + s_cnt[w] + __popc(bal & ((1u << lane) - 1)), at, i, n, c);
             atomicAdd(&s_ids[0], v & 0xFFFF);
             atomicAdd(&s_ids[1], v >> 16);
         }
@@ -823,7 +950,7 @@ __device__ void groups_cta(const DevPlan &p, uint32_t b, uint32_t base, uint32_t
     __syncthreads();
 }
 
-__device__ void bucket_cta(const DevPlan &p, uint32_t b, uint32_t n, BucketCtx c, Item *it) {
+__device__ void bucket_cta(const DevPlan &p, uint32_t b, uint32_t flag, uint32_t n, BucketCtx c, Item *it) {
     const uint32_t base = p.boff[b].x;
     __shared__ uint32_t s_inc;
     if (threadIdx.x == 0) s_inc = 0;
@@ -833,10 +960,10 @@ __device__ void bucket_cta(const DevPlan &p, uint32_t b, uint32_t n, BucketCtx c
     __syncthreads();
     if (s_inc) {
         bitonic<true>(p, it, n, c, threadIdx.x, blockDim.x, [] { __syncthreads(); });
-        groups_cta<true>(p, b, base, n, c, it);
+        groups_cta<true>(p, b, base, flag, n, c, it);
     } else {
         bitonic<false>(p, it, n, c, threadIdx.x, blockDim.x, [] { __syncthreads(); });
-        groups_cta<false>(p, b, base, n, c, it);
+        groups_cta<false>(p, b, base, flag, n, c, it);
     }
 }
 
@@ -856,7 +983,7 @@ __global__ void __launch_bounds__(kBucketThreads) bucket_kernel(__grid_constant_
     const uint64_t warps = (uint64_t)gridDim.x * (kBucketThreads / 32);
     if (p.hdr->items_overflow) return;  // re-run with a larger item array
     for (uint64_t b = ((uint64_t)blockIdx.x * kBucketThreads + threadIdx.x) >> 5; b < NB; b += warps) {
-        const uint32_t base = p.boff[b].x, n = p.boff[b + 1].x - base;
+        const uint32_t base = p.boff[b].x, n = bucket_size(p, b);
         if (n == 0) {
             if (lane == 0) {
                 p.ecount[b] = 0;
@@ -868,14 +995,16 @@ __global__ void __launch_bounds__(kBucketThreads) bucket_kernel(__grid_constant_
             if (lane == 0) p.huge[atomicAdd(&p.hdr->huge_count, 1u)] = (uint32_t)b;
             continue;
         }
-        const Item *it = items_of(p) + base;
         uint32_t tc = 64;  // hash table: a power of two >= 2n
         while (tc < 2 * n) tc <<= 1;
         w.tcap = tc;
         // an incomplete key: the bucket goes to huge_kernel's exact CTA sort
         // (kept out of this kernel: its comparator's state costs registers)
-        if (!group_bucket(p, WarpTeam{}, (uint32_t)b, base, n, it, w) && lane == 0)
-            p.huge[atomicAdd(&p.hdr->huge_count, 1u)] = (uint32_t)b;
+        const bool ok = p.fused_move ? group_bucket(p, WarpTeam{}, (uint32_t)b, base, n,
+                                                    RunAcc{reinterpret_cast<const Item *>(p.items2) + base, base, kItem2}, w)
+                        : p.fused ? group_bucket(p, WarpTeam{}, (uint32_t)b, base, n, IdxAcc{items_of(p), p.iidx + base}, w)
+                                : group_bucket(p, WarpTeam{}, (uint32_t)b, base, n, RunAcc{items_of(p) + base, base, 0}, w);
+        if (!ok && lane == 0) p.huge[atomicAdd(&p.hdr->huge_count, 1u)] = (uint32_t)b;
     }
 }
 
@@ -890,8 +1019,18 @@ __global__ void __launch_bounds__(256) huge_kernel(__grid_constant__ const DevPl
     __shared__ uint32_t s_inc;
     for (uint32_t i = blockIdx.x; i < nh; i += gridDim.x) {
         const uint32_t b = p.huge[i];
-        const uint32_t base = p.boff[b].x, n = p.boff[b + 1].x - base;
+        const uint32_t base = p.boff[b].x, n = bucket_size(p, b);
         Item *it = items_of(p) + base;
+        uint32_t flag = 0;
+        if (p.fused) {  // gather the bucket's listed items into a run of items2
+            it = reinterpret_cast<Item *>(p.items2) + base;
+            flag = kItem2;
+            if (!p.fused_move) {
+                for (uint32_t x = threadIdx.x; x < n; x += blockDim.x)
+                    store_item(it + x, load_item(items_of(p) + p.iidx[base + x]));
+                __syncthreads();
+            }
+        }
         const BucketCtx c = bucket_ctx(p, b);
         if (threadIdx.x == 0) s_inc = 0;
         __syncthreads();
@@ -903,9 +1042,9 @@ __global__ void __launch_bounds__(256) huge_kernel(__grid_constant__ const DevPl
         if (!s_inc && GroupWs::bytes(n, tc) <= kHugeSmem) {
             GroupWs w;
             w.carve(hsm, n, tc);
-            group_bucket(p, CtaTeam{}, b, base, n, it, w);
+            group_bucket(p, CtaTeam{}, b, base, n, RunAcc{it, base, flag}, w);
         } else {
-            bucket_cta(p, b, n, c, it);
+            bucket_cta(p, b, flag, n, c, it);
         }
         __syncthreads();
     }
@@ -952,7 +1091,7 @@ __global__ void write_kernel(__grid_constant__ const DevPlan p, const uint4 *out
         const uint4 o = p.oscan[b];  // (edges, det ids, obs ids) before this bucket
         const uint32_t base = p.boff[b].x;
         const BucketCtx c = bucket_ctx(p, b);
-        const Item *items = items_of(p);
+        const Item *items = items_of(p), *items2 = reinterpret_cast<const Item *>(p.items2);
         uint32_t dcar = 0, ocar = 0;
         for (uint32_t k0 = 0; k0 < ne; k0 += 32) {
             const uint32_t k = k0 + lane;
@@ -977,7 +1116,8 @@ __global__ void write_kernel(__grid_constant__ const DevPlan p, const uint4 *out
                 p.o_det_off[e] = (uint32_t)(bD + d0);
                 p.o_obs_off[e] = (uint32_t)(bO + o0);
                 p.o_prob[e] = p.e_prob[base + k];
-                const Item q = load_item(items + p.e_item[base + k]);
+                const uint32_t ei = p.e_item[base + k];
+                const Item q = load_item((ei & kItem2 ? items2 : items) + (ei & ~kItem2));
                 uint32_t wd = d0, wo = o0;
                 if (q.complete()) {  // detectors q0 - 1, then the differences; observables by mask
                     if (c.q0) {

@@ -42,7 +42,7 @@ struct StageHdr {  // written by the producer into each stage
 static_assert(sizeof(StageHdr) % 16 == 0, "bulk-copy destinations must stay 16-byte aligned");
 
 struct Dims {
-    uint32_t T, R, NST, n2, ell_w, leaf_w, noise_w, src_w, lay_w, map_w, bkt_w;
+    uint32_t T, R, NST, n2, ell_w, leaf_w, noise_w, src_w, lay_w, map_w, bkt_w, nzb_w;
     __host__ __device__ Dims(uint32_t t, uint32_t r, uint32_t nst, uint32_t max_n, uint32_t max_meas,
                              uint32_t max_noise, uint32_t max_l, uint32_t max_comp = 15, bool fuse_key = false)
         : T(t),
@@ -55,14 +55,15 @@ struct Dims {
           src_w((max_noise + 9) & ~3u),
           lay_w((max_l + 4) & ~3u),
           map_w((max_noise * max_comp + 8) & ~7u),
-          bkt_w(fuse_key ? (64 * t + 4) & ~3u : 0) {}
+          bkt_w(fuse_key ? (64 * t + 4) & ~3u : 0),
+          nzb_w(fuse_key ? ((2 * max_n + 31) / 32 + 3) & ~3u : 0) {}
     __host__ __device__ size_t ring_bytes() const { return (size_t)R * T * n2 * 8; }
     __host__ __device__ size_t stage_bytes() const {
         return sizeof(StageHdr) + (size_t)ell_w * 4 + ((size_t)T * leaf_w + noise_w) * 8 + (size_t)src_w * 4;
     }
     __host__ __device__ size_t total_bytes() const {
         return ring_bytes() + NST * stage_bytes() + (2 * NST + 2 * R) * 8 + (size_t)2 * lay_w * 4 + (size_t)bkt_w * 4 +
-               (size_t)map_w * 2 + 64;
+               (size_t)R * nzb_w * 4 + (size_t)map_w * 2 + 64;
     }
     __device__ uint64_t *slot(uint8_t *base, uint32_t r) const {
         return reinterpret_cast<uint64_t *>(base) + (size_t)r * T * n2;
@@ -87,7 +88,11 @@ struct Dims {
     // per-bucket source counts of the CTA's circuit (fused bucket keys)
     __device__ uint32_t *bkt(uint8_t *base) const { return lay(base) + 2 * lay_w; }
     // layer source -> op (source-major emission)
-    __device__ uint16_t *map(uint8_t *base) const { return reinterpret_cast<uint16_t *>(bkt(base) + bkt_w); }
+    // per state slot: one bit per base row, set when the row is nonzero (fused items)
+    __device__ uint32_t *nzb(uint8_t *base, uint32_t r) const { return bkt(base) + bkt_w + r * nzb_w; }
+    __device__ uint16_t *map(uint8_t *base) const {
+        return reinterpret_cast<uint16_t *>(bkt(base) + bkt_w + R * nzb_w);
+    }
 };
 
 __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
@@ -111,22 +116,70 @@ __device__ __forceinline__ bool named_or(int id, int nthreads, bool pred) {
     return out != 0;
 }
 
-// Fused bucket keys (direct traversal: the CTA owns its circuit's every
-// word): each nonempty source's reduce bucket -- (circuit, first detector),
-// gp_reduce.cuh -- is found here from the words in registers and its slot in
-// the bucket claimed on a shared-memory counter; the CTA publishes the
-// circuit's bucket counts at its end. This is the reduce's key pass
-// (red::key_kernel) without re-reading the records.
+// Fused items (direct traversal: the CTA owns its circuit's every word):
+// each nonempty source's reduce sort item (gp_reduce.cuh) is built here from
+// the words in registers -- the probability from the flips / ptab3 -- and
+// written to the circuit's item region in emission order (warp-aggregated
+// slots: coalesced 32-byte stores) with its circuit-local bucket (first
+// detector + 1). Records are written only for items whose key does not fit
+// (the exact comparator reads them). At its end the CTA lists every bucket's
+// items (boff[b] = {first, count}, iidx). This replaces the reduce's key and
+// scatter passes (red::key_kernel, red::scatter_kernel) and their re-reads.
 struct KeyCtx {
-    uint32_t *sbkt;  // shared per-bucket counters (D + 1), or null: no fusion
-    uint32_t bucket_base, D;
+    uint32_t *sbkt;    // shared per-bucket counters (D + 1), or null: no fusion
+    uint32_t *nitems;  // shared item counter of the circuit
+    uint64_t src_base;
+    uint32_t D;
 };
+
+template <int TM>
+__device__ __forceinline__ void emit_item(const DevPlan &p, uint64_t src, uint32_t tw, const uint64_t (&v)[TM],
+                                          const KeyCtx &kc, double prob) {
+    uint32_t nz = 0;
+#pragma unroll
+    for (int w = 0; w < TM; w++) nz += ((uint32_t)w < tw && v[w] != 0);
+    const uint32_t am = __activemask(), lane = threadIdx.x & 31;
+    const uint32_t want = __ballot_sync(am, nz != 0);
+    if (!want) return;
+    const uint32_t leader = __ffs(want) - 1;
+    uint32_t k = 0;
+    if (lane == leader) k = atomicAdd(kc.nitems, (uint32_t)__popc(want));
+    k = __shfl_sync(am, k, leader) + __popc(want & ((1u << lane) - 1));
+    if (nz == 0) return;
+    uint32_t local;
+    const red::Item it = red::item_of_words<TM>(v, tw, kc.D, prob, (uint32_t)src, p.force_collisions != 0, &local);
+    if (!it.complete()) {  // the exact comparator reads this source's records
+        p.cnt[src] = nz;
+        if (nz > p.K) {
+            atomicMax(&p.hdr->record_overflow, nz);
+        } else {
+            uint32_t j = 0;
+#pragma unroll
+            for (int w = 0; w < TM; w++)
+                if ((uint32_t)w < tw && v[w]) {
+                    p.rbits[rec_at(p, src, j)] = v[w];
+                    p.rtile[rec_at(p, src, j)] = (uint32_t)w;
+                    j++;
+                }
+        }
+    }
+    const uint64_t at = kc.src_base + k;
+    red::store_item(red::items_of(p) + at, it);
+    p.ibkt[at] = (uint16_t)local;
+    atomicAdd(&kc.sbkt[local], 1u);
+}
 
 // Writes one source's sparse signature words. `direct`: this CTA owns every
 // word of the source (T == W), so the signature is written without atomics.
+// Fused items: the source's sort item instead (prob is its probability).
 template <int TM>
 __device__ __forceinline__ void emit_source(const DevPlan &p, uint64_t src, uint32_t t0, uint32_t tw,
-                                            const uint64_t (&v)[TM], bool direct, const KeyCtx &kc) {
+                                            const uint64_t (&v)[TM], bool direct, const KeyCtx &kc,
+                                            double prob = 0.0) {
+    if (kc.sbkt) {
+        emit_item<TM>(p, src, tw, v, kc, prob);
+        return;
+    }
     uint32_t nz = 0;
 #pragma unroll
     for (int w = 0; w < TM; w++) nz += ((uint32_t)w < tw && v[w] != 0);
@@ -137,22 +190,13 @@ __device__ __forceinline__ void emit_source(const DevPlan &p, uint64_t src, uint
         atomicMax(&p.hdr->record_overflow, j + nz);
         return;
     }
-    uint32_t first = 0xFFFFFFFFu;
 #pragma unroll
     for (int w = 0; w < TM; w++)
         if ((uint32_t)w < tw && v[w]) {
             p.rbits[rec_at(p, src, j)] = v[w];
             p.rtile[rec_at(p, src, j)] = t0 + w;
             j++;
-            const uint32_t b0 = (t0 + w) * 64;
-            const uint64_t dm = b0 + 64 <= kc.D ? ~0ull : b0 >= kc.D ? 0 : (1ull << (kc.D - b0)) - 1;
-            if (first == 0xFFFFFFFFu && (v[w] & dm)) first = b0 + (uint32_t)__ffsll((long long)(v[w] & dm)) - 1;
         }
-    if (kc.sbkt) {
-        const uint32_t local = first == 0xFFFFFFFFu ? 0 : first + 1;
-        p.s_bkt[src] = kc.bucket_base + local;
-        p.s_pos[src] = atomicAdd(&kc.sbkt[local], 1u);
-    }
 }
 
 // Warp-cooperative append into the record pool: lane-uniform chunk state,
@@ -322,9 +366,11 @@ __global__ void __launch_bounds__(800, 1) traverse_kernel(__grid_constant__ cons
         uint64_t *z = L.slot(smem, L.R - 1);
         for (uint32_t x = tid; x < L.T * n2; x += blockDim.x) z[x] = 0;
     }
-    const KeyCtx kc{cfg.fuse_key ? L.bkt(smem) : nullptr, m.bucket_base, m.D};
+    __shared__ uint32_t s_nitems;
+    const KeyCtx kc{cfg.fuse_key && p.fused ? L.bkt(smem) : nullptr, &s_nitems, m.src_base, m.D};
     if (kc.sbkt)
         for (uint32_t x = tid; x <= m.D; x += blockDim.x) kc.sbkt[x] = 0;
+    if (tid == 0) s_nitems = 0;
     __syncthreads();
 
     const uint32_t *ell = p.ell + m.ell_base;
@@ -340,7 +386,7 @@ __global__ void __launch_bounds__(800, 1) traverse_kernel(__grid_constant__ cons
             if (j >= (int)L.NST) {  // wait until boundary b + NST released stage k
                 const uint32_t par = (uint32_t)(j / (int)L.NST - 1) & 1u;
                 bool ok = false;
-                while (!(ok = mbar_try_wait(&stage_empty[k], par)))
+                while (!(ok = mbar_try_wait_sleep(&stage_empty[k], par, 2000)))  // (re-checks s_stop)
                     if (b < s_stop) break;
                 if (!ok) break;
             }
@@ -397,18 +443,29 @@ __global__ void __launch_bounds__(800, 1) traverse_kernel(__grid_constant__ cons
             uint64_t *now = L.slot(smem, r);
             const uint32_t mb_al = h->mb & ~1u;  // leaf rows are 16-byte aligned: the slice starts there
             bool any = false;
-            for (uint32_t s = tn; s < ((cfg.debug & 2) ? 0 : n2); s += node_threads) {
-                const uint32_t e = s_ell[s];
-                const uint32_t idx = e & kSuccIdx;
+            uint32_t *nzb = kc.sbkt ? L.nzb(smem, r) : nullptr;
+            // (warp-uniform trip count: the row bitmap is a ballot per 32 rows)
+            for (uint32_t s0 = tn - lane; s0 < ((cfg.debug & 2) ? 0 : n2); s0 += node_threads) {
+                const uint32_t s = s0 + lane;
+                bool row = false;
+                if (s < n2) {
+                    const uint32_t e = s_ell[s];
+                    const uint32_t idx = e & kSuccIdx;
 #pragma unroll
-                for (int w = 0; w < TM; w++) {
-                    if ((uint32_t)w >= tw) break;
-                    const uint64_t *nw = nxt + (size_t)w * n2;
-                    const uint64_t *lw = s_leaf + (size_t)w * L.leaf_w - mb_al;
-                    uint64_t acc = (e & kSuccNotSelf) ? 0 : nw[s];
-                    if (e & kSuccOther) acc ^= (e & kSuccLeaf) ? lw[idx] : nw[idx];
-                    now[(size_t)w * n2 + s] = acc;
-                    any |= acc != 0;
+                    for (int w = 0; w < TM; w++) {
+                        if ((uint32_t)w >= tw) break;
+                        const uint64_t *nw = nxt + (size_t)w * n2;
+                        const uint64_t *lw = s_leaf + (size_t)w * L.leaf_w - mb_al;
+                        uint64_t acc = (e & kSuccNotSelf) ? 0 : nw[s];
+                        if (e & kSuccOther) acc ^= (e & kSuccLeaf) ? lw[idx] : nw[idx];
+                        now[(size_t)w * n2 + s] = acc;
+                        row |= acc != 0;
+                    }
+                }
+                any |= row;
+                if (nzb) {
+                    const uint32_t bits = __ballot_sync(0xffffffffu, row);
+                    if (lane == 0) nzb[s0 >> 5] = bits;
                 }
             }
             const bool live = named_or(kBarNode, (int)node_threads, any);
@@ -432,7 +489,7 @@ __global__ void __launch_bounds__(800, 1) traverse_kernel(__grid_constant__ cons
                 uint64_t v[TM];
 #pragma unroll
                 for (int w = 0; w < TM; w++) v[w] = (uint32_t)w < tw ? leaf[(uint64_t)(t0 + w) * leaf_stride(m.M) + mm] : 0;
-                emit_source<TM>(p, src_flip + mm, t0, tw, v, direct, kc);
+                emit_source<TM>(p, src_flip + mm, t0, tw, v, direct, kc, flip[mm]);
             }
         }
         constexpr uint8_t kMask[15] = {4, 8, 1, 5, 2, 10, 12, 9, 3, 6, 13, 7, 15, 11, 14};
@@ -472,8 +529,14 @@ __global__ void __launch_bounds__(800, 1) traverse_kernel(__grid_constant__ cons
                     const uint64_t wd = s_noise[lo];
                     const uint32_t kind = noise_kind(wd), c = ls - s_src[lo];
                     const uint32_t q0 = noise_q0(wd), q1 = noise_q1(wd);
-                    const uint32_t mk = kind == 0 ? 1u : kind == 1 ? 2u : kind == 2 ? (c == 0 ? 1u : c == 1 ? 2u : 3u)
-                                                                                    : (uint32_t)kMask[c];
+                    uint32_t mk = kind == 0 ? 1u : kind == 1 ? 2u : kind == 2 ? (c == 0 ? 1u : c == 1 ? 2u : 3u)
+                                                                              : (uint32_t)kMask[c];
+                    if (kc.sbkt) {  // rows known to be zero are not read (most sources are empty)
+                        const uint32_t *nzb = L.nzb(smem, r);
+                        const uint32_t r0 = 2 * q0, r1 = 2 * q1;
+                        const uint32_t b0 = nzb[r0 >> 5] >> (r0 & 31), b1 = kind == 3 ? nzb[r1 >> 5] >> (r1 & 31) : 0u;
+                        mk &= (b0 & 3u) | (b1 & 3u) << 2;
+                    }
                     uint64_t v[TM];
 #pragma unroll
                     for (int w = 0; w < TM; w++) {
@@ -487,7 +550,11 @@ __global__ void __launch_bounds__(800, 1) traverse_kernel(__grid_constant__ cons
                         }
                         v[w] = x;
                     }
-                    emit_source<TM>(p, m.src_base + ls, t0, tw, v, direct, kc);
+                    double pr = 0.0;
+                    if (kc.sbkt)
+                        pr = p.tot.wide_prob ? p.prob[m.src_base + ls]
+                                             : p.ptab3[4 * noise_pidx(wd) + (kind == 2 ? 1 : kind == 3 ? 2 : 0)];
+                    emit_source<TM>(p, m.src_base + ls, t0, tw, v, direct, kc, pr);
                 }
             } else
             // Warp-uniform trip count (the pool path needs whole-warp rounds).
@@ -584,8 +651,38 @@ __global__ void __launch_bounds__(800, 1) traverse_kernel(__grid_constant__ cons
         pool_close(p, pw, lane);
     }
     __syncthreads();
-    if (kc.sbkt)  // the circuit's bucket counts (the CTA owns all of them)
-        for (uint32_t x = tid; x <= m.D; x += blockDim.x) p.bcount[m.bucket_base + x] = kc.sbkt[x];
+    if (kc.sbkt && !(cfg.debug & 8)) {  // list the circuit's buckets (the CTA owns all of them)
+        const uint32_t nb = m.D + 1, ni = s_nitems;
+        if (warp == 0) {  // exclusive scan of the counts, in place; boff = {first, count}
+            uint32_t carry = 0;
+            for (uint32_t x0 = 0; x0 < nb; x0 += 32) {
+                const uint32_t x = x0 + lane;
+                const uint32_t c = x < nb ? kc.sbkt[x] : 0;
+                uint32_t inc = c;
+#pragma unroll
+                for (int d = 1; d < 32; d <<= 1) {
+                    const uint32_t o = __shfl_up_sync(0xffffffffu, inc, d);
+                    if (lane >= (uint32_t)d) inc += o;
+                }
+                const uint32_t off = carry + inc - c;
+                if (x < nb) {
+                    kc.sbkt[x] = off;
+                    p.boff[m.bucket_base + x] = make_uint4((uint32_t)(m.src_base + off), c, 0, 0);
+                }
+                carry += __shfl_sync(0xffffffffu, inc, 31);
+            }
+        }
+        __syncthreads();
+        for (uint32_t k = tid; k < ni; k += blockDim.x) {
+            const uint64_t at = m.src_base + k;
+            const uint32_t pos = atomicAdd(&kc.sbkt[p.ibkt[at]], 1u);
+            if (p.fused_move)
+                red::store_item(reinterpret_cast<red::Item *>(p.items2) + m.src_base + pos,
+                                red::load_item(red::items_of(p) + at));
+            else
+                p.iidx[m.src_base + pos] = (uint32_t)at;
+        }
+    }
     // Drain bulk copies staged below the stopping boundary (never consumed;
     // each is the latest use of its stage, so its phase parity is unambiguous).
     if (tid == 0)
