@@ -447,6 +447,28 @@ def run_gpu(args, dist):
     parity = branch_parity(compiler, out, first, B, dist) if args.level == 0 else None
     e2e_h2d, e2e_d2h = int(stats["h2d_bytes"]), int(stats["d2h_bytes"])
 
+    # --- device-generated branches: seeds in, DEM out ------
+    # gp_compile_bb_branches builds the same branch circuits on the GPU from
+    # (seed, branch id): no host circuits, packing or circuit upload; the
+    # timed step ends with the batch DEM in host memory, as e2e's does.
+    device_gen = None
+    if args.level == 0:
+        spec = gp.bb72_branch_spec()
+        for _ in range(args.warmup):
+            out_g, st_g = compiler.compile_bb_branches_raw(spec, first, B, 0)
+        dist.barrier()
+        g0 = time.perf_counter()
+        for _ in range(args.steps):
+            out_g, st_g = compiler.compile_bb_branches_raw(spec, first, B, 0)
+        g1 = time.perf_counter()
+        dist.barrier()
+        gen_s = dist.max(g1 - g0)
+        device_gen = {"value": total_edges * args.steps / gen_s, "unit": UNIT, "ms_per_step": gen_s / args.steps * 1e3,
+                      "h2d_bytes_per_step": int(st_g["h2d_bytes"]), "d2h_bytes_per_step": int(st_g["d2h_bytes"]),
+                      "parity": branch_parity(compiler, out_g, first, B, dist),
+                      "how": "gp_compile_bb_branches(spec, first branch, count): check subsets drawn and the "
+                             "circuits written on the GPU, then the same pipeline; wall time per call, host DEM out"}
+
     # --- optional final gather of per-rank DEM tables over NCCL -------------
     gather = None
     if ws > 1:
@@ -517,6 +539,7 @@ def run_gpu(args, dist):
                 "ms_per_step": e2e_s / args.steps * 1e3, "breakdown": e2e_parts},
         "parity": parity,
         "parity_value_path": parity_value_path,
+        "device_generated": device_gen,
         "gpu_launches": launches_per_step * args.steps,
         "gather": gather,
         "roofline": roofline,

@@ -155,6 +155,29 @@ gp_status gp_compile(gp_ctx *ctx, const gp_circuit_view *circuit, uint8_t level,
 gp_status gp_compile_batch(gp_ctx *ctx, const gp_circuit_view *circuits, size_t count,
                            uint8_t level, gp_dem_batch_view *out, gp_stats *stats);
 
+/* Branch batches generated on the device (the seeds-in /
+ * DEM-out mode of the adaptive workload, adaptive.cpp:382-391): circuit c is
+ * the BB memory circuit gp_gen_bb(spec..., branch = first_branch + c) --
+ * identical gates, noise, detectors and observables -- but it is built
+ * straight into device memory from (seed, branch id): the check subsets are
+ * drawn on the GPU (mt19937_64 / seed_seq / uniform_real_distribution
+ * restated bit for bit, gp_rng.h) and the upload image is written there, so
+ * no host circuit, packing or circuit upload exists. The result equals
+ * gp_compile_batch over the host-generated circuits. */
+typedef struct gp_bb_spec {
+    uint32_t l, m;       /* torus; A = x^a0 + y^a1 + y^a2, B = y^b0 + x^b1 + x^b2 */
+    uint32_t a[3], b[3];
+    uint32_t rounds;
+    uint32_t refresh;    /* full rounds: 0, the last, every refresh-th (0: rounds / 2) */
+    int32_t noise_model; /* GP_NOISE_MODEL_* */
+    uint32_t reserved;
+    double p;
+    double check_prob;   /* non-full rounds keep each check with this probability */
+    uint64_t seed;
+} gp_bb_spec;
+gp_status gp_compile_bb_branches(gp_ctx *ctx, const gp_bb_spec *spec, uint64_t first_branch, size_t count,
+                                 uint8_t level, gp_dem_batch_view *out, gp_stats *stats);
+
 /* Fault-range sharding of ONE circuit: shard k of n owns the
  * error sources placed in layers [l*k/n, l*(k+1)/n) -- noise ops of those
  * layers and the outcome flips of their measurements. gp_compile_shard walks

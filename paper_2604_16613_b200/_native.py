@@ -63,6 +63,12 @@ class Metrics(C.Structure):
                                           "measurements")]
 
 
+class BBSpec(C.Structure):  # gp_bb_spec
+    _fields_ = [("l", C.c_uint32), ("m", C.c_uint32), ("a", C.c_uint32 * 3), ("b", C.c_uint32 * 3),
+                ("rounds", C.c_uint32), ("refresh", C.c_uint32), ("noise_model", C.c_int32),
+                ("reserved", C.c_uint32), ("p", C.c_double), ("check_prob", C.c_double), ("seed", C.c_uint64)]
+
+
 class Stats(C.Structure):
     _fields_ = [(n, C.c_uint64) for n in (
         "lower_ns", "traverse_ns", "reduce_ns", "total_ns", "h2d_ns", "kernel_ns", "d2h_ns",
@@ -91,6 +97,8 @@ def lib() -> C.CDLL:
         L.gp_compile.argtypes = [vp, C.POINTER(CircuitView), C.c_uint8, C.POINTER(DemView), C.POINTER(Stats)]
         L.gp_compile_batch.argtypes = [vp, C.POINTER(CircuitView), C.c_size_t, C.c_uint8,
                                        C.POINTER(DemBatchView), C.POINTER(Stats)]
+        L.gp_compile_bb_branches.argtypes = [vp, C.POINTER(BBSpec), C.c_uint64, C.c_size_t, C.c_uint8,
+                                             C.POINTER(DemBatchView), C.POINTER(Stats)]
         L.gp_compile_shard.argtypes = [vp, C.POINTER(CircuitView), C.c_uint8, C.c_uint32, C.c_uint32,
                                        C.c_uint32, C.POINTER(PartialView), C.POINTER(Stats)]
         L.gp_merge_partials.argtypes = [vp, C.POINTER(PartialView), C.c_size_t, C.POINTER(DemView),

@@ -280,6 +280,17 @@ class Compiler:
         self.last_stats = st.as_dict()
         return out, self.last_stats
 
+    def compile_bb_branches_raw(self, spec: "N.BBSpec", first: int, count: int,
+                                level=CorrelationLevel.L0):
+        """Branch circuits generated on the device (gp_compile_bb_branches):
+        seeds in, batch DEM out; returns (DemBatchView, stats)."""
+        out = N.DemBatchView()
+        st = N.Stats()
+        self._check(self._lib.gp_compile_bb_branches(self._ctx, C.byref(spec), first, count, int(level),
+                                                     C.byref(out), C.byref(st)))
+        self.last_stats = st.as_dict()
+        return out, self.last_stats
+
     @staticmethod
     def batch_digests(out) -> np.ndarray:
         """Per-circuit gp_dem_digest of a DemBatchView (host threads)."""
@@ -426,6 +437,20 @@ def gen_bb(l: int, m: int, a=(3, 1, 2), b=(3, 1, 2), rounds: int = 12, p: float 
 def gen_bb144(rounds: int = 12, p: float = 1e-3, noise_model: int = NOISE_MODEL_UNIFORM) -> GenCircuit:
     """Gross code [[144,12,12]]: A = x^3 + y + y^2, B = y^3 + x + x^2, (l, m) = (12, 6)."""
     return gen_bb(12, 6, rounds=rounds, p=p, noise_model=noise_model)
+
+
+def bb_spec(l: int, m: int, a=(3, 1, 2), b=(3, 1, 2), rounds: int = 12, p: float = 1e-3,
+            noise_model: int = NOISE_MODEL_UNIFORM, check_prob: float = 1.0, refresh: int = 0,
+            seed: int = 1) -> "N.BBSpec":
+    """gp_bb_spec of gen_bb's circuits (for Compiler.compile_bb_branches_raw)."""
+    return N.BBSpec(l, m, (C.c_uint32 * 3)(*a), (C.c_uint32 * 3)(*b), rounds, refresh, noise_model, 0, p,
+                    check_prob, seed)
+
+
+def bb72_branch_spec(rounds: int = 6, p: float = 1e-3, check_prob: float = 0.5, seed: int = 1) -> "N.BBSpec":
+    """gp_bb_spec of gen_bb72_branch."""
+    return bb_spec(6, 6, rounds=rounds, p=p, noise_model=NOISE_MODEL_PAPER, check_prob=check_prob,
+                   refresh=max(1, rounds // 2), seed=seed)
 
 
 def gen_bb72_branch(branch: int, rounds: int = 6, p: float = 1e-3, check_prob: float = 0.5,

@@ -24,6 +24,7 @@
 #include "../../include/greenpeas.h"
 #include "gp_device.h"
 #include "gp_layout.h"
+#include "gp_gen.h"
 #include "gp_pack.h"
 
 using gp::BatchTotals;
@@ -88,6 +89,20 @@ struct gp_ctx {
         bool used = false;  // the last compile ran as the graph (no per-stage events)
     } graph;
     gp::PipeState *pipe = nullptr;
+    // Device branch generation (gp_compile_bb_branches): the spec's template
+    // (host + device copies), per-branch check masks and counts.
+    struct {
+        gp_bb_spec spec{};
+        bool valid = false;
+        gp::BBTemplate t;
+        uint32_t *d_tmpl = nullptr;  // xdata | zdata | zfinal | obs_off | obs_q
+        size_t d_tmpl_cap = 0;
+        uint64_t *d_masks = nullptr;
+        size_t d_masks_cap = 0;
+        uint32_t *d_counts = nullptr, *h_counts = nullptr, *d_err = nullptr, *h_err = nullptr;
+        size_t counts_cap = 0;
+    } bb;
+    uint32_t bb_pi[5] = {};  // probability-table index per generator channel (last plan)
 };
 
 namespace {
@@ -378,9 +393,18 @@ struct PartialOut {
     uint64_t *bits = nullptr;
 };
 
+// Device-generated batch (gp_compile_bb_branches): the branches' first id.
+struct BBGenReq {
+    uint64_t first;
+};
+gp_status bbgen_draw(gp_ctx *ctx, const BBGenReq &req, size_t count, uint8_t level);
+gp_status bbgen_plan(gp_ctx *ctx, size_t c0, size_t count, uint8_t level, gp::PackPlan &pp, uint32_t *pi_out);
+gp_status bbgen_fill(gp_ctx *ctx, const BBGenReq &req, size_t c0, uint8_t level, const gp::PackPlan &pp,
+                     const uint32_t *pi, uint8_t *img, cudaStream_t st);
+
 gp_status run_batch(gp_ctx *ctx, const gp_circuit_view *cs, size_t count, uint8_t level, HostOut &ho,
                     DeviceHeader &hdr, gp_stats *stats, uint32_t mode = gp::kModeFull, uint32_t sh_lo = 0,
-                    uint32_t sh_hi = 0xFFFFFFFFu, PartialOut *part = nullptr) {
+                    uint32_t sh_hi = 0xFFFFFFFFu, PartialOut *part = nullptr, const BBGenReq *gen = nullptr) {
     const auto t0 = clk::now();
     if (level > 2) return fail(ctx, GP_ERR_INVALID_ARGUMENT, "correlation level must be 0, 1 or 2");
     if (cudaSetDevice(ctx->device) != cudaSuccess) return fail(ctx, GP_ERR_CUDA, "cudaSetDevice failed");
@@ -388,13 +412,28 @@ gp_status run_batch(gp_ctx *ctx, const gp_circuit_view *cs, size_t count, uint8_
     gp::PackPlan &pp = ctx->pack;
     // Host pool for large jobs (single large circuits pack on every core too).
     uint64_t ops = 0;
-    for (size_t c = 0; c < count; c++)
+    for (size_t c = 0; !gen && c < count; c++)
         ops += (uint64_t)(cs[c].gate_offsets[cs[c].num_layers] - cs[c].gate_offsets[0]) +
                (cs[c].noise_offsets[cs[c].num_layers] - cs[c].noise_offsets[0]);
     PoolLease lease(ops >= (1u << 14));
     gp::HostPool *hpool = lease.pool;
     pp.force_wide = false;
     pp.no_narrow = false;
+    cudaError_t e = cudaSuccess;
+    const std::vector<CircuitMeta> &M = pp.metas;
+    const size_t nchunk = gen ? 1 : count >= 1024 ? 8 : count >= 256 ? 4 : 1;
+    auto slice = [&](uint64_t off, uint64_t elem, uint64_t lo, uint64_t hi) {
+        if (hi > lo && e == cudaSuccess)
+            e = cudaMemcpyAsync(ctx->d_img + off + lo * elem, ctx->h_stage + off + lo * elem, (hi - lo) * elem,
+                                cudaMemcpyHostToDevice, ctx->stream);
+    };
+    if (gen) {  // device generation: plan the image from the drawn counts (no host circuits)
+        cudaEventRecord(ctx->ev_start, ctx->stream);
+        if ((st = bbgen_draw(ctx, *gen, count, level)) != GP_OK) return st;
+        if ((st = bbgen_plan(ctx, 0, count, level, pp, ctx->bb_pi)) != GP_OK) return st;
+        if ((st = ensure_host(ctx, &ctx->h_stage, &ctx->h_stage_cap, pp.L.total)) != GP_OK) return st;
+        if ((st = ensure_device(ctx, &ctx->d_img, &ctx->d_img_cap, pp.L.total)) != GP_OK) return st;
+    } else {
 repack:  // (again with per-op probabilities when the table overflowed)
     gp::pack_plan(hpool, cs, count, level, pp);
     if (pp.err == gp::kPackIndexSpace || pp.err == gp::kPackTooWide) {
@@ -410,15 +449,7 @@ repack:  // (again with per-op probabilities when the table overflowed)
     // Pack in circuit chunks; each chunk's slice of every section is copied
     // while the next chunk is packed (the image is circuit-major per section).
     // One chunk (one copy of the whole image) for single circuits.
-    cudaError_t e = cudaSuccess;
     cudaEventRecord(ctx->ev_start, ctx->stream);
-    const std::vector<CircuitMeta> &M = pp.metas;
-    const size_t nchunk = count >= 1024 ? 8 : count >= 256 ? 4 : 1;
-    auto slice = [&](uint64_t off, uint64_t elem, uint64_t lo, uint64_t hi) {
-        if (hi > lo && e == cudaSuccess)
-            e = cudaMemcpyAsync(ctx->d_img + off + lo * elem, ctx->h_stage + off + lo * elem, (hi - lo) * elem,
-                                cudaMemcpyHostToDevice, ctx->stream);
-    };
     for (size_t k = 0; k < nchunk; k++) {
         const size_t c0 = count * k / nchunk, c1 = count * (k + 1) / nchunk;
         if (c1 == c0) continue;
@@ -447,6 +478,8 @@ repack:  // (again with per-op probabilities when the table overflowed)
         goto repack;
     }
     gp::pack_finish(pp, ctx->h_stage);
+    }  // (host packing)
+    const StageLayout &L = pp.L;
     BatchTotals t = pp.t;
     if (t.sources >= 0xFFFFFFFFull || t.tiles >= 0xFFFFFFFFull || t.gates >= 0xFFFFFFFFull ||
         t.noise >= 0xFFFFFFFFull || t.meas >= 0xFFFFFFFFull || t.layer_slots >= 0xFFFFFFFFull)
@@ -460,7 +493,13 @@ repack:  // (again with per-op probabilities when the table overflowed)
     t.groups = 0;
     for (const CircuitMeta &m : M) t.groups += (m.W + tcfg.T - 1) / tcfg.T;
     gp::pack_head(pp, tcfg.T, ctx->h_stage);
-    if (nchunk == 1) {
+    if (gen) {  // the head (metas, cumulative tables) and the probability table; the rest on the device
+        slice(0, 1, 0, L.lay_gate);
+        slice(L.prob_table, 8, 0, t.prob_table_n);
+        if (e == cudaSuccess && (st = bbgen_fill(ctx, *gen, 0, level, pp, ctx->bb_pi, ctx->d_img, ctx->stream)) != GP_OK)
+            return st;
+        cudaMemcpyAsync(ctx->bb.h_err, ctx->bb.d_err, 4, cudaMemcpyDeviceToHost, ctx->stream);
+    } else if (nchunk == 1) {
         slice(0, 1, 0, pp.image_bytes());  // the whole image in one copy
     } else {
         slice(L.lay_meas, 4, 0, t.layer_slots);  // finished prefix tables
@@ -598,7 +637,7 @@ repack:  // (again with per-op probabilities when the table overflowed)
         if (stats) {
             *stats = gp_stats{};
             stats->num_sources = t.sources;
-            stats->h2d_bytes = pp.image_bytes();
+            stats->h2d_bytes = gen ? L.lay_gate + (uint64_t)t.prob_table_n * 8 : pp.image_bytes();
             stats->kernel_ns = (uint64_t)(elapsed_ms(ctx->ev_h2d, ctx->ev_end) * 1e6);
             stats->kernel_launches = (uint64_t)launches;
         }
@@ -662,7 +701,7 @@ repack:  // (again with per-op probabilities when the table overflowed)
             stats->kernel_ns = (uint64_t)((low + trav + red) * 1e6);  // includes the mapped-output copy
             stats->d2h_ns = (uint64_t)(out_ms * 1e6);
             stats->num_sources = t.sources;
-            stats->h2d_bytes = pp.image_bytes();
+            stats->h2d_bytes = gen ? L.lay_gate + (uint64_t)t.prob_table_n * 8 : pp.image_bytes();
             stats->d2h_bytes = sizeof(DeviceHeader) + (E + 1) * 8 + E * 8 + (nd + no) * 4 + (count + 1) * 8;
             stats->kernel_launches = (uint64_t)launches;
             stats->total_ns = ns_since(t0);
@@ -714,12 +753,214 @@ repack:  // (again with per-op probabilities when the table overflowed)
         stats->kernel_ns = (uint64_t)((low + trav + red) * 1e6);
         stats->d2h_ns = (uint64_t)(d2h_ms * 1e6);
         stats->num_sources = t.sources;
-        stats->h2d_bytes = pp.image_bytes();
+        stats->h2d_bytes = gen ? L.lay_gate + (uint64_t)t.prob_table_n * 8 : pp.image_bytes();
         stats->d2h_bytes = sizeof(DeviceHeader) + o;
         stats->kernel_launches = (uint64_t)launches;
         stats->total_ns = ns_since(t0);
     }
     return GP_OK;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------- device-generated branches
+// gp_compile_bb_branches: the check subsets are drawn on the device, the host
+// plans the image from the drawn counts (gp_gen.h bb_layer_count: the same
+// offsets pack_plan / pack_finish would give the host-generated circuits),
+// uploads only the image head, and the fill kernel writes the rest.
+
+namespace {
+
+gp_status bbgen_params(gp_ctx *ctx, const BBGenReq &req, size_t count, uint8_t level, gp::BBGenParams &g) {
+    auto &bb = ctx->bb;
+    const gp::BBTemplate &T = bb.t;
+    g = gp::BBGenParams{};
+    const uint32_t lm = T.lm;
+    g.xdata = bb.d_tmpl;
+    g.zdata = g.xdata + 7 * lm;
+    g.zfinal = g.zdata + 7 * lm;
+    g.obs_off = g.zfinal + 6 * lm;
+    g.obs_q = g.obs_off + T.O + 1;
+    g.lm = lm;
+    g.nd = T.nd;
+    g.n = T.n;
+    g.rounds = T.rounds;
+    g.refresh = T.refresh;
+    g.O = T.O;
+    g.MW = (lm + 63) / 64;
+    g.level = level;
+    g.C = (uint32_t)count;
+    g.check_prob = T.check_prob;
+    g.pm = T.pm;
+    g.seed = T.seed;
+    g.first = req.first;
+    const size_t masks = count * T.rounds * 2 * g.MW * 8, counts = count * T.rounds * 4;
+    gp_status st;
+    if ((st = ensure_device(ctx, reinterpret_cast<uint8_t **>(&bb.d_masks), &bb.d_masks_cap, masks)) != GP_OK) return st;
+    if (bb.counts_cap < counts) {
+        if (bb.d_counts) cudaFree(bb.d_counts);
+        if (bb.h_counts) cudaFreeHost(bb.h_counts);
+        bb.d_counts = bb.h_counts = nullptr;
+        bb.counts_cap = 0;
+        if (cudaMalloc(&bb.d_counts, counts + counts / 4) != cudaSuccess ||
+            cudaMallocHost(&bb.h_counts, counts + counts / 4) != cudaSuccess) {
+            cudaGetLastError();
+            return fail(ctx, GP_ERR_OUT_OF_MEMORY, "branch count buffers");
+        }
+        bb.counts_cap = counts + counts / 4;
+    }
+    if (!bb.d_err) {
+        if (cudaMalloc(&bb.d_err, 16) != cudaSuccess || cudaMallocHost(&bb.h_err, 16) != cudaSuccess) {
+            cudaGetLastError();
+            return fail(ctx, GP_ERR_OUT_OF_MEMORY, "generator status");
+        }
+    }
+    g.masks = bb.d_masks;
+    g.counts = bb.d_counts;
+    g.err = bb.d_err;
+    return GP_OK;
+}
+
+// Draws every branch's check subsets (masks and counts stay on the device;
+// the counts also come back to the host for planning).
+gp_status bbgen_draw(gp_ctx *ctx, const BBGenReq &req, size_t count, uint8_t level) {
+    auto &bb = ctx->bb;
+    gp::BBGenParams g;
+    gp_status st = bbgen_params(ctx, req, count, level, g);
+    if (st != GP_OK) return st;
+    cudaMemsetAsync(bb.d_err, 0, 4, ctx->stream);
+    gp::launch_bbgen_draw(g, ctx->stream);
+    cudaError_t e = cudaMemcpyAsync(bb.h_counts, bb.d_counts, count * bb.t.rounds * 4, cudaMemcpyDeviceToHost,
+                                    ctx->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+    return e == cudaSuccess ? GP_OK : cuda_fail(ctx, e, "branch draws");
+}
+
+// Image plan of branches [c0, c0 + count) of the drawn batch (host only).
+gp_status bbgen_plan(gp_ctx *ctx, size_t c0, size_t count, uint8_t level, gp::PackPlan &pp, uint32_t *pi_out) {
+    auto &bb = ctx->bb;
+    const gp::BBTemplate &T = bb.t;
+    // probability table (channel -> index; identical values share one entry)
+    pp.prob_table.clear();
+    auto index = [&](double v) {
+        for (size_t i = 0; i < pp.prob_table.size(); i++)
+            if (std::memcmp(&pp.prob_table[i], &v, 8) == 0) return (uint32_t)i;
+        pp.prob_table.push_back(v);
+        return (uint32_t)pp.prob_table.size() - 1;
+    };
+    const double ch[5] = {T.p1, T.p2, T.pr, T.pidle, T.pidle_mr};
+    gp::BBCountParams q{T.n, T.nd, T.lm, T.rounds, 0, level ? 3u : 2u, level == 0 ? 6u : level == 1 ? 10u : 15u};
+    for (int x = 0; x < 5; x++)
+        if (ch[x] > 0) q.on |= 1u << x;
+    BatchTotals &t = pp.t;
+    t = BatchTotals{};
+    t.C = (uint32_t)count;
+    t.level = level;
+    pp.metas.assign(count, CircuitMeta{});
+    const uint32_t l = 2 + 9 * T.rounds, O = T.O, obs_entries = T.obs_off[O];
+    for (size_t c = 0; c < count; c++) {  // pack_plan + pack_finish, from the counts
+        CircuitMeta &m = pp.metas[c];
+        const uint32_t *cnt = bb.h_counts + (c0 + c) * T.rounds;
+        uint64_t gates = 0, noise = 0, meas = 0, src = 0;
+        uint32_t max_noise = 0, max_meas = 0, D = T.lm, de = 7 * T.lm;
+        for (uint32_t li = 0; li < l; li++) {
+            const uint32_t r = li == 0 ? 0 : std::min((li - 1) / 9, T.rounds - 1);
+            const uint32_t ne = cnt[r] & 0xFFFF, nz = cnt[r] >> 16;
+            const gp::BBLayerCount lc = gp::bb_layer_count(q, li, ne, nz);
+            gates += lc.gates;
+            noise += lc.noise;
+            meas += lc.meas;
+            src += lc.src;
+            max_noise = std::max(max_noise, lc.noise);
+            max_meas = std::max(max_meas, lc.meas);
+        }
+        for (uint32_t r = 0; r < T.rounds; r++) {  // DetectorTracker: Z from the first round, X from the second
+            const uint32_t ne = cnt[r] & 0xFFFF, nz = cnt[r] >> 16;
+            D += nz + (r ? ne : 0);
+            de += (r ? 2 : 1) * nz + (r ? 2 * ne : 0);
+        }
+        if ((uint64_t)l * (level == 0 ? 2 : level == 1 ? 4 : 7) * T.n + meas >= 0xFFFFFFFFull)
+            return fail(ctx, GP_ERR_INVALID_ARGUMENT, "circuit exceeds 32-bit node index space");
+        m.n = T.n;
+        m.l = l;
+        m.M = (uint32_t)meas;
+        m.D = D;
+        m.O = O;
+        m.W = (uint32_t)(((uint64_t)D + O + 63) / 64);
+        m.layer_base = (uint32_t)t.layer_slots;
+        m.meas_base = (uint32_t)t.meas;
+        m.det_base = (uint32_t)t.det_slots;
+        m.obs_base = (uint32_t)t.obs_slots;
+        m.tile_base = (uint32_t)t.tiles;
+        m.bucket_base = (uint32_t)t.buckets;
+        m.ell_base = t.ell;
+        m.leaf_base = t.leaf;
+        m.gate_base = t.gates;
+        m.noise_base = t.noise;
+        m.det_entry_base = t.det_entries;
+        m.obs_entry_base = t.obs_entries;
+        m.circ_layer_base = t.layers;
+        m.src_noise = (uint32_t)src;
+        m.max_layer_noise = max_noise;
+        m.src_base = t.sources;
+        t.sources += src + m.M;
+        t.max_n = std::max(t.max_n, m.n);
+        t.max_W = std::max(t.max_W, m.W);
+        t.max_l = std::max(t.max_l, m.l);
+        t.max_layer_noise = std::max(t.max_layer_noise, max_noise);
+        t.max_layer_meas = std::max(t.max_layer_meas, max_meas);
+        t.layers += l;
+        t.layer_slots += l + 1;
+        t.gates += gates;
+        t.noise += noise;
+        t.meas += m.M;
+        t.det_slots += D + 1;
+        t.det_entries += de;
+        t.obs_slots += O + 1;
+        t.obs_entries += obs_entries;
+        t.dets += D;
+        t.obss += O;
+        t.tiles += m.W;
+        t.ell += (uint64_t)(l - 1) * gp::ell_stride(m.n);
+        t.leaf += (uint64_t)m.W * gp::leaf_stride(m.M);
+        t.buckets += (uint64_t)D + 1;
+    }
+    uint32_t pi[5];
+    for (int x = 0; x < 5; x++) pi[x] = ch[x] > 0 ? index(ch[x]) : 0xFFFFFFFFu;
+    std::memcpy(pi_out, pi, sizeof pi);
+    uint32_t max_m = 0;
+    for (const CircuitMeta &m : pp.metas) max_m = std::max(max_m, m.M);
+    if (T.n > gp::kNarrowMaxQubits || max_m > gp::kNarrowMaxMeas || pp.prob_table.size() > gp::kNarrowMaxProbs)
+        return fail(ctx, GP_ERR_UNSUPPORTED, "device-generated branches need narrow words (<= 4096 qubits, 32768 measurements)");
+    t.wide_prob = 0;
+    t.narrow = 1;
+    t.prob_table_n = (uint32_t)pp.prob_table.size();
+    pp.L = gp::stage_layout(t);
+    pp.err = gp::kPackOk;
+    return GP_OK;
+}
+
+// Writes branches [c0, c0 + pp.t.C) into the device image img on stream st
+// (its head -- metas, cumulative tables, probability table -- uploaded first).
+gp_status bbgen_fill(gp_ctx *ctx, const BBGenReq &req, size_t c0, uint8_t level, const gp::PackPlan &pp,
+                     const uint32_t *pi, uint8_t *img, cudaStream_t st) {
+    const gp::BBTemplate &T = ctx->bb.t;
+    gp::BBGenParams g;
+    const gp_status s = bbgen_params(ctx, req, 0, level, g);  // (buffers exist: bbgen_draw sized them)
+    if (s != GP_OK) return s;
+    const uint64_t MW = (T.lm + 63) / 64;
+    g.C = pp.t.C;
+    g.first = req.first + c0;
+    g.masks = ctx->bb.d_masks + c0 * T.rounds * 2 * MW;
+    g.counts = ctx->bb.d_counts + c0 * T.rounds;
+    std::memcpy(g.pi, pi, sizeof g.pi);
+    g.img = img;
+    g.L = pp.L;
+    g.gates = pp.t.gates;
+    g.noise = pp.t.noise;
+    gp::launch_bbgen_fill(g, st);
+    const cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? GP_OK : cuda_fail(ctx, e, "branch fill");
 }
 
 }  // namespace
@@ -812,10 +1053,14 @@ bool pipeline_wanted(gp_ctx *ctx, size_t count) {
 }
 
 gp_status run_batch_pipelined(gp_ctx *ctx, const gp_circuit_view *cs, size_t count, uint8_t level, HostOut &ho,
-                              DeviceHeader &hdr, gp_stats *stats) {
+                              DeviceHeader &hdr, gp_stats *stats, const BBGenReq *gen = nullptr) {
     const auto t0 = clk::now();
     gp::PipeState &ps = *ctx->pipe;
     gp_status st = GP_OK;
+    // device generation: every branch's check subsets drawn up front; each
+    // sub-batch is then planned on the host and written on the device
+    if (gen && (st = bbgen_draw(ctx, *gen, count, level)) != GP_OK) return st;
+    uint32_t gen_pi[gp::kLanes][5] = {};
     static const size_t sub = std::getenv("GP_PIPE_SUB") ? (size_t)std::atoi(std::getenv("GP_PIPE_SUB")) : kSubCircuits;
     const size_t P = std::min(kMaxSub, std::max<size_t>(2, count / sub));
     // Mapped host arrays of the whole batch view, sized by the learned hints.
@@ -917,6 +1162,11 @@ gp_status run_batch_pipelined(gp_ctx *ctx, const gp_circuit_view *cs, size_t cou
         gp::PackPlan &pp = ln.pp;
         pp.force_wide = false;
         pp.no_narrow = false;
+        if (gen) {
+            if ((st = bbgen_plan(ctx, c0, n, level, pp, gen_pi[k % gp::kLanes])) != GP_OK) return drain(), st;
+            if ((st = ensure_host_plain(&ln.h_stage, &ln.h_stage_cap, pp.L.total)) != GP_OK)
+                return drain(), fail(ctx, st, "pinned host allocation failed");
+        } else {
     repack:
         gp::pack_plan(hpool, cs + c0, n, level, pp);
         if (pp.err == gp::kPackIndexSpace || pp.err == gp::kPackTooWide) {
@@ -934,6 +1184,7 @@ gp_status run_batch_pipelined(gp_ctx *ctx, const gp_circuit_view *cs, size_t cou
             goto repack;
         }
         gp::pack_finish(pp, ln.h_stage);
+        }  // (host packing)
         BatchTotals t = pp.t;
         if (t.sources >= 0xFFFFFFFFull || t.tiles >= 0xFFFFFFFFull || t.gates >= 0xFFFFFFFFull ||
             t.noise >= 0xFFFFFFFFull || t.meas >= 0xFFFFFFFFull || t.layer_slots >= 0xFFFFFFFFull)
@@ -982,10 +1233,17 @@ gp_status run_batch_pipelined(gp_ctx *ctx, const gp_circuit_view *cs, size_t cou
         // stream); the upload overwrites the lane's image only once the lane's
         // previous kernels are done reading it
         if (ln.used) cudaStreamWaitEvent(ps.s_in, ln.ev_done, 0);
-        cudaError_t e = cudaMemcpyAsync(ln.d_img, ln.h_stage, pp.image_bytes(), cudaMemcpyHostToDevice, ps.s_in);
+        const uint64_t up = gen ? pp.L.lay_gate : pp.image_bytes();  // device generation: the head only
+        cudaError_t e = cudaMemcpyAsync(ln.d_img, ln.h_stage, up, cudaMemcpyHostToDevice, ps.s_in);
+        if (gen && e == cudaSuccess)
+            e = cudaMemcpyAsync(ln.d_img + pp.L.prob_table, ln.h_stage + pp.L.prob_table, t.prob_table_n * 8,
+                                cudaMemcpyHostToDevice, ps.s_in);
         cudaEventRecord(ln.ev_in, ps.s_in);
         cudaStreamWaitEvent(ln.s_comp, ln.ev_in, 0);
         if (ln.used) cudaStreamWaitEvent(ln.s_comp, ln.ev_out, 0);  // the lane's download read d_out
+        if (gen && e == cudaSuccess &&
+            (st = bbgen_fill(ctx, *gen, c0, level, pp, gen_pi[k % gp::kLanes], ln.d_img, ln.s_comp)) != GP_OK)
+            return drain(), st;
         if (trace) {
             tpack.push_back(ns_since(tp0) / 1e3);
             for (int x = 0; x < 3; x++) tev.push_back(nullptr), cudaEventCreate(&tev.back());
@@ -997,7 +1255,7 @@ gp_status run_batch_pipelined(gp_ctx *ctx, const gp_circuit_view *cs, size_t cou
         cudaEventRecord(ln.ev_done, ln.s_comp);
         ln.used = true;
         if (e != cudaSuccess) return drain(), cuda_fail(ctx, e, "pipelined launch");
-        h2d_bytes += pp.image_bytes();
+        h2d_bytes += gen ? up + t.prob_table_n * 8 : pp.image_bytes();
         sources += t.sources;
     }
     for (size_t j = 0; j < P; j++)
@@ -1007,6 +1265,7 @@ gp_status run_batch_pipelined(gp_ctx *ctx, const gp_circuit_view *cs, size_t cou
     const uint64_t pack_ns = ns_since(t0);
     cudaEventRecord(ctx->ev_h2d, ctx->stream);
     drain();
+    if (gen) cudaMemcpy(ctx->bb.h_err, ctx->bb.d_err, 4, cudaMemcpyDeviceToHost);
     cudaEventRecord(ctx->ev_end, ps.s_out);
     cudaEventSynchronize(ctx->ev_end);
     cudaError_t e = cudaGetLastError();
@@ -1052,15 +1311,15 @@ gp_status run_batch_pipelined(gp_ctx *ctx, const gp_circuit_view *cs, size_t cou
 }
 
 gp_status run_batch_any(gp_ctx *ctx, const gp_circuit_view *cs, size_t count, uint8_t level, HostOut &ho,
-                        DeviceHeader &hdr, gp_stats *stats) {
+                        DeviceHeader &hdr, gp_stats *stats, const BBGenReq *gen = nullptr) {
     if (level > 2) return fail(ctx, GP_ERR_INVALID_ARGUMENT, "correlation level must be 0, 1 or 2");
     if (cudaSetDevice(ctx->device) != cudaSuccess) return fail(ctx, GP_ERR_CUDA, "cudaSetDevice failed");
     if (pipeline_wanted(ctx, count)) {
-        const gp_status st = run_batch_pipelined(ctx, cs, count, level, ho, hdr, stats);
+        const gp_status st = run_batch_pipelined(ctx, cs, count, level, ho, hdr, stats, gen);
         if (st != GP_ERR_UNSUPPORTED || !ctx->err.empty()) return st;
         ctx->err.clear();  // capacity miss: learn with the unpipelined path
     }
-    const gp_status st = run_batch(ctx, cs, count, level, ho, hdr, stats);
+    const gp_status st = run_batch(ctx, cs, count, level, ho, hdr, stats, gp::kModeFull, 0, 0xFFFFFFFFu, nullptr, gen);
     if (st == GP_OK && ctx->pipeline != 0 && count >= 2 * kSubCircuits) {  // learn the pipeline's output sizes
         if (!ctx->pipe) {
             ctx->pipe = new gp::PipeState();
@@ -1137,6 +1396,10 @@ void gp_ctx_destroy(gp_ctx *ctx) {
     if (ctx->d_flush) cudaFree(ctx->d_flush);
     if (ctx->d_merge) cudaFree(ctx->d_merge);
     if (ctx->d_bases) cudaFree(ctx->d_bases);
+    for (void *d : {(void *)ctx->bb.d_tmpl, (void *)ctx->bb.d_masks, (void *)ctx->bb.d_counts, (void *)ctx->bb.d_err})
+        if (d) cudaFree(d);
+    for (void *hp : {(void *)ctx->bb.h_counts, (void *)ctx->bb.h_err})
+        if (hp) cudaFreeHost(hp);
     if (ctx->graph.exec) cudaGraphExecDestroy(ctx->graph.exec);
     gp::pipe_destroy(ctx->pipe);
     for (cudaEvent_t ev : ctx->prof)
@@ -1202,6 +1465,56 @@ gp_status gp_compile_batch(gp_ctx *ctx, const gp_circuit_view *circuits, size_t 
     for (size_t c = 0; c < count; c++) {
         ctx->out_ndet[c] = circuits[c].num_detectors;
         ctx->out_nobs[c] = circuits[c].num_observables;
+    }
+    out->num_circuits = count;
+    out->edge_offsets = ho.edge_off;
+    out->num_detectors = ctx->out_ndet.data();
+    out->num_observables = ctx->out_nobs.data();
+    out->num_edges = hdr.num_edges;
+    out->det_offsets = ho.det_off;
+    out->det_ids = ho.det_ids;
+    out->obs_offsets = ho.obs_off;
+    out->obs_ids = ho.obs_ids;
+    out->probs = ho.probs;
+    return GP_OK;
+}
+
+gp_status gp_compile_bb_branches(gp_ctx *ctx, const gp_bb_spec *spec, uint64_t first_branch, size_t count,
+                                 uint8_t level, gp_dem_batch_view *out, gp_stats *stats) {
+    ctx->err.clear();
+    if (!spec || !out) return fail(ctx, GP_ERR_INVALID_ARGUMENT, "null argument");
+    if (level > 2) return fail(ctx, GP_ERR_INVALID_ARGUMENT, "correlation level must be 0, 1 or 2");
+    if (count == 0 || count >= (1u << 31)) return fail(ctx, GP_ERR_INVALID_ARGUMENT, "branch count must be 1 .. 2^31 - 1");
+    if (cudaSetDevice(ctx->device) != cudaSuccess) return fail(ctx, GP_ERR_CUDA, "cudaSetDevice failed");
+    auto &bb = ctx->bb;
+    if (!bb.valid || std::memcmp(&bb.spec, spec, sizeof *spec) != 0) {  // (re)build the template
+        bb.valid = false;
+        if (const char *why = gp::bb_template(*spec, &bb.t)) return fail(ctx, GP_ERR_INVALID_ARGUMENT, why);
+        if (bb.t.lm > 0xFFFF) return fail(ctx, GP_ERR_UNSUPPORTED, "more than 65535 checks per type");
+        std::vector<uint32_t> h;
+        for (const auto *v : {&bb.t.xdata, &bb.t.zdata, &bb.t.zfinal, &bb.t.obs_off, &bb.t.obs_q})
+            h.insert(h.end(), v->begin(), v->end());
+        gp_status st = ensure_device(ctx, reinterpret_cast<uint8_t **>(&bb.d_tmpl), &bb.d_tmpl_cap, h.size() * 4);
+        if (st != GP_OK) return st;
+        if (cudaMemcpy(bb.d_tmpl, h.data(), h.size() * 4, cudaMemcpyHostToDevice) != cudaSuccess)
+            return fail(ctx, GP_ERR_CUDA, "template upload");
+        bb.spec = *spec;
+        bb.valid = true;
+    }
+    HostOut ho{};
+    DeviceHeader hdr{};
+    const BBGenReq req{first_branch};
+    gp_status st = run_batch_any(ctx, nullptr, count, level, ho, hdr, stats, &req);
+    if (st != GP_OK) return st;
+    if (*bb.h_err) return fail(ctx, GP_ERR_CUDA, "device branch generator disagreed with its plan");
+    ctx->out_ndet.resize(count);
+    ctx->out_nobs.resize(count);
+    for (size_t c = 0; c < count; c++) {  // (DetectorTracker: Z checks from the first round, X from the second)
+        const uint32_t *cnt = bb.h_counts + c * bb.t.rounds;
+        uint32_t D = bb.t.lm;
+        for (uint32_t r = 0; r < bb.t.rounds; r++) D += (cnt[r] >> 16) + (r ? cnt[r] & 0xFFFF : 0);
+        ctx->out_ndet[c] = D;
+        ctx->out_nobs[c] = bb.t.O;
     }
     out->num_circuits = count;
     out->edge_offsets = ho.edge_off;

@@ -145,6 +145,23 @@ struct DevPlan {
 
 enum PipeMode : uint32_t { kModeFull = 0, kModeShard = 1, kModeMerge = 2 };
 
+// Device branch generation (gp_bbgen.cuh): kernel parameters.
+struct BBGenParams {
+    const uint32_t *xdata, *zdata, *zfinal, *obs_off, *obs_q;  // template (gp_gen.h BBTemplate), device copies
+    uint32_t lm, nd, n, rounds, refresh, O, MW, level, C;
+    double check_prob, pm;
+    uint64_t seed, first;
+    uint32_t pi[5];   // probability-table index per channel: p1, p2, pr, pidle, pidle (M/MR/R layers); ~0: off
+    uint64_t *masks;  // [C][rounds][2][MW] executed X / Z checks
+    uint32_t *counts; // [C][rounds] ne | nz << 16
+    uint8_t *img;     // staging image on the device (its head already uploaded)
+    StageLayout L;
+    uint64_t gates, noise;  // planned batch totals (the last circuit's check)
+    uint32_t *err;          // circuits whose fill disagreed with the host plan
+};
+void launch_bbgen_draw(const BBGenParams &g, cudaStream_t st);
+void launch_bbgen_fill(const BBGenParams &g, cudaStream_t st);
+
 struct StageEvents {
     cudaEvent_t lowered, traversed, reduced;
 };

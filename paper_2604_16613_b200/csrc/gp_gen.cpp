@@ -18,6 +18,7 @@
 #include <vector>
 
 #include "../../include/greenpeas.h"
+#include "gp_gen.h"
 
 struct gp_circuit {
     uint32_t num_qubits = 0, num_measurements = 0;
@@ -44,6 +45,21 @@ struct Model {
     int kind;  // GP_NOISE_MODEL_*
     double p;
 };
+
+// Channel probabilities of a layer (has_mr: the layer holds M / MR / R).
+struct ModelProbs {
+    double p1, p2, pm, pr, pidle;
+};
+ModelProbs model_probs(const Model &mdl, bool has_mr) {
+    switch (mdl.kind) {
+        case GP_NOISE_MODEL_SI1000:
+            return {mdl.p / 10, mdl.p, 5 * mdl.p, 2 * mdl.p, has_mr ? 2 * mdl.p : mdl.p / 10};
+        case GP_NOISE_MODEL_UNIFORM:
+            return {mdl.p, mdl.p, mdl.p, mdl.p, mdl.p};
+        default:  // NoiseModel{p}: codes.hpp:30-39
+            return {mdl.p, mdl.p / 10, mdl.p, mdl.p, mdl.p / 10};
+    }
+}
 
 // Open-layer builder (the CircuitBuilder contract: codes.hpp:41-76).
 class Builder {
@@ -94,25 +110,8 @@ class Builder {
             uint8_t k = c_->gate_kind[g];
             if (k == GP_GATE_M || k == GP_GATE_MR || k == GP_GATE_R) has_mr = true;
         }
-        double p1, p2, pm, pr, pidle;
-        switch (mdl.kind) {
-            case GP_NOISE_MODEL_SI1000:
-                p1 = mdl.p / 10;
-                p2 = mdl.p;
-                pm = 5 * mdl.p;
-                pr = 2 * mdl.p;
-                pidle = has_mr ? 2 * mdl.p : mdl.p / 10;
-                break;
-            case GP_NOISE_MODEL_UNIFORM:
-                p1 = p2 = pm = pr = pidle = mdl.p;
-                break;
-            default:  // NoiseModel{p}: codes.hpp:30-39
-                p1 = mdl.p;
-                p2 = mdl.p / 10;
-                pm = mdl.p;
-                pr = mdl.p;
-                pidle = mdl.p / 10;
-        }
+        const ModelProbs mp = model_probs(mdl, has_mr);
+        const double p1 = mp.p1, p2 = mp.p2, pm = mp.pm, pr = mp.pr, pidle = mp.pidle;
         for (size_t g = g0; g < c_->gate_kind.size(); g++) {
             const uint32_t q = c_->gate_q0[g];
             busy[q] = 1;
@@ -270,46 +269,78 @@ std::vector<Bits> null_space(const std::vector<Bits> &H, uint32_t nbits) {
     return out;
 }
 
-gp_circuit *make_bb(uint32_t L, uint32_t Mm, const uint32_t a[3], const uint32_t b[3], uint32_t rounds, double p,
-                    int model, double check_prob, uint32_t refresh, uint64_t seed, uint64_t branch) {
-    const uint32_t lm = L * Mm, nd = 2 * lm, n = 4 * lm;
-    auto idx = [&](uint32_t i, uint32_t j) { return (i % L) * Mm + (j % Mm); };
-    // Monomials: A = x^a0 + y^a1 + y^a2, B = y^b0 + x^b1 + x^b2 (x shifts i, y shifts j).
+// Bivariate bicycle geometry (A = x^a0 + y^a1 + y^a2, B = y^b0 + x^b1 + x^b2
+// on an L x Mm torus): check k's data qubits per direction, logical Z
+// operators. Shared by the host generator (make_bb) and the device branch
+// generator's template (bb_template).
+struct BBGeom {
     struct Mono {
         uint32_t u, v;
     };
-    const Mono A[3] = {{a[0], 0}, {0, a[1]}, {0, a[2]}};
-    const Mono B[3] = {{0, b[0]}, {b[1], 0}, {b[2], 0}};
-    auto fwd = [&](Mono mo, uint32_t c) { return idx(c / Mm + mo.u, c % Mm + mo.v); };
-    auto inv = [&](Mono mo, uint32_t c) { return idx(c / Mm + L - mo.u % L, c % Mm + Mm - mo.v % Mm); };
+    uint32_t L, Mm, lm, nd, n;
+    Mono A[3], B[3];
+    BBGeom(uint32_t l, uint32_t m, const uint32_t a[3], const uint32_t b[3])
+        : L(l), Mm(m), lm(l * m), nd(2 * l * m), n(4 * l * m),
+          A{{a[0], 0}, {0, a[1]}, {0, a[2]}}, B{{0, b[0]}, {b[1], 0}, {b[2], 0}} {}
+    uint32_t idx(uint32_t i, uint32_t j) const { return (i % L) * Mm + (j % Mm); }
+    uint32_t fwd(Mono mo, uint32_t c) const { return idx(c / Mm + mo.u, c % Mm + mo.v); }
+    uint32_t inv(Mono mo, uint32_t c) const { return idx(c / Mm + L - mo.u % L, c % Mm + Mm - mo.v % Mm); }
     // X check c: L data fwd(A_t, c), R data lm + fwd(B_t, c)   (H_X = [A | B])
     // Z check c: L data inv(B_t, c), R data lm + inv(A_t, c)   (H_Z = [B^T | A^T])
-    const size_t W = (nd + 63) / 64;
-    std::vector<Bits> HX(lm, Bits(W, 0)), HZ(lm, Bits(W, 0));
-    for (uint32_t c = 0; c < lm; c++)
-        for (int t = 0; t < 3; t++) {
-            uint32_t q;
-            q = fwd(A[t], c);
-            HX[c][q >> 6] ^= 1ull << (q & 63);
-            q = lm + fwd(B[t], c);
-            HX[c][q >> 6] ^= 1ull << (q & 63);
-            q = inv(B[t], c);
-            HZ[c][q >> 6] ^= 1ull << (q & 63);
-            q = lm + inv(A[t], c);
-            HZ[c][q >> 6] ^= 1ull << (q & 63);
-        }
+    // direction d < 3: the L-data neighbour through A_d (X) or B_d^T (Z);
+    // d >= 3: the R-data neighbour through B_{d-3} (X) or A_{d-3}^T (Z)
+    uint32_t xdata(int d, uint32_t k) const { return d < 3 ? fwd(A[d], k) : lm + fwd(B[d - 3], k); }
+    uint32_t zdata(int d, uint32_t k) const { return d < 3 ? inv(B[d], k) : lm + inv(A[d - 3], k); }
     // Logical Z operators: ker(H_X) modulo rowspace(H_Z).
-    Echelon span{{}, {}, nd};
-    for (const Bits &r : HZ) span.add(r);
-    std::vector<Bits> logicals;
-    for (const Bits &v : null_space(HX, nd)) {
-        Bits red = v;
-        span.reduce(red);
-        bool nz = false;
-        for (uint64_t w : red) nz |= w != 0;
-        if (!nz) continue;
-        if (span.add(v)) logicals.push_back(v);
+    std::vector<Bits> logicals() const {
+        const size_t W = (nd + 63) / 64;
+        std::vector<Bits> HX(lm, Bits(W, 0)), HZ(lm, Bits(W, 0));
+        for (uint32_t c = 0; c < lm; c++)
+            for (int t = 0; t < 3; t++) {
+                uint32_t q;
+                q = fwd(A[t], c);
+                HX[c][q >> 6] ^= 1ull << (q & 63);
+                q = lm + fwd(B[t], c);
+                HX[c][q >> 6] ^= 1ull << (q & 63);
+                q = inv(B[t], c);
+                HZ[c][q >> 6] ^= 1ull << (q & 63);
+                q = lm + inv(A[t], c);
+                HZ[c][q >> 6] ^= 1ull << (q & 63);
+            }
+        Echelon span{{}, {}, nd};
+        for (const Bits &r : HZ) span.add(r);
+        std::vector<Bits> out;
+        for (const Bits &v : null_space(HX, nd)) {
+            Bits red = v;
+            span.reduce(red);
+            bool nz = false;
+            for (uint64_t w : red) nz |= w != 0;
+            if (!nz) continue;
+            if (span.add(v)) out.push_back(v);
+        }
+        return out;
     }
+};
+
+// The depth-8 syndrome cycle of Bravyi et al. (Nature 627, 778 (2024),
+// Fig. 7): seven CX layers in which X and Z checks interleave, each check
+// touching its six data qubits in the direction order kSX / kSZ. Its PrepX /
+// MeasX steps are R/MR + H in this gate set, so a round is
+//   t0  H(X anc)            | Z: CX dir kSZ[0]
+//   t1..t5  X: CX dir kSX[t] | Z: CX dir kSZ[t]
+//   t6  X: CX dir kSX[6]     | Z: MR (measure + re-prepare)
+//   t7  H(X anc)
+//   t8  MR(X anc)
+constexpr int kSX[7] = {-1, 1, 4, 3, 5, 0, 2};
+constexpr int kSZ[7] = {3, 5, 0, 1, 2, 4, -1};
+
+gp_circuit *make_bb(uint32_t L, uint32_t Mm, const uint32_t a[3], const uint32_t b[3], uint32_t rounds, double p,
+                    int model, double check_prob, uint32_t refresh, uint64_t seed, uint64_t branch) {
+    const BBGeom geo(L, Mm, a, b);
+    const uint32_t lm = geo.lm, nd = geo.nd, n = geo.n;
+    auto inv = [&](BBGeom::Mono mo, uint32_t c) { return geo.inv(mo, c); };
+    const BBGeom::Mono *A = geo.A, *B = geo.B;
+    const std::vector<Bits> logicals = geo.logicals();
 
     gp_circuit *c = new gp_circuit();
     Builder bld(c);
@@ -333,21 +364,8 @@ gp_circuit *make_bb(uint32_t L, uint32_t Mm, const uint32_t a[3], const uint32_t
                 ex[k] = unif(rng) < check_prob;
                 ez[k] = unif(rng) < check_prob;
             }
-        // The depth-8 syndrome cycle of Bravyi et al. (Nature 627, 778 (2024),
-        // Fig. 7): seven CX layers in which X and Z checks interleave, each
-        // check touching its six data qubits in the direction order sX / sZ
-        // (direction d < 3: the L-data neighbour through A_d (X) or B_d^T (Z);
-        // d >= 3: the R-data neighbour through B_{d-3} (X) or A_{d-3}^T (Z)).
-        // Its PrepX / MeasX steps are R/MR + H in this gate set, so a round is
-        //   t0  H(X anc)            | Z: CX dir sZ[0]
-        //   t1..t5  X: CX dir sX[t] | Z: CX dir sZ[t]
-        //   t6  X: CX dir sX[6]     | Z: MR (measure + re-prepare)
-        //   t7  H(X anc)
-        //   t8  MR(X anc)
-        static constexpr int kSX[7] = {-1, 1, 4, 3, 5, 0, 2};
-        static constexpr int kSZ[7] = {3, 5, 0, 1, 2, 4, -1};
-        auto xdata = [&](int d, uint32_t k) { return d < 3 ? fwd(A[d], k) : lm + fwd(B[d - 3], k); };
-        auto zdata = [&](int d, uint32_t k) { return d < 3 ? inv(B[d], k) : lm + inv(A[d - 3], k); };
+        auto xdata = [&](int d, uint32_t k) { return geo.xdata(d, k); };
+        auto zdata = [&](int d, uint32_t k) { return geo.zdata(d, k); };
         std::vector<uint32_t> mx(lm), mz(lm);
         for (int t = 0; t < 7; t++) {
             if (t == 0) {
@@ -410,6 +428,71 @@ gp_circuit *make_bb(uint32_t L, uint32_t Mm, const uint32_t a[3], const uint32_t
 }
 
 }  // namespace
+
+namespace gp {
+
+const char *bb_template(const gp_bb_spec &s, BBTemplate *t) {
+    if (s.l < 2 || s.m < 2 || s.rounds < 1) return "BB spec: l, m >= 2 and rounds >= 1 required";
+    const BBGeom geo(s.l, s.m, s.a, s.b);
+    t->lm = geo.lm;
+    t->nd = geo.nd;
+    t->n = geo.n;
+    t->rounds = s.rounds;
+    t->refresh = s.refresh ? s.refresh : std::max<uint32_t>(1, s.rounds / 2);  // (as make_bb)
+    t->check_prob = s.check_prob;
+    t->seed = s.seed;
+    const Model mdl{s.noise_model, s.p};
+    const ModelProbs a = model_probs(mdl, false), b = model_probs(mdl, true);
+    t->p1 = a.p1;
+    t->p2 = a.p2;
+    t->pm = a.pm;
+    t->pr = a.pr;
+    t->pidle = a.pidle;
+    t->pidle_mr = b.pidle;
+    const uint32_t lm = geo.lm;
+    t->xdata.assign(7 * lm, 0);
+    t->zdata.assign(7 * lm, 0);
+    for (int x = 0; x < 7; x++)
+        for (uint32_t k = 0; k < lm; k++) {
+            if (kSX[x] >= 0) t->xdata[x * lm + k] = geo.xdata(kSX[x], k);
+            if (kSZ[x] >= 0) t->zdata[x * lm + k] = geo.zdata(kSZ[x], k);
+        }
+    // Every layer of a full round touches each qubit at most once, so any
+    // check subset does too (the device generator counts busy qubits by
+    // formula; the reference's validate_layers would reject a collision).
+    for (int x = 0; x < 7; x++) {
+        std::vector<uint8_t> used(geo.n, 0);
+        auto use = [&](uint32_t q) { return used[q]++ == 0; };
+        for (uint32_t k = 0; k < lm; k++) {
+            bool ok = use(geo.nd + k);
+            if (kSX[x] >= 0) ok &= use(t->xdata[x * lm + k]);
+            if (kSZ[x] >= 0) ok &= use(t->zdata[x * lm + k]);
+            ok &= use(geo.nd + lm + k);
+            if (!ok) return "BB spec: a syndrome-cycle layer touches a qubit twice";
+        }
+    }
+    t->zfinal.assign(6 * lm, 0);
+    for (uint32_t k = 0; k < lm; k++) {
+        uint32_t *z = &t->zfinal[6 * k];
+        for (int x = 0; x < 3; x++) {
+            z[2 * x] = geo.inv(geo.B[x], k);
+            z[2 * x + 1] = lm + geo.inv(geo.A[x], k);
+        }
+        std::sort(z, z + 6);
+        if (std::adjacent_find(z, z + 6) != z + 6) return "BB spec: a final Z detector repeats a data qubit";
+    }
+    t->obs_off.assign(1, 0);
+    t->obs_q.clear();
+    for (const Bits &v : geo.logicals()) {
+        for (uint32_t q = 0; q < geo.nd; q++)
+            if (get_bit(v, q)) t->obs_q.push_back(q);
+        t->obs_off.push_back((uint32_t)t->obs_q.size());
+    }
+    t->O = (uint32_t)t->obs_off.size() - 1;
+    return nullptr;
+}
+
+}  // namespace gp
 
 extern "C" {
 

@@ -22,6 +22,8 @@
 #include <utility>
 
 #include "gp_device.h"
+#include "gp_rng.h"
+#include "../../include/greenpeas.h"
 
 namespace gp {
 
@@ -291,6 +293,7 @@ __global__ void lower_kernel(__grid_constant__ const DevPlan p, uint32_t blocks_
 #include "gp_reduce.cuh"
 #include "gp_traverse.cuh"
 #include "gp_walk.cuh"
+#include "gp_bbgen.cuh"
 namespace {
 
 // Files the traversal's pooled records into per-source slots: the returning
@@ -837,6 +840,17 @@ reduce:
     if (ev) cudaEventRecord(ev->reduced, st);
     *err = cudaGetLastError();
     return launches;
+}
+
+void launch_bbgen_draw(const BBGenParams &g, cudaStream_t st) {
+    if (g.C) bbgen::bbgen_draw_kernel<<<(g.C + 127) / 128, 128, 0, st>>>(g);
+}
+
+void launch_bbgen_fill(const BBGenParams &g, cudaStream_t st) {
+    constexpr uint32_t kWarps = 4;  // branches per CTA
+    const size_t smem = (size_t)kWarps * bbgen::fill_smem_words(g.n, g.lm) * 4;
+    if (smem > 48 * 1024) cudaFuncSetAttribute(bbgen::bbgen_fill_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (g.C) bbgen::bbgen_fill_kernel<<<(g.C + kWarps - 1) / kWarps, 32 * kWarps, smem, st>>>(g);
 }
 
 }  // namespace gp

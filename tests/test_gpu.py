@@ -513,3 +513,63 @@ def test_reference_acceptance_gate_through_dropin():
     lines = [x for x in out.stdout.splitlines() if x.startswith(("PASS", "FAIL"))]
     assert len(lines) == 10 and all(x.startswith("PASS") for x in lines), out.stdout + out.stderr
     assert out.returncode == 0
+
+
+# ---------------------------------------------------------------- device branch generation
+
+def test_device_generated_branches_match_reference():
+    """gp_compile_bb_branches: the 4,096 headline branches generated on the
+    GPU from (seed, branch id) -- no host circuits -- give every branch's
+    reference DEM (digests of tests/golden/bb72_branches_r6_L0.npz); an offset
+    range too (branch ids 3,000 .. 4,095), and repeated calls."""
+    comp = gp.Compiler(0)
+    spec = gp.bb72_branch_spec()
+    for _ in range(2):
+        out, st = comp.compile_bb_branches_raw(spec, 0, 4096, 0)
+        check_branch_batch(comp, out, 0, 4096)
+    assert st["h2d_bytes"] < 4096 * 512  # the image head only: no circuits cross PCIe
+    out, _ = comp.compile_bb_branches_raw(spec, 3000, 1096, 0)
+    check_branch_batch(comp, out, 3000, 1096)
+
+
+@pytest.mark.parametrize("case", ["bb72-cp0.3-L2", "bb72-cp0.9-L1", "bb144-full-L0", "bb72-si1000-L0"])
+def test_device_generated_branches_equal_host_generated(case):
+    """Other specs (check probability, level, code, noise model): the device
+    generator's batch DEM equals gp_compile_batch over gen_bb's host circuits
+    (digest per circuit)."""
+    kw = {"bb72-cp0.3-L2": dict(l=6, m=6, rounds=6, noise_model=0, check_prob=0.3, refresh=3, seed=7, level=2,
+                                first=1000, count=300),
+          "bb72-cp0.9-L1": dict(l=6, m=6, rounds=8, noise_model=2, check_prob=0.9, refresh=0, seed=3, level=1,
+                                first=5, count=320),
+          "bb144-full-L0": dict(l=12, m=6, rounds=3, noise_model=2, check_prob=1.0, refresh=0, seed=1, level=0,
+                                first=0, count=4),
+          "bb72-si1000-L0": dict(l=6, m=6, rounds=6, noise_model=1, check_prob=0.5, refresh=2, seed=11, level=0,
+                                 first=77, count=400)}[case]
+    level, first, count = kw.pop("level"), kw.pop("first"), kw.pop("count")
+    l, m = kw.pop("l"), kw.pop("m")
+    spec = gp.bb_spec(l, m, p=2e-3, **kw)
+    comp = gp.Compiler(0)
+    comp.set_option(4, 0)
+    out, _ = comp.compile_bb_branches_raw(spec, first, count, level)
+    got = comp.batch_digests(out)
+    gens = [gp.gen_bb(l, m, p=2e-3, branch=b, **kw) for b in range(first, first + count)]
+    from paper_2604_16613_b200 import _native as N
+    arr = (N.CircuitView * count)()
+    for i, g in enumerate(gens):
+        arr[i] = g.view()[0]
+    ref_comp = gp.Compiler(0)
+    ref_comp.set_option(4, 0)
+    want_out, _ = ref_comp.compile_batch_raw(arr, level)
+    want = ref_comp.batch_digests(want_out)
+    bad = np.nonzero(got != want)[0]
+    assert bad.size == 0, f"{bad.size} of {count} differ (first: branch {first + int(bad[0])})"
+
+
+def test_device_generated_branches_errors():
+    comp = gp.Compiler(0)
+    with pytest.raises(ValueError, match="branch count"):
+        comp.compile_bb_branches_raw(gp.bb72_branch_spec(), 0, 0, 0)
+    with pytest.raises(ValueError, match="l, m >= 2"):
+        comp.compile_bb_branches_raw(gp.bb_spec(1, 6), 0, 4, 0)
+    with pytest.raises(ValueError, match="correlation level"):
+        comp.compile_bb_branches_raw(gp.bb72_branch_spec(), 0, 4, 3)
