@@ -293,7 +293,7 @@ gp_status ensure_host(gp_ctx *ctx, uint8_t **buf, size_t *cap, size_t need) {
     if (cudaMallocHost(buf, want) != cudaSuccess) {
         cudaGetLastError();
         *buf = nullptr;
-        return fail(ctx, GP_ERR_OUT_OF_MEMORY, "pinned host allocation failed");
+        return fail(ctx, GP_ERR_OUT_OF_MEMORY, "pinned host allocation of " + std::to_string(want) + " bytes failed");
     }
     *cap = want;
     return GP_OK;
@@ -1062,7 +1062,12 @@ gp_status run_batch_pipelined(gp_ctx *ctx, const gp_circuit_view *cs, size_t cou
     if (gen && (st = bbgen_draw(ctx, *gen, count, level)) != GP_OK) return st;
     uint32_t gen_pi[gp::kLanes][5] = {};
     static const size_t sub = std::getenv("GP_PIPE_SUB") ? (size_t)std::atoi(std::getenv("GP_PIPE_SUB")) : kSubCircuits;
-    const size_t P = std::min(kMaxSub, std::max<size_t>(2, count / sub));
+    // (device generation: GP_GEN_SUB tunes its sub-batch size separately;
+    // measured 13.2 ms per 4,096 branches at 512, 15.8 at 1,024 -- a lane's
+    // next sub-batch waits for its download)
+    const char *gs = std::getenv("GP_GEN_SUB");
+    const size_t gen_sub = gs ? std::max<size_t>(64, (size_t)std::atoi(gs)) : kSubCircuits;
+    const size_t P = std::min(kMaxSub, std::max<size_t>(2, count / (gen ? gen_sub : sub)));
     // Mapped host arrays of the whole batch view, sized by the learned hints.
     const uint64_t e_cap = ps.e_hint, ids_cap = ps.ids_hint, c_cap = count + 1;
     size_t o = 0;
@@ -1165,7 +1170,7 @@ gp_status run_batch_pipelined(gp_ctx *ctx, const gp_circuit_view *cs, size_t cou
         if (gen) {
             if ((st = bbgen_plan(ctx, c0, n, level, pp, gen_pi[k % gp::kLanes])) != GP_OK) return drain(), st;
             if ((st = ensure_host_plain(&ln.h_stage, &ln.h_stage_cap, pp.L.total)) != GP_OK)
-                return drain(), fail(ctx, st, "pinned host allocation failed");
+                return drain(), fail(ctx, st, "pinned host allocation of " + std::to_string(pp.L.total) + " bytes failed");
         } else {
     repack:
         gp::pack_plan(hpool, cs + c0, n, level, pp);
@@ -1175,7 +1180,7 @@ gp_status run_batch_pipelined(gp_ctx *ctx, const gp_circuit_view *cs, size_t cou
             return fail_pack(ctx, leaf_err ? leaf_err : pp.err);
         }
         if ((st = ensure_host_plain(&ln.h_stage, &ln.h_stage_cap, pp.L.total)) != GP_OK)
-            return drain(), fail(ctx, st, "pinned host allocation failed");
+            return drain(), fail(ctx, st, "pinned host allocation of " + std::to_string(pp.L.total) + " bytes failed");
         gp::pack_range(hpool, cs + c0, pp, ln.h_stage, 0, n);
         if (pp.err) return drain(), fail_pack(ctx, pp.err);
         if ((pp.need_wide.load() && !pp.force_wide) || (pp.need_wide_words.load() && !pp.no_narrow)) {
