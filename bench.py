@@ -125,11 +125,12 @@ def shard(rank: int, world: int, per_rank: int) -> range:
 
 
 def gather_flat(dist, arrays: dict, device: str):
-    """Gathers variable-length flat DEM arrays (per-rank tables) to every rank:
-    the final exchange step of SURVEY.md 8e (paper_2604_16613_b200.shard).
-    Returns {name: [per-rank np.ndarray]}."""
-    from paper_2604_16613_b200.shard import gather_flat as g
-    return g(arrays, device)
+    """Gathers variable-length flat DEM arrays (per-rank tables) to rank 0:
+    the final exchange step of SURVEY.md 8e (paper_2604_16613_b200.shard:
+    sizes all-gathered, payloads by grouped sends / receives into exact-size
+    buffers). Returns {name: [per-rank np.ndarray]} on rank 0, None elsewhere."""
+    from paper_2604_16613_b200.shard import gather_to_root
+    return gather_to_root(arrays, device, 0)
 
 
 def build_branches(first: int, count: int):
@@ -342,9 +343,10 @@ def circuit_bytes(views) -> int:
 def sharded_single_block(compiler, dist, reps: int = 10):
     """one large circuit (surface d25 r25, L0) compiled across
     the ranks by fault-range sharding -- shard compile into device tables,
-    NCCL all-gather, merge on rank 0 -- wall p50 (max over ranks), with the
-    one-GPU compile of the same circuit beside it and the merged DEM checked
-    byte for byte against it."""
+    all-to-all of the entries by owning rank (NCCL send/recv), each owner
+    folds its signatures, owners' DEMs gathered to rank 0 -- wall p50 (max
+    over ranks) with its phases, the one-GPU compile of the same circuit
+    beside it and the merged DEM checked byte for byte against it."""
     import socket
 
     import torch.distributed as td
@@ -360,15 +362,21 @@ def sharded_single_block(compiler, dist, reps: int = 10):
     for _ in range(3):
         compile_sharded(compiler, g, 0)
     ts = []
+    phases = {}
     dem = None
     for _ in range(reps):
         dist.barrier()
         t = time.perf_counter()
-        dem = compile_sharded(compiler, g, 0)
+        tm = {}
+        dem = compile_sharded(compiler, g, 0, timings=tm)
         dist.barrier()
         ts.append(dist.max(time.perf_counter() - t))
+        for k, v in tm.items():
+            phases.setdefault(k, []).append(dist.max(float(v)))
     out = {"circuit": "surface_d25_r25_paper_L0", "shards": max(dist.ws, 1),
-           "p50_ms": statistics.median(ts) * 1e3}
+           "p50_ms": statistics.median(ts) * 1e3,
+           "phases_p50_max_over_ranks": {k: statistics.median(v) * (1e3 if k.endswith("_s") else 1)
+                                         for k, v in phases.items()}}
     if dist.rank == 0:
         whole = compiler.compile(g, 0)
         tw = []
@@ -481,9 +489,11 @@ def run_gpu(args, dist):
         g0 = time.perf_counter()
         got = gather_flat(dist, arrays, f"cuda:{device}")
         dist.barrier()
-        gather = {"ms": dist.max(time.perf_counter() - g0) * 1e3,
-                  "bytes": int(sum(sum(x.nbytes for x in v) for v in got.values())),
-                  "edges": int(sum(len(x) for x in got["probs"]))}
+        gms = dist.max(time.perf_counter() - g0) * 1e3
+        if rank == 0:
+            gather = {"ms": gms, "to": "rank 0 (grouped NCCL send/recv)",
+                      "bytes": int(sum(sum(x.nbytes for x in v) for v in got.values())),
+                      "edges": int(sum(len(x) for x in got["probs"]))}
 
     # --- roofline of the dominant kernel ------------------------------------
     from paper_2604_16613_b200 import _native as N

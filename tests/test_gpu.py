@@ -573,3 +573,79 @@ def test_device_generated_branches_errors():
         comp.compile_bb_branches_raw(gp.bb_spec(1, 6), 0, 4, 0)
     with pytest.raises(ValueError, match="correlation level"):
         comp.compile_bb_branches_raw(gp.bb72_branch_spec(), 0, 4, 3)
+
+
+# ---------------------------------------------------------------- two real ranks on the one GPU
+
+def _two_proc_worker(rank, world, port, q):
+    import os
+    import sys
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world),
+                      LOCAL_RANK=str(rank))
+    sys.path.insert(0, str(ROOT))
+    try:
+        import numpy as np
+        import torch.distributed as td
+
+        import bench
+        import paper_2604_16613_b200 as gp
+        from paper_2604_16613_b200 import shard
+        td.init_process_group("gloo")
+        comp = gp.Compiler(0)
+        res = {}
+        # fault-range sharding of one circuit, fold spread over the owners, DEM gathered to rank 0
+        for name, make, level in (("d11_si1000", lambda: gp.gen_surface(11, 11, 1e-3, gp.NOISE_MODEL_SI1000), 0),
+                                  ("bb144", lambda: gp.gen_bb144(6), 2)):
+            g = make()
+            tm = {}
+            dem = shard.compile_sharded(comp, g, level, timings=tm)
+            res[name] = (None if dem is None else dem.to_text() == comp.compile(g, level).to_text(),
+                         tm["merged_entries"])
+        # branch batches sharded by branch id, DEM tables gathered to rank 0
+        per = 300
+        circuits = bench.build_branches(rank * per, per)
+        views = bench.views_of(circuits)
+        out, _ = comp.compile_batch_raw(views, 0)
+        z = np.load(bench.GOLDEN_BRANCHES)
+        ok = bool(np.array_equal(comp.batch_digests(out), z["digests"][rank * per:(rank + 1) * per]))
+        from paper_2604_16613_b200 import _native as N
+        E = int(out.num_edges)
+        got = shard.gather_to_root({"probs": N.copy_f64(out.probs, E),
+                                    "edge_offsets": N.copy_u64(out.edge_offsets, per + 1)}, "cpu", 0)
+        res["branches"] = (ok, None if got is None else [len(x) for x in got["probs"]],
+                           None if got is None else [int(x[-1]) for x in got["edge_offsets"]])
+        td.destroy_process_group()
+        q.put((rank, res))
+    except Exception as e:  # pragma: no cover
+        import traceback
+        q.put((rank, "error " + traceback.format_exc()))
+
+
+def test_two_process_sharded_compile_and_gather():
+    """SURVEY 8e with two real ranks (two processes, gloo, both on cuda:0):
+    compile_sharded of one circuit -- shard compiles, all-to-all of the
+    entries to their owners, each owner's device merge (the fold spread over
+    ranks), owners' DEMs gathered to rank 0 -- is byte-identical to the
+    one-process compile; branch-sharded batches match the reference digests
+    and their DEM tables reach rank 0."""
+    import socket
+
+    import torch.multiprocessing as mp
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_two_proc_worker, args=(r, 2, port, q)) for r in range(2)]
+    [p.start() for p in procs]
+    res = dict(q.get(timeout=600) for _ in procs)
+    [p.join(timeout=120) for p in procs]
+    for r in (0, 1):
+        assert not isinstance(res[r], str), res[r]
+    for name in ("d11_si1000", "bb144"):
+        assert res[0][name][0] is True, name
+        assert res[1][name][0] is None
+        assert res[0][name][1] > 0 and res[1][name][1] > 0  # both owners folded a share
+    assert res[0]["branches"][0] and res[1]["branches"][0]
+    assert res[1]["branches"][1] is None
+    assert res[0]["branches"][2][0] > 0 and res[0]["branches"][2][1] > 0

@@ -50,11 +50,31 @@ def main():
                 dmerge_ms, m = p50(lambda: comp.merge_partials(dparts), 5)
                 assert m.to_text() == want
                 dev_stats = comp.last_stats
+                # the fold spread over owners (shard.compile_sharded): every
+                # shard's entries split by owning rank; owner o merges its
+                # pieces of all shards -- the per-rank merge time at n ranks
+                # is the max over owners (each would run on its own GPU)
+                from paper_2604_16613_b200 import shard
+                pieces = []
+                for k in range(n):
+                    t = comp.compile_shard(g, k, n, level, on_device=True)
+                    pieces.append(shard.split_by_owner(t.num_detectors, *(x.clone() for x in t.arrays().values()), n))
+                owner_ms, owner_entries, texts = [], [], []
+                for o in range(n):
+                    mine = [gp.DevicePartialTable(parts[0].num_detectors, parts[0].num_observables, *pc[o])
+                            for pc in pieces if pc[o][0].numel()]
+                    ms_o, d_o = p50(lambda: comp.merge_partials(mine), 5)
+                    owner_ms.append(ms_o)
+                    owner_entries.append(int(sum(x.probs.numel() for x in mine)))
+                    texts.append(d_o)
+                assert shard.concat_dems(texts).to_text() == want
                 nbytes = sum(p.probs.nbytes + p.rec_offsets.nbytes + p.rec_words.nbytes + p.rec_bits.nbytes
                              for p in parts)
                 row[f"n{n}"] = {"shard_ms": [round(x, 3) for x in shard_ms], "max_shard_ms": max(shard_ms),
                                 "merge_ms": merge_ms, "merge_dev_ms": dmerge_ms,
                                 "merge_dev_kernel_ms": dev_stats["kernel_ns"] / 1e6, "table_bytes": nbytes,
+                                "owner_merge_ms": [round(x, 3) for x in owner_ms],
+                                "max_owner_merge_ms": max(owner_ms), "owner_entries": owner_entries,
                                 "sources": [p.num_sources for p in parts]}
             out[f"{name}_L{level}"] = row
             print(name, level, json.dumps(row), flush=True)
