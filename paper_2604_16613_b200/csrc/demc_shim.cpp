@@ -2,8 +2,10 @@
 // C ABI: demc::Circuit -> flat gp_circuit_view -> gp_compile -> demc::Dem.
 // Restores the reference signature (compile.hpp:35-36) and its exception
 // behaviour (stepg.cpp:172-174, eec.cpp:44-46 / 52-54).
+#include <algorithm>
 #include <chrono>
 #include <cstdlib>
+#include <functional>
 #include <memory>
 #include <stdexcept>
 #include <string>
@@ -12,9 +14,28 @@
 #include "../../include/demc/compile.hpp"
 #include "../../include/greenpeas.h"
 
+namespace gp {
+void host_parallel_for(size_t n, const std::function<void(size_t)> &f);  // gp_api.cpp
+}
+
 namespace demc {
 
 namespace {
+
+// Work below this many elements stays on the calling thread (a pool wake-up
+// costs more than it saves on small circuits).
+constexpr size_t kParallelMin = 1 << 15;
+
+// Contiguous pieces of [0, n) for the pool.
+template <class F>
+void pieces(size_t n, size_t work, F &&f) {
+    const size_t k = work < kParallelMin ? 1 : std::min<size_t>({64, n, std::max<size_t>(1, work / 8192)});
+    if (k <= 1) {
+        f(0, n);
+        return;
+    }
+    gp::host_parallel_for(k, [&](size_t i) { f(n * i / k, n * (i + 1) / k); });
+}
 
 struct CtxHolder {
     gp_ctx *ctx = nullptr;
@@ -41,34 +62,61 @@ gp_ctx *thread_ctx() {
 }
 
 gp_circuit_view flatten(const Circuit &c, Flat &f) {
-    f = Flat{};
-    f.gate_off.push_back(0);
-    f.noise_off.push_back(0);
-    for (const Layer &L : c.layers) {
-        for (const GateOp &g : L.gates) {
-            f.gate_kind.push_back((uint8_t)g.kind);
-            f.gate_q0.push_back(g.q0);
-            f.gate_q1.push_back(g.q1);
-            f.gate_meas.push_back(g.meas_index);
-            f.gate_flip.push_back(g.flip_prob);
-        }
-        for (const NoiseOp &n : L.noise) {
-            f.noise_kind.push_back((uint8_t)n.kind);
-            f.noise_prob.push_back(n.prob);
-            f.noise_q0.push_back(n.q0);
-            f.noise_q1.push_back(n.q1);
-        }
-        f.gate_off.push_back((uint32_t)f.gate_kind.size());
-        f.noise_off.push_back((uint32_t)f.noise_kind.size());
+    // offsets first (O(layers + detectors)), then the ops and lists copied in
+    // parallel pieces
+    const size_t L = c.layers.size(), D = c.detectors.size(), O = c.observables.size();
+    f.gate_off.resize(L + 1);
+    f.noise_off.resize(L + 1);
+    f.gate_off[0] = f.noise_off[0] = 0;
+    for (size_t i = 0; i < L; i++) {
+        f.gate_off[i + 1] = f.gate_off[i] + (uint32_t)c.layers[i].gates.size();
+        f.noise_off[i + 1] = f.noise_off[i] + (uint32_t)c.layers[i].noise.size();
     }
-    f.det_off.push_back(0);
-    for (const Detector &d : c.detectors) {
-        f.det_meas.insert(f.det_meas.end(), d.measurements.begin(), d.measurements.end());
-        f.det_off.push_back((uint32_t)f.det_meas.size());
-    }
-    f.obs_off.push_back(0);
-    for (const Observable &o : c.observables) {
-        f.obs_meas.insert(f.obs_meas.end(), o.measurements.begin(), o.measurements.end());
+    const size_t G = f.gate_off[L], N = f.noise_off[L];
+    f.gate_kind.resize(G);
+    f.gate_q0.resize(G);
+    f.gate_q1.resize(G);
+    f.gate_meas.resize(G);
+    f.gate_flip.resize(G);
+    f.noise_kind.resize(N);
+    f.noise_prob.resize(N);
+    f.noise_q0.resize(N);
+    f.noise_q1.resize(N);
+    pieces(L, G + N, [&](size_t a, size_t b) {
+        for (size_t i = a; i < b; i++) {
+            size_t x = f.gate_off[i];
+            for (const GateOp &g : c.layers[i].gates) {
+                f.gate_kind[x] = (uint8_t)g.kind;
+                f.gate_q0[x] = g.q0;
+                f.gate_q1[x] = g.q1;
+                f.gate_meas[x] = g.meas_index;
+                f.gate_flip[x] = g.flip_prob;
+                x++;
+            }
+            x = f.noise_off[i];
+            for (const NoiseOp &n : c.layers[i].noise) {
+                f.noise_kind[x] = (uint8_t)n.kind;
+                f.noise_prob[x] = n.prob;
+                f.noise_q0[x] = n.q0;
+                f.noise_q1[x] = n.q1;
+                x++;
+            }
+        }
+    });
+    f.det_off.resize(D + 1);
+    f.det_off[0] = 0;
+    for (size_t d = 0; d < D; d++) f.det_off[d + 1] = f.det_off[d] + (uint32_t)c.detectors[d].measurements.size();
+    f.det_meas.resize(f.det_off[D]);
+    pieces(D, f.det_off[D], [&](size_t a, size_t b) {
+        for (size_t d = a; d < b; d++)
+            std::copy(c.detectors[d].measurements.begin(), c.detectors[d].measurements.end(),
+                      f.det_meas.begin() + f.det_off[d]);
+    });
+    f.obs_off.assign(1, 0);
+    f.obs_meas.clear();
+    for (size_t o = 0; o < O; o++) {
+        const Observable &ob = c.observables[o];
+        f.obs_meas.insert(f.obs_meas.end(), ob.measurements.begin(), ob.measurements.end());
         f.obs_off.push_back((uint32_t)f.obs_meas.size());
     }
     gp_circuit_view v{};
@@ -112,12 +160,16 @@ Dem compile_circuit(const Circuit &c, CorrelationLevel level, uint32_t threads, 
     d.num_detectors = out.num_detectors;
     d.num_observables = out.num_observables;
     d.hyperedges.resize(out.num_edges);
-    for (uint64_t e = 0; e < out.num_edges; e++) {
-        Hyperedge &h = d.hyperedges[e];
-        h.detectors.assign(out.det_ids + out.det_offsets[e], out.det_ids + out.det_offsets[e + 1]);
-        h.observables.assign(out.obs_ids + out.obs_offsets[e], out.obs_ids + out.obs_offsets[e + 1]);
-        h.probability = out.probs[e];
-    }
+    // one allocation per id list, made on the pool's threads for large DEMs
+    // (malloc arenas are per thread)
+    pieces(out.num_edges, out.num_edges * 4, [&](size_t a, size_t b) {
+        for (size_t e = a; e < b; e++) {
+            Hyperedge &h = d.hyperedges[e];
+            h.detectors.assign(out.det_ids + out.det_offsets[e], out.det_ids + out.det_offsets[e + 1]);
+            h.observables.assign(out.obs_ids + out.obs_offsets[e], out.obs_ids + out.obs_offsets[e + 1]);
+            h.probability = out.probs[e];
+        }
+    });
     if (stats) {
         stats->lower_ns = st.lower_ns;
         stats->traverse_ns = st.traverse_ns;

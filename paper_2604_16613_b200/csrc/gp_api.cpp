@@ -150,6 +150,21 @@ gp_status fail(gp_ctx *ctx, gp_status st, const std::string &msg) {
     return st;
 }
 
+}  // namespace
+
+namespace gp {
+// Host tasks [0, n) on the shared pool when it is free (else on the caller):
+// the C++ drop-in's circuit flattening and demc::Dem materialisation.
+void host_parallel_for(size_t n, const std::function<void(size_t)> &f) {
+    PoolLease lease(n > 1);
+    if (lease.pool) lease.pool->run(n, f);
+    else
+        for (size_t i = 0; i < n; i++) f(i);
+}
+}  // namespace gp
+
+namespace {
+
 gp_status cuda_fail(gp_ctx *ctx, cudaError_t e, const char *what) {
     return fail(ctx, GP_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
 }
