@@ -1846,31 +1846,57 @@ gp_status gp_circuit_metrics(const gp_circuit_view *v, uint8_t level, gp_metrics
 
 char *gp_serialize_dem(const gp_dem_view *d, size_t *len) {
     // serialize_dem (dem.cpp:144-157) with format_double = std::to_chars
-    // shortest round-trip (util.hpp:24-28).
-    std::string s;
-    s.reserve(d->num_edges * 40 + 1);
-    char buf[64];
-    for (uint64_t e = 0; e < d->num_edges; e++) {
-        s += "error(";
-        auto r = std::to_chars(buf, buf + sizeof buf, d->probs[e]);
-        s.append(buf, r.ptr);
-        s += ')';
-        for (uint64_t k = d->det_offsets[e]; k < d->det_offsets[e + 1]; k++) {
-            s += " D";
-            r = std::to_chars(buf, buf + sizeof buf, d->det_ids[k]);
-            s.append(buf, r.ptr);
+    // shortest round-trip (util.hpp:24-28). Large DEMs are formatted in edge
+    // pieces on the shared host pool: a first pass formats each piece into the
+    // worker's scratch buffer (kept across calls) for its exact length, the
+    // second formats it again straight into its place in the output.
+    const uint64_t E = d->num_edges;
+    const size_t k = E < 4096 ? 1 : std::min<uint64_t>(256, E / 1024);
+    auto format = [&](uint64_t e0, uint64_t e1, char *p) {
+        char *const end = p + (e1 - e0) * 40 +
+                          ((uint64_t)(d->det_offsets[e1] - d->det_offsets[e0]) + (d->obs_offsets[e1] - d->obs_offsets[e0])) * 12;
+        char *const start = p;
+        for (uint64_t e = e0; e < e1; e++) {
+            std::memcpy(p, "error(", 6);
+            p = std::to_chars(p + 6, end, d->probs[e]).ptr;
+            *p++ = ')';
+            for (uint64_t x = d->det_offsets[e]; x < d->det_offsets[e + 1]; x++) {
+                p[0] = ' ';
+                p[1] = 'D';
+                p = std::to_chars(p + 2, end, d->det_ids[x]).ptr;
+            }
+            for (uint64_t x = d->obs_offsets[e]; x < d->obs_offsets[e + 1]; x++) {
+                p[0] = ' ';
+                p[1] = 'L';
+                p = std::to_chars(p + 2, end, d->obs_ids[x]).ptr;
+            }
+            *p++ = '\n';
         }
-        for (uint64_t k = d->obs_offsets[e]; k < d->obs_offsets[e + 1]; k++) {
-            s += " L";
-            r = std::to_chars(buf, buf + sizeof buf, d->obs_ids[k]);
-            s.append(buf, r.ptr);
-        }
-        s += '\n';
-    }
-    char *out = (char *)std::malloc(s.size() + 1);
-    std::memcpy(out, s.data(), s.size());
-    out[s.size()] = 0;
-    if (len) *len = s.size();
+        return (size_t)(p - start);
+    };
+    // bound of a piece: error(<= 24 chars)\n per edge, " D" / " L" + <= 10 digits per id
+    auto bound = [&](uint64_t e0, uint64_t e1) {
+        return (size_t)((e1 - e0) * 40 +
+                        ((uint64_t)(d->det_offsets[e1] - d->det_offsets[e0]) + (d->obs_offsets[e1] - d->obs_offsets[e0])) * 12);
+    };
+    std::vector<size_t> at(k + 1, 0);
+    gp::host_parallel_for(k, [&](size_t i) {
+        thread_local std::vector<char> scratch;
+        const uint64_t e0 = E * i / k, e1 = E * (i + 1) / k;
+        if (scratch.size() < bound(e0, e1)) scratch.resize(bound(e0, e1));
+        at[i + 1] = format(e0, e1, scratch.data());
+    });
+    for (size_t i = 0; i < k; i++) at[i + 1] += at[i];
+    char *out = (char *)std::malloc(at[k] + 1 + 64);
+    gp::host_parallel_for(k, [&](size_t i) {
+        const uint64_t e0 = E * i / k, e1 = E * (i + 1) / k;
+        thread_local std::vector<char> scratch;
+        if (scratch.size() < bound(e0, e1)) scratch.resize(bound(e0, e1));
+        const size_t n = format(e0, e1, scratch.data());  // (to_chars needs the bound's room)
+        std::memcpy(out + at[i], scratch.data(), n);
+    });
+    out[at[k]] = 0;
+    if (len) *len = at[k];
     return out;
 }
 
