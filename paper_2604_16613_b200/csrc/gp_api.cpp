@@ -592,6 +592,20 @@ repack:  // (again with per-op probabilities when the table overflowed)
                 p.hmap.edge_off = (uint64_t *)(ctx->h_map + m_edge);
             }
         }
+        // One small circuit (D + O <= 64) compiles in one CTA (gp_tiny.cuh)
+        // straight into the mapped output: no per-stage launches.
+        p.tiny = 0;
+        if (mode == gp::kModeFull && count == 1 && !gen && p.out_mapped && !ctx->force_collisions && t.max_W <= 1 &&
+            t.max_l >= 1 && t.sources <= 8192 && !std::getenv("GP_NO_TINY")) {
+            uint32_t cap = 32;
+            while (cap < t.sources) cap <<= 1;
+            const size_t b = gp::tiny_smem_bytes(t.max_n, t.max_l, M[0].M, cap);
+            if (b <= (size_t)200 * 1024) {
+                p.tiny = 1;
+                p.tiny_cap = cap;
+                p.tiny_smem = b;
+            }
+        }
         if (ctx->trav_debug & 4) {  // experiments: per-step walk timestamps of every CTA
             if (!ctx->d_dbg) cudaMalloc(&ctx->d_dbg, (size_t)8192 * 512 * 4 * 8);
             cudaMemsetAsync(ctx->d_dbg, 0, (size_t)8192 * 512 * 4 * 8, ctx->stream);

@@ -89,6 +89,10 @@ struct DevPlan {
     // then lists every bucket's items in `iidx` (boff[b] = {first, count});
     // huge_kernel gathers a listed bucket into `items2` (same positions) and
     // marks its e_item entries with kItem2.
+    // Tiny circuits (one CTA does everything, gp_tiny.cuh): enabled by the
+    // host for single circuits with D + O <= 64; items capacity (power of 2).
+    uint32_t tiny, tiny_cap;
+    size_t tiny_smem;
     uint32_t fused;
     uint32_t fused_move;  // the CTA moves the items into bucket order in items2 (no index list)
     ItemStub *items2;  // [S + 16]
@@ -159,6 +163,8 @@ struct BBGenParams {
     uint64_t gates, noise;  // planned batch totals (the last circuit's check)
     uint32_t *err;          // circuits whose fill disagreed with the host plan
 };
+// Dynamic shared memory of the one-CTA tiny compile (0: does not fit).
+size_t tiny_smem_bytes(uint32_t n, uint32_t l, uint32_t M, uint32_t cap);
 void launch_bbgen_draw(const BBGenParams &g, cudaStream_t st);
 void launch_bbgen_fill(const BBGenParams &g, cudaStream_t st);
 

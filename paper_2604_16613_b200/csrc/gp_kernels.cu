@@ -294,6 +294,7 @@ __global__ void lower_kernel(__grid_constant__ const DevPlan p, uint32_t blocks_
 #include "gp_traverse.cuh"
 #include "gp_walk.cuh"
 #include "gp_bbgen.cuh"
+#include "gp_tiny.cuh"
 namespace {
 
 // Files the traversal's pooled records into per-source slots: the returning
@@ -710,6 +711,18 @@ int enqueue_pipeline(const DevPlan &p, cudaStream_t st, const StageEvents *ev, c
         if (prof) cudaEventRecord(prof[k], st);
     };
     mark(kProfStart);
+    if (p.tiny) {  // one CTA: lowering, Alg. 1, emission, reduce, output (gp_tiny.cuh)
+        smem_optin(tiny::tiny_kernel);
+        tiny::tiny_kernel<<<1, tiny::kThreads, p.tiny_smem, st>>>(p);
+        for (int k = kProfMemset; k < kProfCount; k++) mark(k);
+        if (ev) {
+            cudaEventRecord(ev->lowered, st);
+            cudaEventRecord(ev->traversed, st);
+            cudaEventRecord(ev->reduced, st);
+        }
+        *err = cudaGetLastError();
+        return 1;
+    }
     const uint64_t S = p.tot.sources, NB = p.tot.buckets;
     // Zero fills (one launch): ELLPACK (idle nodes are word 0), leaf rows,
     // per-source record counts, bucket counts, the header.
@@ -840,6 +853,10 @@ reduce:
     if (ev) cudaEventRecord(ev->reduced, st);
     *err = cudaGetLastError();
     return launches;
+}
+
+size_t tiny_smem_bytes(uint32_t n, uint32_t l, uint32_t M, uint32_t cap) {
+    return tiny::Dims{2 * n, l, M, cap}.bytes();
 }
 
 void launch_bbgen_draw(const BBGenParams &g, cudaStream_t st) {

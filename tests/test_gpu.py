@@ -649,3 +649,35 @@ def test_two_process_sharded_compile_and_gather():
     assert res[0]["branches"][0] and res[1]["branches"][0]
     assert res[1]["branches"][1] is None
     assert res[0]["branches"][2][0] > 0 and res[0]["branches"][2][1] > 0
+
+
+# ---------------------------------------------------------------- one-CTA tiny compiles
+
+@pytest.mark.parametrize("fx", FIXTURES, ids=lambda p: p.name)
+def test_tiny_and_general_paths_agree_on_fixtures(fx, monkeypatch):
+    """Single circuits with D + O <= 64 compile in one CTA (gp_tiny.cuh);
+    the general multi-kernel pipeline (GP_NO_TINY) gives the same bytes, and
+    both equal the reference's golden text."""
+    circuit, level, text, golden = fixture_case(fx)
+    comp = gp.Compiler(0)
+    assert comp.compile(circuit, level).to_text() == text
+    monkeypatch.setenv("GP_NO_TINY", "1")
+    assert gp.Compiler(0).compile(circuit, level).to_text() == text
+
+
+@pytest.mark.parametrize("level", [0, 1, 2])
+def test_tiny_path_random_small_circuits(port, level, monkeypatch):
+    """Surface / repetition circuits that fit one word, every level: the
+    one-CTA path equals the oracle and the general pipeline; the launch count
+    shows the one kernel."""
+    cases = [gp.gen_surface(3, 3, 1e-3), gp.gen_surface(3, 5, 2e-3, gp.NOISE_MODEL_SI1000), gp.gen_repetition(5, 4, 1e-2),
+             gp.gen_surface(3, 1, 1e-3)]
+    comp = gp.Compiler(0)
+    for i, g in enumerate(cases):
+        dem = comp.compile(g, level)
+        if i == 0:  # (d3 r3 fits at every level; larger ones may exceed the one-CTA shared memory)
+            assert comp.last_stats["kernel_launches"] == 1
+        assert dem.hyperedges() == port.compile(g.to_circuit(), level)[0]
+        monkeypatch.setenv("GP_NO_TINY", "1")
+        assert gp.Compiler(0).compile(g, level).to_text() == dem.to_text()
+        monkeypatch.delenv("GP_NO_TINY")
