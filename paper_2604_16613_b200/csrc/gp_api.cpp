@@ -508,6 +508,22 @@ repack:  // (again with per-op probabilities when the table overflowed)
     t.groups = 0;
     for (const CircuitMeta &m : M) t.groups += (m.W + tcfg.T - 1) / tcfg.T;
     gp::pack_head(pp, tcfg.T, ctx->h_stage);
+    // One small circuit (D + O <= 64) compiles in one CTA (gp_tiny.cuh) that
+    // reads its image in place from the pinned staging memory (zero copy: no
+    // upload) and writes the mapped output: one launch, no copies.
+    uint32_t tiny_cap = 0;
+    size_t tiny_smem = 0;
+    if (mode == gp::kModeFull && count == 1 && !gen && !ctx->force_collisions && t.max_W <= 1 && t.max_l >= 1 &&
+        t.sources <= 8192 && !std::getenv("GP_NO_TINY")) {
+        uint32_t cap = 32;
+        while (cap < t.sources) cap <<= 1;
+        const size_t b = gp::tiny_smem_bytes(t, M[0], cap);
+        if (b <= (size_t)200 * 1024) {
+            tiny_cap = cap;
+            tiny_smem = b;
+        }
+    }
+    bool uploaded = !tiny_cap;
     if (gen) {  // the head (metas, cumulative tables) and the probability table; the rest on the device
         slice(0, 1, 0, L.lay_gate);
         slice(L.prob_table, 8, 0, t.prob_table_n);
@@ -515,7 +531,7 @@ repack:  // (again with per-op probabilities when the table overflowed)
             return st;
         cudaMemcpyAsync(ctx->bb.h_err, ctx->bb.d_err, 4, cudaMemcpyDeviceToHost, ctx->stream);
     } else if (nchunk == 1) {
-        slice(0, 1, 0, pp.image_bytes());  // the whole image in one copy
+        if (uploaded) slice(0, 1, 0, pp.image_bytes());  // the whole image in one copy
     } else {
         slice(L.lay_meas, 4, 0, t.layer_slots);  // finished prefix tables
         slice(L.lay_src, 4, 0, t.layer_slots);
@@ -592,31 +608,35 @@ repack:  // (again with per-op probabilities when the table overflowed)
                 p.hmap.edge_off = (uint64_t *)(ctx->h_map + m_edge);
             }
         }
-        // One small circuit (D + O <= 64) compiles in one CTA (gp_tiny.cuh)
-        // straight into the mapped output: no per-stage launches.
         p.tiny = 0;
-        if (mode == gp::kModeFull && count == 1 && !gen && p.out_mapped && !ctx->force_collisions && t.max_W <= 1 &&
-            t.max_l >= 1 && t.sources <= 8192 && !std::getenv("GP_NO_TINY")) {
-            uint32_t cap = 32;
-            while (cap < t.sources) cap <<= 1;
-            const size_t b = gp::tiny_smem_bytes(t.max_n, t.max_l, M[0].M, cap);
-            if (b <= (size_t)200 * 1024) {
-                p.tiny = 1;
-                p.tiny_cap = cap;
-                p.tiny_smem = b;
-            }
+        if (tiny_cap && p.out_mapped) {
+            p.tiny = 1;
+            p.tiny_cap = tiny_cap;
+            p.tiny_smem = tiny_smem;
+            p.tiny_meta = M[0];
+            p.img = ctx->h_stage;  // pinned host memory, read in place (unified addressing)
+        } else if (!uploaded) {  // (no mapped output after all: the general pipeline, after the upload)
+            e = cudaMemcpyAsync(ctx->d_img, ctx->h_stage, pp.image_bytes(), cudaMemcpyHostToDevice, ctx->stream);
+            if (e != cudaSuccess) return cuda_fail(ctx, e, "upload");
+            uploaded = true;
         }
         if (ctx->trav_debug & 4) {  // experiments: per-step walk timestamps of every CTA
             if (!ctx->d_dbg) cudaMalloc(&ctx->d_dbg, (size_t)8192 * 512 * 4 * 8);
             cudaMemsetAsync(ctx->d_dbg, 0, (size_t)8192 * 512 * 4 * 8, ctx->stream);
-            p.dbg = t.groups <= 8192 ? ctx->d_dbg : nullptr;
+            p.dbg = t.groups <= 8192 || p.tiny ? ctx->d_dbg : nullptr;
         }
+        static const bool lat = std::getenv("GP_LAT_TRACE") != nullptr;  // experiments: host phase times
+        const uint64_t t_pre = lat ? ns_since(t0) : 0;
         launches += launch_pipeline(ctx, p, &e);
         if (e != cudaSuccess) return cuda_fail(ctx, e, "kernel launch");
         if (!p.out_mapped)
             e = cudaMemcpyAsync(ctx->h_hdr, p.hdr, sizeof(DeviceHeader), cudaMemcpyDeviceToHost, ctx->stream);
         cudaEventRecord(ctx->ev_end, ctx->stream);
+        const uint64_t t_launch = lat ? ns_since(t0) : 0;
         if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+        if (lat)
+            std::fprintf(stderr, "lat: pack %.1f  carve+plan %.1f  launch %.1f  sync %.1f us\n", pack_ns / 1e3,
+                         (t_pre - pack_ns) / 1e3, (t_launch - t_pre) / 1e3, (ns_since(t0) - t_launch) / 1e3);
         if (e != cudaSuccess) return cuda_fail(ctx, e, "device pipeline");
         hdr = p.out_mapped ? *p.hmap.hdr : *ctx->h_hdr;
         const bool retry = hdr.items_overflow || hdr.pool_overflow || hdr.record_overflow ||
@@ -649,7 +669,14 @@ repack:  // (again with per-op probabilities when the table overflowed)
     }
     ctx->last_plan = p;
     ctx->has_plan = true;
-    if (p.dbg) {
+    if (p.dbg && p.tiny) {  // experiments: the one-CTA kernel's phase timestamps
+        uint64_t h[32];
+        cudaMemcpy(h, p.dbg, sizeof h, cudaMemcpyDeviceToHost);
+        std::fprintf(stderr, "tiny phases (us):");
+        for (int i = 1; i < 32 && h[i] >= h[i - 1] && h[i] - h[0] < 1000000; i++)
+            std::fprintf(stderr, " %.2f", (h[i] - h[i - 1]) / 1e3);
+        std::fprintf(stderr, "\n");
+    } else if (p.dbg) {
         const char *path = std::getenv("GP_DEBUG_DUMP");
         std::vector<uint64_t> h((size_t)t.groups * 512 * 4);
         cudaMemcpy(h.data(), p.dbg, h.size() * 8, cudaMemcpyDeviceToHost);
@@ -715,7 +742,7 @@ repack:  // (again with per-op probabilities when the table overflowed)
         ho.edge_off = p.hmap.edge_off;
         if (stats) {
             const double h2d = elapsed_ms(ctx->ev_start, ctx->ev_h2d);
-            const bool g = ctx->graph.used;
+            const bool g = ctx->graph.used || p.tiny;  // (one launch: no stage split)
             const double low = g ? 0 : elapsed_ms(ctx->ev_h2d, ctx->stage_ev.lowered);
             const double trav = g ? 0 : elapsed_ms(ctx->stage_ev.lowered, ctx->stage_ev.traversed);
             const double red = g ? elapsed_ms(ctx->ev_h2d, ctx->stage_ev.reduced)
@@ -767,7 +794,7 @@ repack:  // (again with per-op probabilities when the table overflowed)
     ho.edge_off = (uint64_t *)(ctx->h_out + o_edge);
     if (stats) {
         const double h2d = elapsed_ms(ctx->ev_start, ctx->ev_h2d);
-        const bool g = ctx->graph.used;  // one graph launch: device time without the stage split
+        const bool g = ctx->graph.used || p.tiny;  // one graph launch / one kernel: no stage split
         const double low = g ? 0 : elapsed_ms(ctx->ev_h2d, ctx->stage_ev.lowered);
         const double trav = g ? 0 : elapsed_ms(ctx->stage_ev.lowered, ctx->stage_ev.traversed);
         const double red = g ? elapsed_ms(ctx->ev_h2d, ctx->stage_ev.reduced)

@@ -93,6 +93,7 @@ struct DevPlan {
     // host for single circuits with D + O <= 64; items capacity (power of 2).
     uint32_t tiny, tiny_cap;
     size_t tiny_smem;
+    CircuitMeta tiny_meta;
     uint32_t fused;
     uint32_t fused_move;  // the CTA moves the items into bucket order in items2 (no index list)
     ItemStub *items2;  // [S + 16]
@@ -164,7 +165,7 @@ struct BBGenParams {
     uint32_t *err;          // circuits whose fill disagreed with the host plan
 };
 // Dynamic shared memory of the one-CTA tiny compile (0: does not fit).
-size_t tiny_smem_bytes(uint32_t n, uint32_t l, uint32_t M, uint32_t cap);
+size_t tiny_smem_bytes(const BatchTotals &t, const CircuitMeta &m, uint32_t cap);
 void launch_bbgen_draw(const BBGenParams &g, cudaStream_t st);
 void launch_bbgen_fill(const BBGenParams &g, cudaStream_t st);
 

@@ -713,13 +713,12 @@ int enqueue_pipeline(const DevPlan &p, cudaStream_t st, const StageEvents *ev, c
     mark(kProfStart);
     if (p.tiny) {  // one CTA: lowering, Alg. 1, emission, reduce, output (gp_tiny.cuh)
         smem_optin(tiny::tiny_kernel);
-        tiny::tiny_kernel<<<1, tiny::kThreads, p.tiny_smem, st>>>(p);
-        for (int k = kProfMemset; k < kProfCount; k++) mark(k);
-        if (ev) {
-            cudaEventRecord(ev->lowered, st);
-            cudaEventRecord(ev->traversed, st);
-            cudaEventRecord(ev->reduced, st);
-        }
+        static const int tt = std::getenv("GP_TINY_THREADS") ? std::atoi(std::getenv("GP_TINY_THREADS")) : 0;
+        const uint32_t threads = tt >= 64 && tt <= (int)tiny::kThreads ? (uint32_t)tt & ~31u : tiny::kThreads;
+        tiny::tiny_kernel<<<1, threads, p.tiny_smem, st>>>(p);
+        if (prof)
+            for (int k = kProfMemset; k < kProfCount; k++) mark(k);
+        if (ev) cudaEventRecord(ev->reduced, st);  // (one kernel: no stage split; the host reads `reduced` only)
         *err = cudaGetLastError();
         return 1;
     }
@@ -855,8 +854,10 @@ reduce:
     return launches;
 }
 
-size_t tiny_smem_bytes(uint32_t n, uint32_t l, uint32_t M, uint32_t cap) {
-    return tiny::Dims{2 * n, l, M, cap}.bytes();
+size_t tiny_smem_bytes(const BatchTotals &t, const CircuitMeta &m, uint32_t cap) {
+    const tiny::Head h = tiny::head_of(m.l, m.D, m.O, (uint32_t)t.det_entries, (uint32_t)t.obs_entries,
+                                       t.prob_table_n, 0, 0, 0, t.wide_prob != 0);
+    return tiny::Dims{2 * m.n, m.l, m.M, cap, (uint32_t)h.bytes()}.bytes();
 }
 
 void launch_bbgen_draw(const BBGenParams &g, cudaStream_t st) {
