@@ -278,6 +278,23 @@ void gp_circuit_free(gp_circuit *c);
 gp_circuit_view gp_circuit_get_view(const gp_circuit *c);
 /* Circuit text in the reference grammar (circuit.cpp:328-388 layout). */
 char *gp_circuit_serialize(const gp_circuit *c, size_t *len);
+/* parse_circuit + validate_layers (circuit.cpp:107-326), natively and on the
+ * host pool for large texts: text[len] -> owning circuit (release with
+ * gp_circuit_free). On malformed text returns NULL and *error (malloc'd,
+ * release with gp_free) holds the reference's message: "line N: ..."
+ * (ParseError) or "layer L: ..." (validate_layers' invalid_argument). */
+gp_circuit *gp_parse_circuit(const char *text, size_t len, char **error);
+/* Annotations of a circuit in declaration order, with their layers (the
+ * layout serialize_circuit and demc::Layer::annotations need); valid while
+ * the circuit lives. */
+typedef struct gp_annotation_view {
+    uint32_t layer;
+    uint32_t is_observable;
+    uint32_t id;
+    uint32_t num_meas;
+    const uint32_t *meas; /* absolute, ascending */
+} gp_annotation_view;
+const gp_annotation_view *gp_circuit_annotations(const gp_circuit *c, size_t *count);
 
 #ifdef __cplusplus
 }

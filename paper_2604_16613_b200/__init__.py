@@ -24,6 +24,8 @@ from .api import (  # noqa: F401
     compile_circuit,
     gen_bb,
     gen_bb72_branch,
+    parse_circuit_native,
+    CircuitParseError,
     bb_spec,
     bb72_branch_spec,
     gen_bb144,

@@ -126,6 +126,8 @@ def lib() -> C.CDLL:
         L.gp_circuit_free.argtypes = [vp]
         L.gp_circuit_get_view.argtypes = [vp]
         L.gp_circuit_get_view.restype = CircuitView
+        L.gp_parse_circuit.argtypes = [C.c_char_p, C.c_size_t, C.POINTER(C.c_void_p)]
+        L.gp_parse_circuit.restype = vp
         L.gp_circuit_serialize.argtypes = [vp, C.POINTER(C.c_size_t)]
         L.gp_circuit_serialize.restype = vp
         _lib = L

@@ -417,6 +417,25 @@ def algorithmic_bytes(metrics: dict, edges: int, ids: int) -> dict:
     return {"traverse": trav, "reduce": red, "total": trav + red}
 
 
+class CircuitParseError(ValueError):
+    """gp_parse_circuit's error: the reference's message ("line N: ..." or
+    "layer L: ...")."""
+
+
+def parse_circuit_native(text: str) -> "GenCircuit":
+    """parse_circuit + validate_layers (circuit.cpp:107-326) in native code
+    (gp_parse_circuit; parallel on the host pool for large texts)."""
+    data = text.encode()
+    err = C.c_void_p()
+    h = N.lib().gp_parse_circuit(data, len(data), C.byref(err))
+    if not h:
+        msg = C.string_at(err.value).decode() if err.value else "parse failed"
+        if err.value:
+            N.lib().gp_free(err)
+        raise CircuitParseError(msg)
+    return GenCircuit(h)
+
+
 def gen_repetition(d: int, rounds: int, p: float) -> GenCircuit:
     return GenCircuit(N.lib().gp_gen_repetition(d, rounds, p))
 

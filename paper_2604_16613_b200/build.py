@@ -26,7 +26,7 @@ CUDA_HOME = Path(os.environ.get("CUDA_HOME", "/usr/local/cuda"))
 NVCC = CUDA_HOME / "bin" / "nvcc"
 
 CU_SOURCES = ["gp_kernels.cu"]
-CPP_SOURCES = ["gp_api.cpp", "gp_pack.cpp", "gp_gen.cpp", "demc_shim.cpp"]
+CPP_SOURCES = ["gp_api.cpp", "gp_pack.cpp", "gp_gen.cpp", "gp_parse.cpp", "demc_shim.cpp"]
 HEADERS = ["gp_layout.h", "gp_device.h", "gp_pack.h"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 

@@ -11,6 +11,7 @@
 #include <string>
 #include <vector>
 
+#include "../../include/demc/circuit.hpp"
 #include "../../include/demc/compile.hpp"
 #include "../../include/greenpeas.h"
 
@@ -179,6 +180,45 @@ Dem compile_circuit(const Circuit &c, CorrelationLevel level, uint32_t threads, 
                               .count();
     }
     return d;
+}
+
+Circuit parse_circuit(const std::string &text) {
+    char *err = nullptr;
+    gp_circuit *g = gp_parse_circuit(text.data(), text.size(), &err);
+    if (!g) {
+        std::string m = err ? err : "parse failed";
+        gp_free(err);
+        if (m.rfind("line ", 0) == 0) {  // "line N: msg" -> ParseError(N, msg)
+            const size_t colon = m.find(": ");
+            const size_t line = std::stoul(m.substr(5, colon - 5));
+            throw ParseError(line, m.substr(colon + 2));
+        }
+        throw std::invalid_argument(m);
+    }
+    const gp_circuit_view v = gp_circuit_get_view(g);
+    Circuit c;
+    c.num_qubits = v.num_qubits;
+    c.num_measurements = v.num_measurements;
+    c.layers.resize(v.num_layers);
+    for (uint32_t i = 0; i < v.num_layers; i++) {
+        Layer &L = c.layers[i];
+        for (uint32_t x = v.gate_offsets[i]; x < v.gate_offsets[i + 1]; x++)
+            L.gates.push_back({(GateKind)v.gate_kind[x], v.gate_q0[x], v.gate_q1[x], v.gate_meas[x], v.gate_flip[x]});
+        for (uint32_t x = v.noise_offsets[i]; x < v.noise_offsets[i + 1]; x++)
+            L.noise.push_back({(NoiseKind)v.noise_kind[x], v.noise_prob[x], v.noise_q0[x], v.noise_q1[x]});
+    }
+    for (uint32_t d = 0; d < v.num_detectors; d++)
+        c.detectors.push_back({d, std::vector<uint32_t>(v.det_meas + v.det_offsets[d], v.det_meas + v.det_offsets[d + 1])});
+    for (uint32_t o = 0; o < v.num_observables; o++)
+        c.observables.push_back({o, std::vector<uint32_t>(v.obs_meas + v.obs_offsets[o], v.obs_meas + v.obs_offsets[o + 1])});
+    // annotations, placed in their layers in declaration order
+    size_t n = 0;
+    const gp_annotation_view *a = gp_circuit_annotations(g, &n);
+    for (size_t i = 0; i < n; i++)
+        c.layers[a[i].layer].annotations.push_back(
+            {a[i].is_observable != 0, a[i].id, std::vector<uint32_t>(a[i].meas, a[i].meas + a[i].num_meas)});
+    gp_circuit_free(g);
+    return c;
 }
 
 std::string serialize_dem(const Dem &d) {

@@ -20,24 +20,6 @@
 #include "../../include/greenpeas.h"
 #include "gp_gen.h"
 
-struct gp_circuit {
-    uint32_t num_qubits = 0, num_measurements = 0;
-    std::vector<uint32_t> gate_offsets{0}, noise_offsets{0};
-    std::vector<uint8_t> gate_kind, noise_kind;
-    std::vector<uint32_t> gate_q0, gate_q1, noise_q0, noise_q1;
-    std::vector<int32_t> gate_meas;
-    std::vector<double> gate_flip, noise_prob;
-    std::vector<uint32_t> det_offsets{0}, det_meas, obs_offsets{0}, obs_meas;
-    // Annotation placement for serialization: (layer, is_obs, id, measurements).
-    struct Ann {
-        uint32_t layer;
-        bool is_obs;
-        uint32_t id;
-        std::vector<uint32_t> meas;
-    };
-    std::vector<Ann> anns;
-    uint32_t layers() const { return (uint32_t)gate_offsets.size() - 1; }
-};
 
 namespace {
 
@@ -601,6 +583,15 @@ gp_circuit *gp_gen_bb(uint32_t l, uint32_t m, const uint32_t a[3], const uint32_
 }
 
 void gp_circuit_free(gp_circuit *c) { delete c; }
+
+const gp_annotation_view *gp_circuit_annotations(const gp_circuit *c, size_t *count) {
+    auto &v = const_cast<gp_circuit *>(c)->ann_views;
+    v.clear();
+    for (const auto &a : c->anns)
+        v.push_back({a.layer, a.is_obs ? 1u : 0u, a.id, (uint32_t)a.meas.size(), a.meas.data()});
+    if (count) *count = v.size();
+    return v.data();
+}
 
 gp_circuit_view gp_circuit_get_view(const gp_circuit *c) {
     gp_circuit_view v{};

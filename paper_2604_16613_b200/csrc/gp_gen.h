@@ -10,6 +10,28 @@
 #include "../../include/greenpeas.h"
 #include "gp_layout.h"  // (__host__ / __device__ for host-only compiles)
 
+// Owning flat circuit (include/greenpeas.h gp_circuit): the generators' and
+// the native parser's output.
+struct gp_circuit {
+    uint32_t num_qubits = 0, num_measurements = 0;
+    std::vector<uint32_t> gate_offsets{0}, noise_offsets{0};
+    std::vector<uint8_t> gate_kind, noise_kind;
+    std::vector<uint32_t> gate_q0, gate_q1, noise_q0, noise_q1;
+    std::vector<int32_t> gate_meas;
+    std::vector<double> gate_flip, noise_prob;
+    std::vector<uint32_t> det_offsets{0}, det_meas, obs_offsets{0}, obs_meas;
+    // Annotation placement for serialization: (layer, is_obs, id, measurements).
+    struct Ann {
+        uint32_t layer;
+        bool is_obs;
+        uint32_t id;
+        std::vector<uint32_t> meas;
+    };
+    std::vector<Ann> anns;
+    std::vector<gp_annotation_view> ann_views;  // (gp_circuit_annotations)
+    uint32_t layers() const { return (uint32_t)gate_offsets.size() - 1; }
+};
+
 namespace gp {
 
 struct BBTemplate {
