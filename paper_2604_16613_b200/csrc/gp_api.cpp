@@ -1043,7 +1043,11 @@ struct PipeLane {
 }  // namespace
 
 namespace gp {
-constexpr size_t kLanes = 3;  // sub-batches in flight (staging, image and output buffers)
+constexpr size_t kLanes = 4;         // lanes allocated: sub-batches in flight (staging, image, output buffers)
+// lanes used (GP_PIPE_LANES): with per-sub-batch output regions a lane is
+// reused without waiting for a download; two lanes measured best for 4,096
+// branches (host circuits 13.6 ms against 14.8 with three and 15.0 with four)
+constexpr size_t kLanesDefault = 2;
 struct PipeState {
     PipeLane lane[kLanes];
     cudaStream_t s_in = nullptr, s_out = nullptr;
@@ -1051,6 +1055,11 @@ struct PipeState {
     size_t h_map_cap = 0;
     uint8_t *h_misc = nullptr;  // mapped: bases [(kMaxSub + 1) * 4], status, headers [kMaxSub]
     uint64_t e_hint = 0, ids_hint = 0;
+    // per sub-batch: device output region and completion event (a lane is
+    // reused before its previous sub-batch's download has run)
+    std::vector<uint8_t *> outs;
+    std::vector<size_t> out_caps;
+    std::vector<cudaEvent_t> done;
 };
 void pipe_destroy(PipeState *ps) {
     if (!ps) return;
@@ -1067,6 +1076,10 @@ void pipe_destroy(PipeState *ps) {
     if (ps->s_out) cudaStreamDestroy(ps->s_out);
     if (ps->h_map) cudaFreeHost(ps->h_map);
     if (ps->h_misc) cudaFreeHost(ps->h_misc);
+    for (uint8_t *o : ps->outs)
+        if (o) cudaFree(o);
+    for (cudaEvent_t e : ps->done)
+        if (e) cudaEventDestroy(e);
     delete ps;
 }
 }  // namespace gp
@@ -1074,6 +1087,7 @@ void pipe_destroy(PipeState *ps) {
 namespace {
 
 constexpr size_t kMaxSub = 64, kSubCircuits = 512;
+constexpr bool kRampDefault = false;  // half-size first / last sub-batches (GP_PIPE_RAMP)
 
 gp_status ensure_host_plain(uint8_t **buf, size_t *cap, size_t need) {
     if (*cap >= need) return GP_OK;
@@ -1117,7 +1131,12 @@ gp_status run_batch_pipelined(gp_ctx *ctx, const gp_circuit_view *cs, size_t cou
     // sub-batch is then planned on the host and written on the device
     if (gen && (st = bbgen_draw(ctx, *gen, count, level)) != GP_OK) return st;
     uint32_t gen_pi[gp::kLanes][5] = {};
-    static const size_t sub = std::getenv("GP_PIPE_SUB") ? (size_t)std::atoi(std::getenv("GP_PIPE_SUB")) : kSubCircuits;
+    const char *ps_env = std::getenv("GP_PIPE_SUB");  // tuning knobs (read per call)
+    const size_t sub = ps_env ? std::max<size_t>(64, (size_t)std::atoi(ps_env)) : kSubCircuits;
+    const char *pl_env = std::getenv("GP_PIPE_LANES");
+    const size_t NL = pl_env ? std::min<size_t>(gp::kLanes, std::max(2, std::atoi(pl_env))) : gp::kLanesDefault;
+    const char *pr_env = std::getenv("GP_PIPE_RAMP");
+    const bool ramp = pr_env ? std::atoi(pr_env) != 0 : kRampDefault;
     // (device generation: GP_GEN_SUB tunes its sub-batch size separately;
     // measured 13.2 ms per 4,096 branches at 512, 15.8 at 1,024 -- a lane's
     // next sub-batch waits for its download)
@@ -1178,12 +1197,19 @@ gp_status run_batch_pipelined(gp_ctx *ctx, const gp_circuit_view *cs, size_t cou
     };
     // Download of sub-batch j by the copy engine: sizes and global offsets
     // are in mapped memory (written by its write_kernel) once it is done.
-    DevPlan plans[gp::kLanes];
+    std::vector<DevPlan> plans(P);
     std::vector<uint8_t> downloaded(P, 0);
+    if (ps.outs.size() < P) {
+        ps.outs.resize(P, nullptr);
+        ps.out_caps.resize(P, 0);
+    }
+    while (ps.done.size() < P) {
+        ps.done.push_back(nullptr);
+        cudaEventCreateWithFlags(&ps.done.back(), cudaEventDisableTiming);
+    }
     auto download = [&](size_t j) {
-        PipeLane &l = ps.lane[j % gp::kLanes];
-        const DevPlan &pj = plans[j % gp::kLanes];
-        cudaEventSynchronize(l.ev_done);
+        const DevPlan &pj = plans[j];
+        cudaEventSynchronize(ps.done[j]);
         const DeviceHeader &h = hdrs[j];
         downloaded[j] = 1;
         if (h.num_det_ids == 0xFFFFFFFFu || h.items_overflow || h.record_overflow || h.pool_overflow) {
@@ -1205,7 +1231,6 @@ gp_status run_batch_pipelined(gp_ctx *ctx, const gp_circuit_view *cs, size_t cou
                 cudaMemcpyAsync(hm.edge_off + bC, pj.o_edge_off, (C + 1) * 8, cudaMemcpyDeviceToHost, ps.s_out);
             }
         }
-        cudaEventRecord(l.ev_out, ps.s_out);
     };
     cudaEventRecord(ctx->ev_start, ctx->stream);
     // GP_PIPE_TRACE=1: per sub-batch host pack time and device event times (stderr)
@@ -1213,18 +1238,29 @@ gp_status run_batch_pipelined(gp_ctx *ctx, const gp_circuit_view *cs, size_t cou
     std::vector<cudaEvent_t> tev;
     std::vector<double> tpack;
     for (size_t k = 0; k < P; k++) {
-        PipeLane &ln = ps.lane[k % gp::kLanes];
-        for (size_t j = k >= gp::kLanes ? k - gp::kLanes + 1 : 0; j < k; j++)  // finished ones: download now
-            if (!downloaded[j] && cudaEventQuery(ps.lane[j % gp::kLanes].ev_done) == cudaSuccess) download(j);
-        if (k >= gp::kLanes && !downloaded[k - gp::kLanes]) download(k - gp::kLanes);  // before the lane is reused
+        PipeLane &ln = ps.lane[k % NL];
+        for (size_t j = 0; j < k; j++)  // finished ones: download now (in order)
+            if (!downloaded[j]) {
+                if (cudaEventQuery(ps.done[j]) != cudaSuccess) break;
+                download(j);
+            }
         const auto tp0 = clk::now();
-        const size_t c0 = count * k / P, c1 = count * (k + 1) / P, n = c1 - c0;
+        // sub-batch k: [bound(k), bound(k + 1)); with the ramp the first and
+        // the last are half size (the pipeline fills and drains sooner)
+        auto bound = [&](size_t x) -> size_t {
+            if (!ramp || P < 3) return count * x / P;
+            if (x == 0) return 0;
+            if (x >= P) return count;
+            const double u = 0.5 + (double)(x - 1);  // units: halves at both ends, P - 1 in all
+            return (size_t)((double)count * u / (double)(P - 1));
+        };
+        const size_t c0 = bound(k), c1 = bound(k + 1), n = c1 - c0;
         if (ln.used) cudaEventSynchronize(ln.ev_in);  // the lane's previous staging was uploaded
         gp::PackPlan &pp = ln.pp;
         pp.force_wide = false;
         pp.no_narrow = false;
         if (gen) {
-            if ((st = bbgen_plan(ctx, c0, n, level, pp, gen_pi[k % gp::kLanes])) != GP_OK) return drain(), st;
+            if ((st = bbgen_plan(ctx, c0, n, level, pp, gen_pi[k % NL])) != GP_OK) return drain(), st;
             if ((st = ensure_host_plain(&ln.h_stage, &ln.h_stage_cap, pp.L.total)) != GP_OK)
                 return drain(), fail(ctx, st, "pinned host allocation of " + std::to_string(pp.L.total) + " bytes failed");
         } else {
@@ -1265,7 +1301,7 @@ gp_status run_batch_pipelined(gp_ctx *ctx, const gp_circuit_view *cs, size_t cou
         const uint64_t slabs = tcfg.split ? t.groups * t.max_l : 0;
         const uint64_t sub_ids = std::max<uint64_t>(3 * t.sources + 1024, ids_cap / P * 2);
         const uint64_t sub_items = t.sources + 16;
-        DevPlan &p = plans[k % gp::kLanes];
+        DevPlan &p = plans[k];
         p = DevPlan{};
         p.lay = pp.L;
         p.tot = t;
@@ -1277,15 +1313,12 @@ gp_status run_batch_pipelined(gp_ctx *ctx, const gp_circuit_view *cs, size_t cou
             cudaStreamSynchronize(ln.s_comp);
             if ((st = ensure_device(ctx, &ln.d_ws, &ln.d_ws_cap, need_ws)) != GP_OK) return drain(), st;
         }
-        if (ln.used && (need_out > ln.d_out_cap || pp.L.total > ln.d_img_cap)) {
-            cudaEventSynchronize(ln.ev_out);
-            cudaEventSynchronize(ln.ev_done);
-        }
-        if (ensure_dev_plain(&ln.d_out, &ln.d_out_cap, need_out) != GP_OK ||
+        if (ln.used && pp.L.total > ln.d_img_cap) cudaEventSynchronize(ln.ev_done);
+        if (ensure_dev_plain(&ps.outs[k], &ps.out_caps[k], need_out) != GP_OK ||
             ensure_dev_plain(&ln.d_img, &ln.d_img_cap, pp.L.total) != GP_OK)
             return drain(), fail(ctx, GP_ERR_OUT_OF_MEMORY, "device allocation failed");
         carve(ctx, p, t, ln.d_ws, K, sub_ids, pool, slabs, sub_items, false);
-        carve_out(p, ln.d_out, sub_items, sub_ids, t.C);
+        carve_out(p, ps.outs[k], sub_items, sub_ids, t.C);
         p.img = ln.d_img;
         p.base_in = bases + 4 * k;
         p.base_out = bases + 4 * (k + 1);
@@ -1301,19 +1334,19 @@ gp_status run_batch_pipelined(gp_ctx *ctx, const gp_circuit_view *cs, size_t cou
                                 cudaMemcpyHostToDevice, ps.s_in);
         cudaEventRecord(ln.ev_in, ps.s_in);
         cudaStreamWaitEvent(ln.s_comp, ln.ev_in, 0);
-        if (ln.used) cudaStreamWaitEvent(ln.s_comp, ln.ev_out, 0);  // the lane's download read d_out
         if (gen && e == cudaSuccess &&
-            (st = bbgen_fill(ctx, *gen, c0, level, pp, gen_pi[k % gp::kLanes], ln.d_img, ln.s_comp)) != GP_OK)
+            (st = bbgen_fill(ctx, *gen, c0, level, pp, gen_pi[k % NL], ln.d_img, ln.s_comp)) != GP_OK)
             return drain(), st;
         if (trace) {
             tpack.push_back(ns_since(tp0) / 1e3);
             for (int x = 0; x < 3; x++) tev.push_back(nullptr), cudaEventCreate(&tev.back());
             cudaEventRecord(tev[tev.size() - 3], ps.s_in);
         }
-        cudaEvent_t prev_written = k ? ps.lane[(k - 1) % gp::kLanes].ev_written : nullptr;
+        cudaEvent_t prev_written = k ? ps.lane[(k - 1) % NL].ev_written : nullptr;
         launches += gp::enqueue_pipeline(p, ln.s_comp, nullptr, nullptr, &e, prev_written, ln.ev_written);
         if (trace) cudaEventRecord(tev[tev.size() - 2], ln.s_comp);
         cudaEventRecord(ln.ev_done, ln.s_comp);
+        cudaEventRecord(ps.done[k], ln.s_comp);
         ln.used = true;
         if (e != cudaSuccess) return drain(), cuda_fail(ctx, e, "pipelined launch");
         h2d_bytes += gen ? up + t.prob_table_n * 8 : pp.image_bytes();

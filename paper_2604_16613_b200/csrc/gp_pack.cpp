@@ -373,6 +373,59 @@ void pack_range(HostPool *pool, const gp_circuit_view *cs, PackPlan &pp, uint8_t
             ProbCache pidx{&pp.dict};
             uint32_t comp_tab[8];  // components per noise kind (stepg.cpp:66-103)
             for (uint32_t x = 0; x < 8; x++) comp_tab[x] = components((uint8_t)x, level);
+            if (narrow && !t.wide_prob) {  // the common case: one tight pass per layer, 4-byte words
+                const uint8_t *__restrict gk = v.gate_kind, *__restrict nk = v.noise_kind;
+                const uint32_t *__restrict gq0 = v.gate_q0, *__restrict gq1 = v.gate_q1;
+                const int32_t *__restrict gm = v.gate_meas;
+                const double *__restrict gf = v.gate_flip, *__restrict np = v.noise_prob;
+                const uint32_t *__restrict nq0 = v.noise_q0, *__restrict nq1 = v.noise_q1;
+                uint32_t *__restrict gout = gates32 + m.gate_base - g0;
+                uint32_t *__restrict nout = noise32 + m.noise_base - n0;
+                double *__restrict fout = flip + m.meas_base;
+                uint64_t last_bits = ~0ull;
+                uint32_t last_pi = 0;
+                bool big = false;
+                for (uint32_t i = tk.a; i < tk.b; i++) {
+                    const uint32_t li = m.layer_base + i;
+                    const uint32_t ga = v.gate_offsets[i], gb = v.gate_offsets[i + 1];
+                    const uint32_t na = v.noise_offsets[i], nb = v.noise_offsets[i + 1];
+                    lay_gate[li] = (uint32_t)(m.gate_base + ga - g0);
+                    lay_noise[li] = (uint32_t)(m.noise_base + na - n0);
+                    uint32_t meas = 0;
+                    for (uint32_t g = ga; g < gb; g++) {
+                        const uint32_t kd = gk[g];
+                        const bool ms = kd == GP_GATE_M || kd == GP_GATE_MR;
+                        uint32_t hi = kd == GP_GATE_CX ? gq1[g] : 0;
+                        if (ms) {
+                            hi = (uint32_t)gm[g];
+                            fout[hi] = gf[g];
+                            meas++;
+                        }
+                        put32(&gout[g], narrow_gate(gq0[g], kd, hi));
+                    }
+                    lay_meas[li] = meas;  // count; prefix in pack_finish
+                    uint32_t src = 0;
+                    for (uint32_t o = na; o < nb; o++) {
+                        const uint32_t kd = nk[o];
+                        uint64_t bits;
+                        std::memcpy(&bits, &np[o], 8);
+                        if (bits != last_bits) {  // runs of one probability: one compare
+                            const uint32_t x = pidx(np[o]);
+                            last_bits = bits;
+                            last_pi = x;
+                            if (x >= kNarrowMaxProbs) big = true;
+                        }
+                        const uint32_t q1 = kd == GP_NOISE_DEPOLARIZE2 ? nq1[o] : 0;
+                        put32(&nout[o], narrow_noise(nq0[o], q1, kd, last_pi < kNarrowMaxProbs ? last_pi : 0));
+                        src += comp_tab[kd & 7];
+                    }
+                    lay_src[li] = src;  // count; prefix in pack_finish
+                }
+                if (big) {  // ProbDict::kFull or a 65th probability: repack (wide table or 8-byte words)
+                    if (pp.dict.size() > kNoisePidxMax) pp.need_wide.store(true, std::memory_order_relaxed);
+                    pp.need_wide_words.store(true, std::memory_order_relaxed);
+                }
+            } else
             for (uint32_t i = tk.a; i < tk.b; i++) {
                 const uint32_t li = m.layer_base + i;
                 lay_gate[li] = (uint32_t)(m.gate_base + v.gate_offsets[i] - g0);
