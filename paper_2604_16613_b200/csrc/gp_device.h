@@ -24,6 +24,7 @@ struct TravCfg {
     uint32_t G;          // boundaries per staged group (walk_kernel)
     uint32_t max_comp;   // sources per noise op at this level (6 / 10 / 15): the layer source map
     uint32_t fuse_key;   // direct traversal builds the reduce's sort items (red::key_kernel / scatter_kernel skipped)
+    uint32_t wide;       // split traversal with the walk state in global memory (circuits too wide for on-chip state)
     uint32_t debug;      // experiments only: bit0 skip emission work, bit1 skip node work
 };
 

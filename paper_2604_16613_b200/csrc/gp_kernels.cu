@@ -645,10 +645,13 @@ bool plan_traversal(const BatchTotals &t, int device, TravCfg *cfg, size_t *smem
     // (the copy latency of a boundary's stage hides behind NST-1 boundaries).
     static const uint32_t kBatch[][2] = {{2, 3}, {2, 2}, {3, 3}};
     static const uint32_t kSingle[][2] = {{6, 8}, {4, 8}, {4, 6}, {4, 4}, {3, 3}, {2, 2}};
-    if (T == 1) {  // split traversal: walk_kernel + emit_kernel
+    // split traversal: walk_kernel + emit_kernel; walk_wide_kernel (state in
+    // global memory) when even the shallowest on-chip staging does not fit
+    auto split = [&]() {
         c.T = 1;
         c.direct = t.max_W <= 1;
         c.split = 1;
+        c.wide = 0;
         // Threads per column (a power-of-two number of warps) and unrolled
         // nodes per thread: the fewest warps with <= kWalkNpl nodes each (one
         // warp needs no CTA barrier at all); GP_WALK_WPC overrides (tuning).
@@ -660,19 +663,27 @@ bool plan_traversal(const BatchTotals &t, int device, TravCfg *cfg, size_t *smem
         c.walk_npt = npl <= 2 ? 2 : npl <= 4 ? 4 : npl <= 8 ? 8 : npl <= 16 ? 16 : 0;
         // Deepest staging that fits: groups of G boundaries, NST groups in flight.
         static const uint32_t kOpts[][2] = {{3, 8}, {2, 8}, {3, 4}, {2, 4}, {2, 2}, {2, 1}};
-        for (const auto &o : kOpts) {
-            const walk::WalkDims d(o[0], o[1], t.max_n, t.max_layer_meas, t.max_l);
-            if (d.total_bytes() <= budget) {
-                c.NST = o[0];
-                c.G = o[1];
-                c.R = 2;
-                *cfg = c;
-                *smem = d.total_bytes();
-                return true;
+        if (!std::getenv("GP_WALK_WIDE"))  // (tests: force the global-state walk)
+            for (const auto &o : kOpts) {
+                const walk::WalkDims d(o[0], o[1], t.max_n, t.max_layer_meas, t.max_l);
+                if (d.total_bytes() <= budget) {
+                    c.NST = o[0];
+                    c.G = o[1];
+                    c.R = 2;
+                    *cfg = c;
+                    *smem = d.total_bytes();
+                    return true;
+                }
             }
-        }
-        return false;
-    }
+        c.wide = 1;
+        c.walk_threads = 1024;
+        c.NST = c.G = 1;
+        c.R = 2;
+        *cfg = c;
+        *smem = (size_t)((t.max_l + 4) & ~3u) * 5 + 64;  // layer table + liveness flags
+        return true;
+    };
+    if (T == 1) return split();
     for (;; T = (T + 1) / 2) {
         const bool batch = T > 1;
         const uint32_t(*opts)[2] = batch ? kBatch : kSingle;
@@ -700,7 +711,7 @@ bool plan_traversal(const BatchTotals &t, int device, TravCfg *cfg, size_t *smem
                 return true;
             }
         }
-        if (T == 1) return false;
+        if (T == 1) return split();  // (the fused kernel's ring does not fit)
     }
 }
 
@@ -771,7 +782,12 @@ int enqueue_pipeline(const DevPlan &p, cudaStream_t st, const StageEvents *ev, c
             smem_optin(kern);
             kern<<<(uint32_t)p.tot.groups, p.trav.walk_threads, p.trav_smem, st>>>(p, p.trav);
         };
-        walk_dispatch(p.trav.walk_threads / 32, p.trav.walk_npt, launch);
+        if (p.trav.wide) {
+            smem_optin(walk::walk_wide_kernel);
+            walk::walk_wide_kernel<<<(uint32_t)p.tot.groups, 1024, p.trav_smem, st>>>(p, p.trav);
+        } else {
+            walk_dispatch(p.trav.walk_threads / 32, p.trav.walk_npt, launch);
+        }
         mark(kProfTraverse);
         walk::emit_kernel<<<kEmitBlocks, 256, 0, st>>>(p);
         launches += 2;

@@ -302,6 +302,108 @@ __global__ void __launch_bounds__(32 * WPC) walk_kernel(__grid_constant__ const 
             mbar_wait(&full[(uint32_t)x % L.NST], (uint32_t)(x / (int)L.NST) & 1u);
 }
 
+// Circuits too wide for on-chip state (2n nodes x 2 buffers + staging beyond
+// shared memory, about 4,800 qubits): the same walk with the state in global
+// memory -- each boundary's column IS its slab (L2-resident), read back as
+// the next boundary's successor values; ELLPACK rows and leaf words are read
+// in place. One CTA per word, one block barrier (with the zero vote) per
+// boundary. Slower than walk_kernel, but any width the workspace holds.
+__global__ void __launch_bounds__(1024) walk_wide_kernel(__grid_constant__ const DevPlan p, TravCfg cfg) {
+    extern __shared__ __align__(128) uint8_t smem[];
+    __shared__ CircuitMeta s_meta;
+    __shared__ uint32_t s_min_m, s_max_m, s_grp, s_circ;
+    const uint32_t tid = threadIdx.x, nt = blockDim.x;
+    if (tid == 0) {
+        const uint32_t *circ_grp = arr<uint32_t>(p, p.lay.circ_grp);
+        const uint32_t c = find_u32(circ_grp, p.tot.C, blockIdx.x);
+        s_meta = arr<CircuitMeta>(p, p.lay.meta)[c];
+        s_grp = blockIdx.x - circ_grp[c];
+        s_circ = c;
+        s_min_m = 0xFFFFFFFFu;
+        s_max_m = 0;
+    }
+    __syncthreads();
+    const CircuitMeta m = s_meta;
+    const uint32_t word = s_grp, n2 = 2 * m.n, circ_id = s_circ;
+    uint4 *hdrs = p.slab_hdr + (uint64_t)blockIdx.x * p.slab_stride;
+    {  // measurement window of the word's detectors / observables (as walk_kernel)
+        const uint32_t b0 = word * 64, b1 = min(b0 + 64, m.D + m.O);
+        const uint32_t *doff = arr<uint32_t>(p, p.lay.det_off) + m.det_base;
+        const uint32_t *dms = arr<uint32_t>(p, p.lay.det_meas);
+        uint32_t lo = 0xFFFFFFFFu, hi = 0;
+        for (uint32_t d = b0 + tid; d < min(b1, m.D); d += nt)
+            for (uint32_t k = doff[d]; k < doff[d + 1]; k++) {
+                lo = min(lo, dms[k]);
+                hi = max(hi, dms[k]);
+            }
+        const uint32_t *ooff = arr<uint32_t>(p, p.lay.obs_off) + m.obs_base;
+        const uint32_t *oms = arr<uint32_t>(p, p.lay.obs_meas);
+        for (uint32_t b = max(b0, m.D); b < b1; b++)
+            for (uint32_t k = ooff[b - m.D] + tid; k < ooff[b - m.D + 1]; k += nt) {
+                lo = min(lo, oms[k]);
+                hi = max(hi, oms[k]);
+            }
+        if (lo != 0xFFFFFFFFu) {
+            atomicMin(&s_min_m, lo);
+            atomicMax(&s_max_m, hi);
+        }
+    }
+    __syncthreads();
+    const uint32_t min_m = s_min_m, max_m = s_max_m;
+    if (min_m == 0xFFFFFFFFu) {
+        for (uint32_t x = tid; x < p.slab_stride; x += nt) hdrs[x] = make_uint4(0, 0, 0, kSlabDead);
+        return;
+    }
+    const uint32_t lay_w = (cfg.max_l + 4) & ~3u;
+    uint32_t *lay_meas = reinterpret_cast<uint32_t *>(smem);
+    uint8_t *s_live = smem + (size_t)lay_w * 4;
+    {
+        const uint32_t *gm = arr<uint32_t>(p, p.lay.lay_meas) + m.layer_base;
+        for (uint32_t i = tid; i <= m.l; i += nt) lay_meas[i] = gm[i];
+    }
+    __syncthreads();
+    auto layer_of = [&](uint32_t mm) {
+        uint32_t lo = 0, hi = m.l;
+        while (hi - lo > 1) {
+            const uint32_t mid = (lo + hi) >> 1;
+            if (lay_meas[mid] <= mm) lo = mid;
+            else hi = mid;
+        }
+        return (int)lo;
+    };
+    const int first_layer = layer_of(min_m);
+    const int b_hi = layer_of(max_m) - 1;
+    const int b_lo = (int)min(p.shard_lo, 0x7FFFFFFFu);
+    const uint32_t estride = ell_stride(m.n);
+    const uint32_t *ell = p.ell + m.ell_base;
+    const uint64_t *leaf = p.leaf + m.leaf_base + (uint64_t)word * leaf_stride(m.M);
+    uint64_t *slab0 = p.slab + (uint64_t)blockIdx.x * p.slab_stride * p.slab_words;
+    int j = 0;
+    for (int b = b_hi; b >= b_lo && b >= 0; b--, j++) {
+        const uint32_t *row = ell + (uint64_t)b * estride;
+        const uint64_t *nxt = j ? slab0 + (uint64_t)(j - 1) * p.slab_words : nullptr;  // S_{b+1} (0 at the top)
+        uint64_t *g = slab0 + (uint64_t)j * p.slab_words;
+        uint64_t any = 0;
+        for (uint32_t s = tid; s < n2; s += nt) {
+            const uint32_t e = row[s], idx = e & kSuccIdx;
+            uint64_t acc = (e & kSuccNotSelf) || !nxt ? 0 : nxt[s];
+            if (e & kSuccOther) acc ^= (e & kSuccLeaf) ? leaf[idx] : (nxt ? nxt[idx] : 0);
+            g[s] = acc;
+            any |= acc;
+        }
+        const bool live = __syncthreads_or(any != 0) != 0;  // (also orders this column before the next reads it)
+        if (tid == 0) s_live[j] = live;
+        if ((!live && first_layer > b) || b <= b_lo) {
+            j++;
+            break;
+        }
+    }
+    __syncthreads();
+    for (uint32_t x = tid; x < p.slab_stride; x += nt)
+        hdrs[x] = (int)x < j ? make_uint4(circ_id, word, (uint32_t)(b_hi - (int)x), s_live[x] ? kSlabLive : kSlabZero)
+                             : make_uint4(0, 0, 0, kSlabDead);
+}
+
 // Files one signature record of `src`: word index and its nonzero bits.
 __device__ __forceinline__ void put_record(const DevPlan &p, uint64_t src, uint32_t word, uint64_t bits) {
     const uint32_t j = atomicAdd(&p.cnt[src], 1u);

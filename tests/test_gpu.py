@@ -681,3 +681,29 @@ def test_tiny_path_random_small_circuits(port, level, monkeypatch):
         monkeypatch.setenv("GP_NO_TINY", "1")
         assert gp.Compiler(0).compile(g, level).to_text() == dem.to_text()
         monkeypatch.delenv("GP_NO_TINY")
+
+
+# ---------------------------------------------------------------- circuits too wide for on-chip walk state
+
+@pytest.mark.parametrize("name,level", [("surface_d11_r11_si1000", 1), ("bb144_r12_uniform", 2),
+                                        ("surface_d25_r25_paper", 0)])
+def test_global_state_walk_matches_reference(name, level, monkeypatch):
+    """walk_wide_kernel (the walk state in global memory, the fallback for
+    circuits beyond ~4,800 qubits) forced on the BASELINE circuits: the DEM
+    hashes equal the reference's (tests/golden/full_size.json)."""
+    monkeypatch.setenv("GP_WALK_WIDE", "1")
+    g = FULL_MAKERS[name]()
+    comp = gp.Compiler(0)
+    dem = comp.compile(g, level)
+    assert sha(dem.to_text()) == FULL[name]["levels"][str(level)]["dem_sha256"]
+
+
+def test_circuit_wider_than_shared_memory(ref):
+    """Surface d = 51, 2 rounds: 5,201 qubits, beyond the on-chip walk state
+    (round 1 failed with "circuit too wide"); compiled through the global-state
+    walk, its DEM text equals the reference's."""
+    g = gp.gen_surface(51, 2, 1e-3)
+    assert g.num_qubits > 5000
+    got = gp.Compiler(0).compile(g, 0).to_text()
+    want, _ = ref.parse(g.to_text()).compile(0)
+    assert got == want
