@@ -135,10 +135,16 @@ __device__ __forceinline__ bool mbar_try_wait_sleep(uint64_t *bar, uint32_t pari
 
 // Bounded wait: a protocol bug traps (a CUDA error the host reports) instead
 // of hanging the device (a few seconds of suspended try_waits).
+// A failed try leaves the warp asleep (__nanosleep, growing to 256 ns):
+// measured, the suspend-time hint alone still re-polls often enough to cost
+// ~15 % of a traversal's issued instructions.
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
-    uint32_t spins = 0;
-    while (!mbar_try_wait_sleep(bar, parity))
-        if (++spins > 200000u) __trap();
+    uint32_t spins = 0, ns = 32;
+    while (!mbar_try_wait_sleep(bar, parity)) {
+        if (++spins > 20000000u) __trap();
+        __nanosleep(ns);
+        ns = ns < 256 ? 2 * ns : ns;
+    }
 }
 
 __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {

@@ -790,18 +790,50 @@ __device__ bool group_bucket(const DevPlan &p, const Team &tm, uint32_t b, uint3
     }
     tm.sync();
     if (tm.any(inc)) return false;
-    // 2. members grouped by representative; sorted ascending fold per group
+    // 2. members grouped by representative (any order); each group's end
+    // offset replaces its (now zero) count; the hash table is free again and
+    // holds each member's slot
     const uint32_t G = scan_groups(tm, w, n);
     constexpr bool kWarp = std::is_same<Team, WarpTeam>::value;
     for (uint32_t i = t0; i < n; i += nt) {
         const uint32_t r = w.rep[i];
-        w.mp[w.off[r] + atomicSub(&w.cnt[r], 1u) - 1] = it.prob(i);
+        const uint32_t pos = w.off[r] + atomicSub(&w.cnt[r], 1u) - 1;
+        w.mp[pos] = it.prob(i);
+        w.tab[i] = (uint16_t)pos;
     }
     tm.sync();
+    for (uint32_t g = t0; g < G; g += nt) w.cnt[w.grp[g]] = g + 1 < G ? w.off[w.grp[g + 1]] : n;
+    tm.sync();
+    // every member's rank in its group by (value, slot), all members at once:
+    // each group sorted ascending in place, then folded from 0 by one thread
+    // (dem.cpp:97-106). A NaN (no order) sends the bucket to fold_sorted.
+    bool nan = false;
+    for (uint32_t i = t0; i < n; i += nt) {
+        const uint32_t r = w.rep[i], o = w.off[r], e = w.cnt[r], me = w.tab[i];
+        const double v = w.mp[me];
+        nan |= v != v;
+        uint32_t rank = 0;
+        for (uint32_t a = o; a < e; a++) {
+            const double x = w.mp[a];
+            rank += (x < v) || (x == v && a < me);
+        }
+        w.tab[i] = (uint16_t)(o + rank);
+    }
+    const bool any_nan = tm.any(nan);  // (also the barrier between the ranks and the moves)
+    if (!any_nan) {
+        for (uint32_t i = t0; i < n; i += nt) w.mp[w.tab[i]] = it.prob(i);
+        tm.sync();
+    }
     for (uint32_t g = t0; g < G; g += nt) {
         const uint32_t r = w.grp[g];
-        const uint32_t o = w.off[r], e = g + 1 < G ? w.off[w.grp[g + 1]] : n;
-        w.mp[o] = fold_sorted(w.mp, o, e);
+        const uint32_t o = w.off[r], e = w.cnt[r];
+        double acc = 0.0;
+        if (any_nan) {
+            acc = fold_sorted(w.mp, o, e);
+        } else {
+            for (uint32_t a = o; a < e; a++) acc = merge_prob(acc, w.mp[a]);
+        }
+        w.mp[o] = acc;
     }
     tm.sync();
     // 3. groups in canonical order. A warp with at most 32 groups ranks them

@@ -386,8 +386,10 @@ __global__ void __launch_bounds__(800, 1) traverse_kernel(__grid_constant__ cons
             if (j >= (int)L.NST) {  // wait until boundary b + NST released stage k
                 const uint32_t par = (uint32_t)(j / (int)L.NST - 1) & 1u;
                 bool ok = false;
-                while (!(ok = mbar_try_wait_sleep(&stage_empty[k], par, 2000)))  // (re-checks s_stop)
+                while (!(ok = mbar_try_wait_sleep(&stage_empty[k], par, 2000))) {  // (re-checks s_stop)
                     if (b < s_stop) break;
+                    __nanosleep(512);
+                }
                 if (!ok) break;
             }
             if (b < s_stop) break;  // below the node warps' stopping boundary: nothing to stage
