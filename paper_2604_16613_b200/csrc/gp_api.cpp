@@ -653,9 +653,9 @@ repack:  // (again with per-op probabilities when the table overflowed)
             continue;
         }
         if (hdr.record_overflow) {  // a signature spans more words than inline slots
-            K = std::min<uint32_t>(16, std::max<uint32_t>(hdr.record_overflow, 2 * K));
-            if (hdr.record_overflow > 16)
-                return fail(ctx, GP_ERR_UNSUPPORTED, "signature spans more than 16 detector words");
+            K = std::min<uint32_t>(64, std::max<uint32_t>(hdr.record_overflow, 2 * K));  // (red::kMaxRecords)
+            if (hdr.record_overflow > 64)
+                return fail(ctx, GP_ERR_UNSUPPORTED, "signature spans more than 64 detector words");
             ctx->record_slots = K;
             continue;
         }
@@ -1513,7 +1513,7 @@ gp_status gp_ctx_set_option(gp_ctx *ctx, int option, int64_t value) {
             ctx->force_collisions = value != 0;
             return GP_OK;
         case GP_OPT_RECORD_SLOTS:
-            if (value < 1 || value > 16) return fail(ctx, GP_ERR_INVALID_ARGUMENT, "record slots must be 1..16");
+            if (value < 1 || value > 64) return fail(ctx, GP_ERR_INVALID_ARGUMENT, "record slots must be 1..64");
             ctx->record_slots = (uint32_t)value;
             return GP_OK;
         case GP_OPT_SYNC_TIMING:

@@ -35,9 +35,13 @@ namespace red {
 constexpr uint32_t kBucketThreads = 128, kWarpItems = 256;  // bucket_kernel: a warp groups up to kWarpItems
 
 
-// Slots of source s's records sorted by word (insertion sort, n <= 16).
+// Records per source the exact paths handle (signatures spanning up to this
+// many nonzero 64-bit words; the host grows the record slots up to it).
+constexpr uint32_t kMaxRecords = 64;
+
+// Slots of source s's records sorted by word (insertion sort, n <= kMaxRecords).
 __device__ __forceinline__ uint32_t sig_order(const DevPlan &p, uint64_t s, uint32_t n, uint8_t *ord) {
-    uint32_t tile[16];
+    uint32_t tile[kMaxRecords];
     for (uint32_t x = 0; x < n; x++) {
         const uint32_t t = p.rtile[rec_at(p, s, x)];
         uint32_t b = x;
@@ -61,14 +65,14 @@ struct SeqIt {
     uint32_t n, D, r, phase;  // phase 0: detectors, 1: observables, 2: done
     uint64_t bits;
     uint32_t tile;
-    uint8_t ord[16];
+    uint8_t ord[kMaxRecords];
 
     __device__ void init(const DevPlan &pl, uint64_t src, uint32_t d) {
         rtile = pl.rtile + src;
         rbits = pl.rbits + src;
         stride = pl.tot.sources;
         D = d;
-        n = min(pl.cnt[src], 16u);
+        n = min(pl.cnt[src], kMaxRecords);
         sig_order(pl, src, n, ord);
         phase = 0;
         r = 0;
@@ -449,7 +453,7 @@ __device__ __forceinline__ uint32_t key_ndno(const Item &it) {
 // Id counts of any item's signature (an incomplete one: from its records).
 __device__ __forceinline__ uint32_t item_ndno(const DevPlan &p, const Item &it, BucketCtx c) {
     if (it.complete()) return key_ndno(it);
-    const uint32_t s = it.src(), n = min(p.cnt[s], 16u);
+    const uint32_t s = it.src(), n = min(p.cnt[s], kMaxRecords);
     uint32_t nd = 0, no = 0;
     for (uint32_t x = 0; x < n; x++) {
         const uint64_t b = p.rbits[rec_at(p, s, x)], dm = det_mask(p.rtile[rec_at(p, s, x)], c.D);
@@ -1165,8 +1169,8 @@ __global__ void write_kernel(__grid_constant__ const DevPlan p, const uint4 *out
                     for (uint64_t ob = q.obs; ob; ob &= ob - 1) p.o_obs[wo++] = (uint32_t)__ffsll((long long)ob) - 1;
                 } else {  // ids from the representative's records, in word order
                     const uint32_t r = q.src();
-                    uint8_t ord[16];
-                    const uint32_t n = min(p.cnt[r], 16u);
+                    uint8_t ord[kMaxRecords];
+                    const uint32_t n = min(p.cnt[r], kMaxRecords);
                     sig_order(p, r, n, ord);
                     for (uint32_t x = 0; x < n; x++) {
                         const uint32_t t = p.rtile[rec_at(p, r, ord[x])];

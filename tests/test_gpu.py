@@ -707,3 +707,21 @@ def test_circuit_wider_than_shared_memory(ref):
     got = gp.Compiler(0).compile(g, 0).to_text()
     want, _ = ref.parse(g.to_text()).compile(0)
     assert got == want
+
+
+def test_signature_spanning_many_words(ref):
+    """A measurement flip whose signature has detectors in 18 different
+    64-bit words (more than round 1's 16-record limit): the record slots grow
+    on overflow and the DEM text equals the reference's."""
+    n = 1100
+    lines = [f"M(0.01) {' '.join(str(q) for q in range(n))}", "X_ERROR(0.02) 0 5 70"]
+    # detector d holds measurement d, and measurement 0 when d is a multiple of 64
+    for d in range(n):
+        recs = {n - d}
+        if d % 64 == 0 and d:
+            recs.add(n)
+        lines.append("DETECTOR " + " ".join(f"rec[-{k}]" for k in sorted(recs)))
+    text = "\n".join(lines) + "\n"
+    want, _ = ref.parse(text).compile(0)
+    comp = gp.Compiler(0)
+    assert comp.compile(gp.parse_circuit(text), 0).to_text() == want
