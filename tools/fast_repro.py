@@ -1,6 +1,8 @@
 """One batch compile of BB72 branch circuits (for ncu captures of the reduce)."""
 import sys
-sys.path.insert(0, '/root/repo')
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 import paper_2604_16613_b200 as gp  # noqa: E402
 from bench import views_of  # noqa: E402
 

@@ -1,4 +1,5 @@
-"""Compile one workload a few times (for ncu captures)."""
+"""Compile one workload a few times (for ncu captures; `--workload d3` is the
+one-CTA small path)."""
 import argparse, sys
 from pathlib import Path
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
@@ -17,7 +18,7 @@ if a.workload == "branches":
         comp.compile_batch(gens, a.level)
 else:
     g = {"bb144": lambda: gp.gen_bb144(), "d11": lambda: gp.gen_surface(11, 11, 1e-3, gp.NOISE_MODEL_SI1000),
-         "d25": lambda: gp.gen_surface(25, 25, 1e-3)}[a.workload]()
+         "d25": lambda: gp.gen_surface(25, 25, 1e-3), "d3": lambda: gp.gen_surface(3, 3, 1e-3)}[a.workload]()
     for _ in range(a.iters):
         d = comp.compile(g, a.level)
     print(a.workload, d.num_edges, comp.last_stats)
