@@ -1207,11 +1207,19 @@ gp_status run_batch_pipelined(gp_ctx *ctx, const gp_circuit_view *cs, size_t cou
         ps.done.push_back(nullptr);
         cudaEventCreateWithFlags(&ps.done.back(), cudaEventDisableTiming);
     }
+    // GP_PIPE_TRACE=1: per sub-batch host pack time and device event times (stderr)
+    const bool trace = std::getenv("GP_PIPE_TRACE") != nullptr;
+    // six events per sub-batch: upload start / end, kernels start / end,
+    // download start / end; host: pack start / enqueue end
+    std::vector<cudaEvent_t> tev(trace ? 6 * P : 0, nullptr);
+    for (cudaEvent_t &ev : tev) cudaEventCreate(&ev);
+    std::vector<double> tpack0(P, 0.0), tpack1(P, 0.0);
     auto download = [&](size_t j) {
         const DevPlan &pj = plans[j];
         cudaEventSynchronize(ps.done[j]);
         const DeviceHeader &h = hdrs[j];
         downloaded[j] = 1;
+        if (trace) cudaEventRecord(tev[6 * j + 4], ps.s_out);
         if (h.num_det_ids == 0xFFFFFFFFu || h.items_overflow || h.record_overflow || h.pool_overflow) {
             *status |= 2;
         } else {
@@ -1231,12 +1239,9 @@ gp_status run_batch_pipelined(gp_ctx *ctx, const gp_circuit_view *cs, size_t cou
                 cudaMemcpyAsync(hm.edge_off + bC, pj.o_edge_off, (C + 1) * 8, cudaMemcpyDeviceToHost, ps.s_out);
             }
         }
+        if (trace) cudaEventRecord(tev[6 * j + 5], ps.s_out);
     };
     cudaEventRecord(ctx->ev_start, ctx->stream);
-    // GP_PIPE_TRACE=1: per sub-batch host pack time and device event times (stderr)
-    static const bool trace = std::getenv("GP_PIPE_TRACE") != nullptr;
-    std::vector<cudaEvent_t> tev;
-    std::vector<double> tpack;
     for (size_t k = 0; k < P; k++) {
         PipeLane &ln = ps.lane[k % NL];
         for (size_t j = 0; j < k; j++)  // finished ones: download now (in order)
@@ -1244,7 +1249,7 @@ gp_status run_batch_pipelined(gp_ctx *ctx, const gp_circuit_view *cs, size_t cou
                 if (cudaEventQuery(ps.done[j]) != cudaSuccess) break;
                 download(j);
             }
-        const auto tp0 = clk::now();
+        if (trace) tpack0[k] = ns_since(t0) / 1e3;
         // sub-batch k: [bound(k), bound(k + 1)); with the ramp the first and
         // the last are half size (the pipeline fills and drains sooner)
         auto bound = [&](size_t x) -> size_t {
@@ -1327,6 +1332,7 @@ gp_status run_batch_pipelined(gp_ctx *ctx, const gp_circuit_view *cs, size_t cou
         // stream); the upload overwrites the lane's image only once the lane's
         // previous kernels are done reading it
         if (ln.used) cudaStreamWaitEvent(ps.s_in, ln.ev_done, 0);
+        if (trace) cudaEventRecord(tev[6 * k], ps.s_in);
         const uint64_t up = gen ? pp.L.lay_gate : pp.image_bytes();  // device generation: the head only
         cudaError_t e = cudaMemcpyAsync(ln.d_img, ln.h_stage, up, cudaMemcpyHostToDevice, ps.s_in);
         if (gen && e == cudaSuccess)
@@ -1338,13 +1344,15 @@ gp_status run_batch_pipelined(gp_ctx *ctx, const gp_circuit_view *cs, size_t cou
             (st = bbgen_fill(ctx, *gen, c0, level, pp, gen_pi[k % NL], ln.d_img, ln.s_comp)) != GP_OK)
             return drain(), st;
         if (trace) {
-            tpack.push_back(ns_since(tp0) / 1e3);
-            for (int x = 0; x < 3; x++) tev.push_back(nullptr), cudaEventCreate(&tev.back());
-            cudaEventRecord(tev[tev.size() - 3], ps.s_in);
+            cudaEventRecord(tev[6 * k + 1], ps.s_in);
+            cudaEventRecord(tev[6 * k + 2], ln.s_comp);
         }
         cudaEvent_t prev_written = k ? ps.lane[(k - 1) % NL].ev_written : nullptr;
         launches += gp::enqueue_pipeline(p, ln.s_comp, nullptr, nullptr, &e, prev_written, ln.ev_written);
-        if (trace) cudaEventRecord(tev[tev.size() - 2], ln.s_comp);
+        if (trace) {
+            cudaEventRecord(tev[6 * k + 3], ln.s_comp);
+            tpack1[k] = ns_since(t0) / 1e3;
+        }
         cudaEventRecord(ln.ev_done, ln.s_comp);
         cudaEventRecord(ps.done[k], ln.s_comp);
         ln.used = true;
@@ -1354,8 +1362,6 @@ gp_status run_batch_pipelined(gp_ctx *ctx, const gp_circuit_view *cs, size_t cou
     }
     for (size_t j = 0; j < P; j++)
         if (!downloaded[j]) download(j);
-    if (trace)
-        for (size_t k = 0; k < P; k++) cudaEventRecord(tev[3 * k + 2], ps.s_out);
     const uint64_t pack_ns = ns_since(t0);
     cudaEventRecord(ctx->ev_h2d, ctx->stream);
     drain();
@@ -1365,11 +1371,11 @@ gp_status run_batch_pipelined(gp_ctx *ctx, const gp_circuit_view *cs, size_t cou
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(ctx, e, "pipelined batch");
     if (trace) {
-        for (size_t k = 0; k < tpack.size(); k++) {
-            std::fprintf(stderr, "sub %zu pack %.0f us  upload done %.0f  kernels done %.0f  copy-out done %.0f (us from start)\n", k,
-                         tpack[k], elapsed_ms(ctx->ev_start, tev[3 * k]) * 1e3, elapsed_ms(ctx->ev_start, tev[3 * k + 1]) * 1e3,
-                         elapsed_ms(ctx->ev_start, tev[3 * k + 2]) * 1e3);
-        }
+        auto at = [&](size_t x) { return elapsed_ms(ctx->ev_start, tev[x]) * 1e3; };
+        for (size_t k = 0; k < P; k++)
+            std::fprintf(stderr, "sub %zu host %.0f-%.0f  up %.0f-%.0f  kern %.0f-%.0f  down %.0f-%.0f (us)\n", k,
+                         tpack0[k], tpack1[k], at(6 * k), at(6 * k + 1), at(6 * k + 2), at(6 * k + 3), at(6 * k + 4),
+                         at(6 * k + 5));
         for (cudaEvent_t ev : tev) cudaEventDestroy(ev);
     }
     if (*status & 4) return fail(ctx, GP_ERR_UNSUPPORTED, "batch exceeds 2^32 detector or observable ids; split it");
