@@ -53,6 +53,9 @@ __host__ __device__ inline uint32_t noise_q0(uint64_t w) { return (uint32_t)(w &
 __host__ __device__ inline uint32_t noise_q1(uint64_t w) { return (uint32_t)(w >> kNoiseQubitBits & kNoiseQubitMask); }
 __host__ __device__ inline uint32_t noise_kind(uint64_t w) { return (uint32_t)(w >> kNoiseKindShift & 3); }
 __host__ __device__ inline uint32_t noise_pidx(uint64_t w) { return (uint32_t)(w >> kNoisePidxShift); }
+// DEPOLARIZE2 component c (0..14) -> mask of (q0 X, q0 Z, q1 X, q1 Z) rows
+// (stepg.cpp:66-103 component order), as packed nibbles: no table in memory.
+__host__ __device__ inline uint32_t dep2_mask(uint32_t c) { return (uint32_t)(0xEBF7D639CA25184ull >> (4 * c)) & 15u; }
 
 // Narrow upload (BatchTotals.narrow: every circuit of the batch has at most
 // 4096 qubits and 32768 measurements, and the batch at most 64 distinct noise

@@ -224,7 +224,6 @@ __global__ void __launch_bounds__(kThreads, 1) tiny_kernel(__grid_constant__ con
     }
     // the emission's inputs of this thread's first noise op (its word came in
     // the first round)
-    constexpr uint8_t kMask[15] = {4, 8, 1, 5, 2, 10, 12, 9, 3, 6, 13, 7, 15, 11, 14};
     const double *ptab = s_ptab;
     const double *nprob = arr<double>(p, p.lay.noise_prob);
     const double *flip = arr<double>(p, p.lay.meas_flip) + m.meas_base;
@@ -288,7 +287,7 @@ __global__ void __launch_bounds__(kThreads, 1) tiny_kernel(__grid_constant__ con
                 const uint64_t c = row[2 * op.q1], dz = row[2 * op.q1 + 1];
                 const uint32_t nc = level == 0 ? 6 : level == 1 ? 10 : 15;
                 for (uint32_t x = 0; x < nc; x++) {
-                    const uint32_t mk = kMask[x];
+                    const uint32_t mk = dep2_mask(x);
                     f(((mk & 1) ? a : 0) ^ ((mk & 2) ? bz : 0) ^ ((mk & 4) ? c : 0) ^ ((mk & 8) ? dz : 0), op.pe);
                 }
             }

@@ -406,23 +406,28 @@ __global__ void __launch_bounds__(800, 1) traverse_kernel(__grid_constant__ cons
                 h->noise_shift = (uint32_t)(((uint64_t)(noise + n0) & 15ull) >> 3);
                 h->src_shift = (uint32_t)(((uint64_t)(nsrc + n0) & 15ull) >> 2);
                 uint32_t bytes = estride * 4;
-                uint32_t leaf_b[8] = {};
-                uint64_t leaf_a[8] = {};
-                for (uint32_t w = 0; w < tw; w++) {
+                // leaf row slices [mb, me) of the tw words, 16-byte aligned
+                // (addresses recomputed in the issue loop: no local arrays)
+                auto leaf_slice = [&](uint32_t w, uint64_t *a) {
                     const uint64_t *row = leaf + (uint64_t)(t0 + w) * leaf_stride(m.M);
-                    leaf_a[w] = (uint64_t)(row + mb) & ~15ull;
-                    h->leaf_shift[w] = (uint32_t)(((uint64_t)(row + mb) & 15ull) >> 3);
-                    leaf_b[w] = me > mb ? (uint32_t)((((uint64_t)(row + me) + 15) & ~15ull) - leaf_a[w]) : 0;
-                    bytes += leaf_b[w];
+                    *a = (uint64_t)(row + mb) & ~15ull;
+                    return me > mb ? (uint32_t)((((uint64_t)(row + me) + 15) & ~15ull) - *a) : 0u;
+                };
+                for (uint32_t w = 0; w < tw; w++) {
+                    uint64_t a;
+                    bytes += leaf_slice(w, &a);
+                    h->leaf_shift[w] = (uint32_t)(((uint64_t)(leaf + (uint64_t)(t0 + w) * leaf_stride(m.M) + mb) & 15ull) >> 3);
                 }
                 const uint32_t nb = n1 > n0 ? (uint32_t)(ne - na) : 0, sb = n1 > n0 ? (uint32_t)(se - sa) : 0;
                 bytes += nb + sb;
                 fence_proxy_async();
                 mbar_arrive_expect_tx(&stage_full[k], bytes);
                 bulk_g2s(L.ell(smem, k), ell + (uint64_t)b * estride, estride * 4, &stage_full[k]);
-                for (uint32_t w = 0; w < tw; w++)
-                    if (leaf_b[w]) bulk_g2s(L.leaf(smem, k) + (size_t)w * L.leaf_w, (const void *)leaf_a[w], leaf_b[w],
-                                            &stage_full[k]);
+                for (uint32_t w = 0; w < tw; w++) {
+                    uint64_t a;
+                    const uint32_t lb = leaf_slice(w, &a);
+                    if (lb) bulk_g2s(L.leaf(smem, k) + (size_t)w * L.leaf_w, (const void *)a, lb, &stage_full[k]);
+                }
                 if (nb) bulk_g2s(L.noise(smem, k), (const void *)na, nb, &stage_full[k]);
                 if (sb) bulk_g2s(L.src(smem, k), (const void *)sa, sb, &stage_full[k]);
             }
@@ -494,7 +499,6 @@ __global__ void __launch_bounds__(800, 1) traverse_kernel(__grid_constant__ cons
                 emit_source<TM>(p, src_flip + mm, t0, tw, v, direct, kc, flip[mm]);
             }
         }
-        constexpr uint8_t kMask[15] = {4, 8, 1, 5, 2, 10, 12, 9, 3, 6, 13, 7, 15, 11, 14};
         PoolWriter pw{kPoolInvalid, 0};
         for (int j = 0; b_hi - j >= 0; j++) {
             const int b = b_hi - j;
@@ -532,7 +536,7 @@ __global__ void __launch_bounds__(800, 1) traverse_kernel(__grid_constant__ cons
                     const uint32_t kind = noise_kind(wd), c = ls - s_src[lo];
                     const uint32_t q0 = noise_q0(wd), q1 = noise_q1(wd);
                     uint32_t mk = kind == 0 ? 1u : kind == 1 ? 2u : kind == 2 ? (c == 0 ? 1u : c == 1 ? 2u : 3u)
-                                                                              : (uint32_t)kMask[c];
+                                                                              : dep2_mask(c);
                     if (kc.sbkt) {  // rows known to be zero are not read (most sources are empty)
                         const uint32_t *nzb = L.nzb(smem, r);
                         const uint32_t r0 = 2 * q0, r1 = 2 * q1;
@@ -587,7 +591,7 @@ __global__ void __launch_bounds__(800, 1) traverse_kernel(__grid_constant__ cons
                                                                           : (level == 0 ? 6 : level == 1 ? 10 : 15);
 #pragma unroll
                             for (int c = 0; c < 15; c++) {
-                                uint32_t mk = kMask[c];
+                                uint32_t mk = dep2_mask(c);
                                 if (kind == 0) mk = 1;
                                 else if (kind == 1) mk = 2;
                                 else if (kind == 2) mk = c == 0 ? 1 : c == 1 ? 2 : 3;
@@ -630,7 +634,7 @@ __global__ void __launch_bounds__(800, 1) traverse_kernel(__grid_constant__ cons
                     if (!anyw) continue;
                     const uint32_t nc = level == 0 ? 6 : level == 1 ? 10 : 15;
                     for (uint32_t c = 0; c < nc; c++) {
-                        const uint32_t mk = kMask[c];
+                        const uint32_t mk = dep2_mask(c);
                         uint64_t v[TM];
 #pragma unroll
                         for (int w = 0; w < TM; w++) {

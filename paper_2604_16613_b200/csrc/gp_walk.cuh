@@ -421,7 +421,6 @@ __global__ void __launch_bounds__(256) emit_kernel(__grid_constant__ const DevPl
     const CircuitMeta *meta = arr<CircuitMeta>(p, p.lay.meta);
     const uint32_t *lay_noise = arr<uint32_t>(p, p.lay.lay_noise);
     const uint64_t *noise = p.noise_words();
-    constexpr uint8_t kMask[15] = {4, 8, 1, 5, 2, 10, 12, 9, 3, 6, 13, 7, 15, 11, 14};
     // Noise ops at live boundaries: one CTA per slab.
     for (uint64_t sl = blockIdx.x; sl < used; sl += gridDim.x) {
         const uint4 h = p.slab_hdr[sl];
@@ -452,7 +451,7 @@ __global__ void __launch_bounds__(256) emit_kernel(__grid_constant__ const DevPl
             } else {
                 const uint32_t nc = level == 0 ? 6 : level == 1 ? 10 : 15;
                 for (uint32_t c = 0; c < nc; c++) {
-                    const uint32_t mk = kMask[c];
+                    const uint32_t mk = dep2_mask(c);
                     const uint64_t v = ((mk & 1) ? x0 : 0) ^ ((mk & 2) ? z0 : 0) ^ ((mk & 4) ? x1 : 0) ^
                                        ((mk & 8) ? z1 : 0);
                     if (v) put_record(p, src + c, h.y, v);
