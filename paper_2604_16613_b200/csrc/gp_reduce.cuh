@@ -619,10 +619,13 @@ __device__ __forceinline__ uint32_t emit_group(const DevPlan &p, const Item *ite
 //   4. one edge per group in that order.
 // Items stay in global memory (the bucket's contiguous run; L1-resident).
 
+// Table index source for a complete key (the table compares full keys, so
+// this only spreads): the three words folded by rotations, one multiply.
 __device__ __forceinline__ uint32_t item_hash(const Item &it) {
-    uint64_t h = mix64(0x9e3779b97f4a7c15ull ^ it.obs);
-    h = mix64(h ^ it.k0);
-    h = mix64(h ^ it.k1);
+    uint64_t h = it.k0 ^ (it.k1 << 17 | it.k1 >> 47) ^ (it.obs << 41 | it.obs >> 23);
+    h ^= h >> 32;
+    h *= 0x9e3779b97f4a7c15ull;
+    h ^= h >> 29;
     return (uint32_t)(h >> 32);
 }
 
@@ -768,7 +771,10 @@ template <class Team, class Acc>
 __device__ bool group_bucket(const DevPlan &p, const Team &tm, uint32_t b, uint32_t base, uint32_t n,
                              const Acc &it, GroupWs &w) {
     const uint32_t t0 = tm.t0(), nt = tm.nt();
-    for (uint32_t x = t0; x < w.tcap; x += nt) w.tab[x] = 0xFFFF;
+    if (((uintptr_t)w.tab & 7) == 0)  // (tcap >= 64: whole 8-byte words)
+        for (uint32_t x = t0; x < w.tcap / 4; x += nt) reinterpret_cast<uint64_t *>(w.tab)[x] = ~0ull;
+    else
+        for (uint32_t x = t0; x < w.tcap; x += nt) w.tab[x] = 0xFFFF;
     for (uint32_t x = t0; x < n; x += nt) w.cnt[x] = 0;
     tm.sync();
     // 1. representatives: hash + full key compare
@@ -848,12 +854,22 @@ __device__ bool group_bucket(const DevPlan &p, const Team &tm, uint32_t b, uint3
         uint32_t rank = 0;
         Item me{};
         if (lane < G) me = it.load(mine);
-        for (uint32_t h = 0; h < G; h++) {  // the others' keys by shuffle (all lanes take part)
-            Item o;
-            o.k0 = __shfl_sync(0xffffffffu, me.k0, h);
-            o.k1 = __shfl_sync(0xffffffffu, me.k1, h);
-            o.obs = __shfl_sync(0xffffffffu, me.obs, h);
-            rank += (lane < G && h != lane && key_cmp(o, me) < 0) ? 1u : 0u;
+        // the others' first key words by shuffle (all lanes take part); keys
+        // equal there (rare) are compared in full in a second round
+        bool tie = false;
+        for (uint32_t h = 0; h < G; h++) {
+            const uint64_t o0 = __shfl_sync(0xffffffffu, me.k0, h);
+            rank += (lane < G && o0 < me.k0) ? 1u : 0u;
+            tie |= lane < G && h != lane && o0 == me.k0;
+        }
+        if (__any_sync(0xffffffffu, tie)) {
+            for (uint32_t h = 0; h < G; h++) {
+                Item o;
+                o.k0 = __shfl_sync(0xffffffffu, me.k0, h);
+                o.k1 = __shfl_sync(0xffffffffu, me.k1, h);
+                o.obs = __shfl_sync(0xffffffffu, me.obs, h);
+                rank += (tie && h != lane && o.k0 == me.k0 && key_cmp(o, me) < 0) ? 1u : 0u;
+            }
         }
         __syncwarp();
         if (lane < G) w.grp[rank] = (uint16_t)mine;
