@@ -43,6 +43,20 @@ __device__ __forceinline__ uint32_t find_u32(const uint32_t *base, uint32_t C, u
     return lo;
 }
 
+// find_u32 by a whole (converged) warp: 32 probes per round, so C = 4,096
+// takes 3 rounds of loads instead of 12 dependent ones.
+__device__ __forceinline__ uint32_t find_u32_warp(const uint32_t *base, uint32_t C, uint32_t x) {
+    const uint32_t lane = threadIdx.x & 31;
+    uint32_t lo = 0, hi = C;  // base[lo] <= x; the answer is in [lo, hi)
+    while (hi - lo > 1) {
+        const uint32_t step = (hi - lo + 31) >> 5, pos = lo + lane * step;
+        const uint32_t m = __ballot_sync(0xffffffffu, pos < hi && base[pos] <= x);  // lanes 0..k (lane 0: pos = lo)
+        lo += (31 - __clz(m)) * step;
+        hi = min(hi, lo + step);
+    }
+    return lo;
+}
+
 __device__ __forceinline__ uint32_t find_u64(const uint64_t *base, uint32_t C, uint64_t x) {
     uint32_t lo = 0, hi = C;
     while (hi - lo > 1) {
@@ -177,7 +191,7 @@ __global__ void lower_kernel(__grid_constant__ const DevPlan p, uint32_t blocks_
         const uint32_t lane = threadIdx.x & 31;
         if (gw >= p.tot.layers) return;
         const uint32_t *circ_layer = arr<uint32_t>(p, p.lay.circ_layer);
-        const uint32_t c = find_u32(circ_layer, C, (uint32_t)gw);
+        const uint32_t c = find_u32_warp(circ_layer, C, (uint32_t)gw);  // (gw is warp-uniform)
         const CircuitMeta m = meta[c];
         const uint32_t i = (uint32_t)gw - circ_layer[c];
         const uint32_t li = m.layer_base + i;

@@ -582,6 +582,13 @@ __device__ __forceinline__ BucketCtx bucket_ctx(const DevPlan &p, uint64_t b) {
     return BucketCtx{m.D, (uint32_t)b - m.bucket_base};
 }
 
+// bucket_ctx for a whole converged warp (one bucket per warp).
+__device__ __forceinline__ BucketCtx bucket_ctx_warp(const DevPlan &p, uint64_t b) {
+    const uint32_t c = find_u32_warp(arr<uint32_t>(p, p.lay.circ_bkt), p.tot.C, (uint32_t)b);
+    const CircuitMeta &m = arr<CircuitMeta>(p, p.lay.meta)[c];
+    return BucketCtx{m.D, (uint32_t)b - m.bucket_base};
+}
+
 // Group starting at sorted position i0 of a bucket (at(x): the bucket index
 // of the item at sorted position x): walks to the group's end, folding the
 // members' probabilities -- already ascending -- from 0 (merge_prob,
@@ -1142,7 +1149,7 @@ __global__ void write_kernel(__grid_constant__ const DevPlan p, const uint4 *out
         if (ne == 0) continue;
         const uint4 o = p.oscan[b];  // (edges, det ids, obs ids) before this bucket
         const uint32_t base = p.boff[b].x;
-        const BucketCtx c = bucket_ctx(p, b);
+        const BucketCtx c = bucket_ctx_warp(p, b);
         const Item *items = items_of(p), *items2 = reinterpret_cast<const Item *>(p.items2);
         uint32_t dcar = 0, ocar = 0;
         for (uint32_t k0 = 0; k0 < ne; k0 += 32) {
