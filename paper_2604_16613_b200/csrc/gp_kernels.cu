@@ -877,7 +877,7 @@ reduce:
     mark(kProfScanOut);
     if (wait_write) cudaStreamWaitEvent(st, wait_write, 0);  // the previous sub-batch's bases
     {
-        const uint64_t threads = std::max<uint64_t>(NB * 32, p.tot.C + 1);
+        const uint64_t threads = std::max<uint64_t>(NB, p.tot.C + 1);  // (a warp per 32 buckets)
         red::write_kernel<<<(uint32_t)std::min<uint64_t>(blocks_for(threads, 128), 148 * 256), 128, 0, st>>>(
             p, &totals[1]);
         launches++;

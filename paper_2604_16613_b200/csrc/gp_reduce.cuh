@@ -582,13 +582,6 @@ __device__ __forceinline__ BucketCtx bucket_ctx(const DevPlan &p, uint64_t b) {
     return BucketCtx{m.D, (uint32_t)b - m.bucket_base};
 }
 
-// bucket_ctx for a whole converged warp (one bucket per warp).
-__device__ __forceinline__ BucketCtx bucket_ctx_warp(const DevPlan &p, uint64_t b) {
-    const uint32_t c = find_u32_warp(arr<uint32_t>(p, p.lay.circ_bkt), p.tot.C, (uint32_t)b);
-    const CircuitMeta &m = arr<CircuitMeta>(p, p.lay.meta)[c];
-    return BucketCtx{m.D, (uint32_t)b - m.bucket_base};
-}
-
 // Group starting at sorted position i0 of a bucket (at(x): the bucket index
 // of the item at sorted position x): walks to the group's end, folding the
 // members' probabilities -- already ascending -- from 0 (merge_prob,
@@ -1144,43 +1137,70 @@ __global__ void write_kernel(__grid_constant__ const DevPlan p, const uint4 *out
         const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
         if (t <= p.tot.C) p.o_edge_off[t] = bE + (t < p.tot.C ? p.oscan[meta[t].bucket_base].x : tot.x);
     }
-    for (uint64_t b = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; b < NB; b += warps) {
-        const uint32_t ne = p.ecount[b];
-        if (ne == 0) continue;
-        const uint4 o = p.oscan[b];  // (edges, det ids, obs ids) before this bucket
-        const uint32_t base = p.boff[b].x;
-        const BucketCtx c = bucket_ctx_warp(p, b);
-        const Item *items = items_of(p), *items2 = reinterpret_cast<const Item *>(p.items2);
+    // One warp per 32 consecutive buckets, their edges packed onto the lanes
+    // (a bucket holds ~9 edges: one bucket per warp would idle most lanes).
+    // Edge j of the chunk is edge oscan[B0].x + j of the output; its id
+    // offsets are the chunk's (oscan[B0]) plus a warp scan of the id counts.
+    const Item *items = items_of(p), *items2 = reinterpret_cast<const Item *>(p.items2);
+    const uint32_t *circ_bkt = arr<uint32_t>(p, p.lay.circ_bkt);
+    for (uint64_t B0 = (((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 32; B0 < NB; B0 += warps * 32) {
+        const uint64_t b = B0 + lane;
+        const uint32_t ne = b < NB ? p.ecount[b] : 0;
+        uint32_t st = ne;  // inclusive scan of the edge counts
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const uint32_t x = __shfl_up_sync(0xffffffffu, st, d);
+            if (lane >= (uint32_t)d) st += x;
+        }
+        const uint32_t T = __shfl_sync(0xffffffffu, st, 31), start = st - ne;
+        if (T == 0) continue;
+        uint32_t c = find_u32_warp(circ_bkt, p.tot.C, (uint32_t)B0);  // B0's circuit; lanes step forward
+        uint32_t base = 0, q0 = 0, D = 0;
+        if (ne) {
+            while (c + 1 < p.tot.C && circ_bkt[c + 1] <= (uint32_t)b) c++;
+            const CircuitMeta &m = meta[c];
+            base = p.boff[b].x;
+            q0 = (uint32_t)b - m.bucket_base;
+            D = m.D;
+        }
+        const uint4 o = p.oscan[B0];  // (edges, det ids, obs ids) before bucket B0
         uint32_t dcar = 0, ocar = 0;
-        for (uint32_t k0 = 0; k0 < ne; k0 += 32) {
-            const uint32_t k = k0 + lane;
+        for (uint32_t j0 = 0; j0 < T; j0 += 32) {
+            const uint32_t j = j0 + lane;
+            uint32_t l = 0;  // the lane holding edge j's bucket: largest l with start_l <= j
+#pragma unroll
+            for (uint32_t step = 16; step > 0; step >>= 1)
+                if (__shfl_sync(0xffffffffu, start, l + step) <= j) l += step;
+            const uint32_t k = j - __shfl_sync(0xffffffffu, start, l);
+            const uint32_t bb = __shfl_sync(0xffffffffu, base, l);
+            const BucketCtx cx{__shfl_sync(0xffffffffu, D, l), __shfl_sync(0xffffffffu, q0, l)};
             uint32_t nd = 0, no = 0;
-            if (k < ne) {
-                const uint32_t v = p.e_ndno[base + k];
+            if (j < T) {
+                const uint32_t v = p.e_ndno[bb + k];
                 nd = v & 0xFFFF;
                 no = v >> 16;
             }
             uint32_t di = nd, oi = no;  // inclusive warp scans
 #pragma unroll
             for (int d = 1; d < 32; d <<= 1) {
-                const uint32_t a = __shfl_up_sync(0xffffffffu, di, d), cc = __shfl_up_sync(0xffffffffu, oi, d);
+                const uint32_t x = __shfl_up_sync(0xffffffffu, di, d), y = __shfl_up_sync(0xffffffffu, oi, d);
                 if (lane >= (uint32_t)d) {
-                    di += a;
-                    oi += cc;
+                    di += x;
+                    oi += y;
                 }
             }
-            if (k < ne) {
-                const uint64_t e = (uint64_t)o.x + k;
+            if (j < T) {
+                const uint64_t e = (uint64_t)o.x + j;
                 const uint32_t d0 = o.y + dcar + di - nd, o0 = o.z + ocar + oi - no;
                 p.o_det_off[e] = (uint32_t)(bD + d0);
                 p.o_obs_off[e] = (uint32_t)(bO + o0);
-                p.o_prob[e] = p.e_prob[base + k];
-                const uint32_t ei = p.e_item[base + k];
+                p.o_prob[e] = p.e_prob[bb + k];
+                const uint32_t ei = p.e_item[bb + k];
                 const Item q = load_item((ei & kItem2 ? items2 : items) + (ei & ~kItem2));
                 uint32_t wd = d0, wo = o0;
                 if (q.complete()) {  // detectors q0 - 1, then the differences; observables by mask
-                    if (c.q0) {
-                        uint32_t id = c.q0 - 1;
+                    if (cx.q0) {
+                        uint32_t id = cx.q0 - 1;
                         p.o_det[wd++] = id;
                         for (uint32_t f = 0; f < kKeyFields; f++) {
                             const uint32_t dv = key_get(q, f);
@@ -1201,8 +1221,8 @@ __global__ void write_kernel(__grid_constant__ const DevPlan p, const uint4 *out
                         while (bits) {
                             const uint32_t id = t * 64 + (uint32_t)__ffsll((long long)bits) - 1;
                             bits &= bits - 1;
-                            if (id < c.D) p.o_det[wd++] = id;
-                            else p.o_obs[wo++] = id - c.D;
+                            if (id < cx.D) p.o_det[wd++] = id;
+                            else p.o_obs[wo++] = id - cx.D;
                         }
                     }
                 }
