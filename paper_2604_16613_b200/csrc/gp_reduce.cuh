@@ -146,12 +146,14 @@ __device__ __forceinline__ uint32_t key_get(const Item &it, uint32_t f) {
     return (uint32_t)(((f < 5 ? it.k0 : it.k1) >> (52 - 12 * (f % 5))) & 0xFFF);
 }
 
-// Detectors after d0 in a complete key (its nonzero fields form a prefix).
+// Detectors after d0 in a complete key. Its nonzero fields form a prefix, so
+// the lowest set field bit names the last one (field f of a word spans bits
+// 52 - 12 f .. 63 - 12 f; k1's bits 0..3 are flags).
 __device__ __forceinline__ uint32_t key_len(const Item &it) {
-    uint32_t n = 0;
-#pragma unroll
-    for (uint32_t f = 0; f < kKeyFields; f++) n += key_get(it, f) != 0;
-    return n;
+    const uint64_t h = it.k1 & ~15ull;
+    if (h) return 5 + (63 - (uint32_t)(__ffsll((long long)h) - 1)) / 12 + 1;
+    if (it.k0) return (63 - (uint32_t)(__ffsll((long long)it.k0) - 1)) / 12 + 1;
+    return 0;
 }
 
 constexpr uint64_t kItemIncomplete = 1, kItemHasDet = 2;
