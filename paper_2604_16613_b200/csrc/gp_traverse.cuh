@@ -529,6 +529,7 @@ __global__ void __launch_bounds__(800, 1) traverse_kernel(__grid_constant__ cons
                     for (uint32_t c = 0; c < nc; c++) smap[f + c] = (uint16_t)o;
                 }
                 named_sync(kBarEmit, (int)emit_threads);
+                const uint32_t *nzb = kc.sbkt ? L.nzb(smem, r) : nullptr;  // (per boundary)
                 for (uint32_t i = te; i < ns; i += emit_threads) {
                     const uint32_t ls = sfirst + i;
                     const uint32_t lo = smap[i];
@@ -538,7 +539,6 @@ __global__ void __launch_bounds__(800, 1) traverse_kernel(__grid_constant__ cons
                     uint32_t mk = kind == 0 ? 1u : kind == 1 ? 2u : kind == 2 ? (c == 0 ? 1u : c == 1 ? 2u : 3u)
                                                                               : dep2_mask(c);
                     if (kc.sbkt) {  // rows known to be zero are not read (most sources are empty)
-                        const uint32_t *nzb = L.nzb(smem, r);
                         const uint32_t r0 = 2 * q0, r1 = 2 * q1;
                         const uint32_t b0 = nzb[r0 >> 5] >> (r0 & 31), b1 = kind == 3 ? nzb[r1 >> 5] >> (r1 & 31) : 0u;
                         mk &= (b0 & 3u) | (b1 & 3u) << 2;
