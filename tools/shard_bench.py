@@ -1,7 +1,10 @@
 """Fault-range sharding timing on one GPU: each shard of a
 single circuit compiled in turn (what rank k would run), the merge of all
 partial tables, and the whole-circuit compile for comparison. Wall-clock per
-call through the C ABI, p50 over repeats (host packing + upload included)."""
+call through the C ABI, p50 over repeats (host packing + upload included).
+shard_ms keeps each partial table on the device (what a rank of
+compile_sharded runs before the owner exchange); shard_host_table_ms also
+copies it out to host arrays."""
 import json
 import sys
 import time
@@ -34,11 +37,17 @@ def main():
             want = dem.to_text()
             row = {"whole_ms": whole_ms, "edges": dem.num_edges}
             for n in (2, 4, 8):
-                shard_ms, parts = [], []
+                shard_ms, shard_host_ms, parts = [], [], []
                 for k in range(n):
+                    # a rank's shard as compile_sharded runs it: the partial
+                    # table stays on the device for the owner exchange
+                    comp.compile_shard(g, k, n, level, on_device=True)
+                    ms, _ = p50(lambda: comp.compile_shard(g, k, n, level, on_device=True), 5)
+                    shard_ms.append(ms)
+                    # the same with the table copied out to host arrays
                     comp.compile_shard(g, k, n, level)
                     ms, part = p50(lambda: comp.compile_shard(g, k, n, level), 5)
-                    shard_ms.append(ms)
+                    shard_host_ms.append(ms)
                     parts.append(part)
                 merge_ms, m = p50(lambda: comp.merge_partials(parts), 5)
                 assert m.to_text() == want
@@ -71,6 +80,7 @@ def main():
                 nbytes = sum(p.probs.nbytes + p.rec_offsets.nbytes + p.rec_words.nbytes + p.rec_bits.nbytes
                              for p in parts)
                 row[f"n{n}"] = {"shard_ms": [round(x, 3) for x in shard_ms], "max_shard_ms": max(shard_ms),
+                                "shard_host_table_ms": [round(x, 3) for x in shard_host_ms],
                                 "merge_ms": merge_ms, "merge_dev_ms": dmerge_ms,
                                 "merge_dev_kernel_ms": dev_stats["kernel_ns"] / 1e6, "table_bytes": nbytes,
                                 "owner_merge_ms": [round(x, 3) for x in owner_ms],
