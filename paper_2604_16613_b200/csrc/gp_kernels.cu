@@ -877,9 +877,13 @@ reduce:
     mark(kProfScanOut);
     if (wait_write) cudaStreamWaitEvent(st, wait_write, 0);  // the previous sub-batch's bases
     {
-        const uint64_t threads = std::max<uint64_t>(NB, p.tot.C + 1);  // (a warp per 32 buckets)
+        // buckets per warp: 32 for batches; single circuits keep >= ~4,700
+        // warps (32 per SM) busy with fewer
+        uint32_t cb = 32;
+        while (cb > 1 && NB < (uint64_t)cb * 148 * 32) cb >>= 1;
+        const uint64_t threads = std::max<uint64_t>((NB + cb - 1) / cb * 32, p.tot.C + 1);
         red::write_kernel<<<(uint32_t)std::min<uint64_t>(blocks_for(threads, 128), 148 * 256), 128, 0, st>>>(
-            p, &totals[1]);
+            p, &totals[1], cb);
         launches++;
     }
     mark(kProfWrite);

@@ -1108,7 +1108,7 @@ __global__ void __launch_bounds__(256) huge_kernel(__grid_constant__ const DevPl
 // Bucket b's groups become edges [eoff, eoff + ecount) of the flat DEM, ids
 // decoded from the representative's key (or expanded from its records, in
 // word order: bit b < D -> detector b, else observable b - D; dem.cpp:108-116).
-__global__ void write_kernel(__grid_constant__ const DevPlan p, const uint4 *out_total) {
+__global__ void write_kernel(__grid_constant__ const DevPlan p, const uint4 *out_total, uint32_t cb) {
     const uint64_t NB = p.tot.buckets;
     const uint32_t lane = threadIdx.x & 31;
     const uint64_t warps = (uint64_t)gridDim.x * (blockDim.x >> 5);
@@ -1139,15 +1139,16 @@ __global__ void write_kernel(__grid_constant__ const DevPlan p, const uint4 *out
         const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
         if (t <= p.tot.C) p.o_edge_off[t] = bE + (t < p.tot.C ? p.oscan[meta[t].bucket_base].x : tot.x);
     }
-    // One warp per 32 consecutive buckets, their edges packed onto the lanes
-    // (a bucket holds ~9 edges: one bucket per warp would idle most lanes).
+    // One warp per cb (<= 32) consecutive buckets, their edges packed onto
+    // the lanes (a bucket holds ~9 edges: one bucket per warp would idle most
+    // lanes; batches take cb = 32, single circuits fewer -- enough warps).
     // Edge j of the chunk is edge oscan[B0].x + j of the output; its id
     // offsets are the chunk's (oscan[B0]) plus a warp scan of the id counts.
     const Item *items = items_of(p), *items2 = reinterpret_cast<const Item *>(p.items2);
     const uint32_t *circ_bkt = arr<uint32_t>(p, p.lay.circ_bkt);
-    for (uint64_t B0 = (((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 32; B0 < NB; B0 += warps * 32) {
+    for (uint64_t B0 = (((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * cb; B0 < NB; B0 += warps * cb) {
         const uint64_t b = B0 + lane;
-        const uint32_t ne = b < NB ? p.ecount[b] : 0;
+        const uint32_t ne = lane < cb && b < NB ? p.ecount[b] : 0;
         uint32_t st = ne;  // inclusive scan of the edge counts
 #pragma unroll
         for (int d = 1; d < 32; d <<= 1) {
