@@ -470,7 +470,7 @@ struct OutScanF {  // (edges, detector ids, observable ids) per bucket, in canon
     __device__ bool active(uint64_t) const { return true; }
     __device__ uint4 operator()(uint64_t b) const {
         const uint2 v = eids[b];
-        return make_uint4(ecount[b], v.x, v.y, 0);
+        return make_uint4(ecount[b] & 0x7FFFFFFFu, v.x, v.y, 0);  // (bit 31: red::kEdgesInItems)
     }
 };
 

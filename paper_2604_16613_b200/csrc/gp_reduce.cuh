@@ -561,6 +561,8 @@ struct RunAcc {  // a contiguous run (bucket order); e_item = position | flag
     __device__ Item load(uint32_t i) const { return load_item(it + i); }
     __device__ double prob(uint32_t i) const { return it[i].prob; }
     __device__ uint32_t gidx(uint32_t i) const { return (base + i) | flag; }
+    // the bucket's own run in items2: its edges may be written over it
+    __device__ Item *edges() const { return flag == kItem2 ? const_cast<Item *>(it) : nullptr; }
 };
 struct IdxAcc {  // fused items: through the bucket's index list
     const Item *items;
@@ -568,7 +570,12 @@ struct IdxAcc {  // fused items: through the bucket's index list
     __device__ Item load(uint32_t i) const { return load_item(items + idx[i]); }
     __device__ double prob(uint32_t i) const { return items[idx[i]].prob; }
     __device__ uint32_t gidx(uint32_t i) const { return idx[i]; }
+    __device__ Item *edges() const { return nullptr; }
 };
+
+// ecount[b] flag: bucket b's edges are items2[base + g] in canonical order,
+// each carrying its folded probability (no e_item / e_prob / e_ndno entries).
+constexpr uint32_t kEdgesInItems = 0x80000000u;
 
 // Items and item count of bucket b.
 __device__ __forceinline__ uint32_t bucket_size(const DevPlan &p, uint64_t b) {
@@ -876,6 +883,33 @@ __device__ bool group_bucket(const DevPlan &p, const Team &tm, uint32_t b, uint3
         __syncwarp();
         if (lane < G) w.grp[rank] = (uint16_t)mine;
         __syncwarp();
+        if (Item *ed = it.edges()) {
+            // the edges over the bucket's own run: group `rank` (its key in
+            // this lane's registers, every read of the run done) with its
+            // folded probability -- the write kernel then streams them
+            uint32_t nd = 0, no = 0;
+            Item e{};
+            if (lane < G) {
+                e = me;
+                e.prob = w.mp[w.off[mine]];
+                const uint32_t v = key_ndno(me);
+                nd = v & 0xFFFF;
+                no = v >> 16;
+            }
+            __syncwarp();
+            if (lane < G) store_item(ed + rank, e);
+#pragma unroll
+            for (int d = 16; d > 0; d >>= 1) {
+                nd += __shfl_xor_sync(0xffffffffu, nd, d);
+                no += __shfl_xor_sync(0xffffffffu, no, d);
+            }
+            if (lane == 0) {
+                p.ecount[b] = G | kEdgesInItems;
+                p.eids[b] = make_uint2(nd, no);
+            }
+            __syncwarp();
+            return true;
+        }
     } else {
         uint32_t np = 1;
         while (np < G) np <<= 1;
@@ -1148,7 +1182,9 @@ __global__ void write_kernel(__grid_constant__ const DevPlan p, const uint4 *out
     const uint32_t *circ_bkt = arr<uint32_t>(p, p.lay.circ_bkt);
     for (uint64_t B0 = (((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * cb; B0 < NB; B0 += warps * cb) {
         const uint64_t b = B0 + lane;
-        const uint32_t ne = lane < cb && b < NB ? p.ecount[b] : 0;
+        const uint32_t ec = lane < cb && b < NB ? p.ecount[b] : 0;
+        const uint32_t ne = ec & ~kEdgesInItems;
+        const bool inl = (ec & kEdgesInItems) != 0;  // edges = items2[base + k]
         uint32_t st = ne;  // inclusive scan of the edge counts
 #pragma unroll
         for (int d = 1; d < 32; d <<= 1) {
@@ -1177,9 +1213,22 @@ __global__ void write_kernel(__grid_constant__ const DevPlan p, const uint4 *out
             const uint32_t k = j - __shfl_sync(0xffffffffu, start, l);
             const uint32_t bb = __shfl_sync(0xffffffffu, base, l);
             const BucketCtx cx{__shfl_sync(0xffffffffu, D, l), __shfl_sync(0xffffffffu, q0, l)};
+            const bool ein = __shfl_sync(0xffffffffu, (uint32_t)inl, l) != 0;
             uint32_t nd = 0, no = 0;
+            Item q{};
+            double pe = 0.0;
             if (j < T) {
-                const uint32_t v = p.e_ndno[bb + k];
+                uint32_t v;
+                if (ein) {  // the edge itself (consecutive k: a streamed run)
+                    q = load_item(items2 + bb + k);
+                    pe = q.prob;
+                    v = key_ndno(q);
+                } else {
+                    v = p.e_ndno[bb + k];
+                    pe = p.e_prob[bb + k];
+                    const uint32_t ei = p.e_item[bb + k];
+                    q = load_item((ei & kItem2 ? items2 : items) + (ei & ~kItem2));
+                }
                 nd = v & 0xFFFF;
                 no = v >> 16;
             }
@@ -1197,9 +1246,7 @@ __global__ void write_kernel(__grid_constant__ const DevPlan p, const uint4 *out
                 const uint32_t d0 = o.y + dcar + di - nd, o0 = o.z + ocar + oi - no;
                 p.o_det_off[e] = (uint32_t)(bD + d0);
                 p.o_obs_off[e] = (uint32_t)(bO + o0);
-                p.o_prob[e] = p.e_prob[bb + k];
-                const uint32_t ei = p.e_item[bb + k];
-                const Item q = load_item((ei & kItem2 ? items2 : items) + (ei & ~kItem2));
+                p.o_prob[e] = pe;
                 uint32_t wd = d0, wo = o0;
                 if (q.complete()) {  // detectors q0 - 1, then the differences; observables by mask
                     if (cx.q0) {
