@@ -263,11 +263,12 @@ __global__ void lower_kernel(__grid_constant__ const DevPlan p, uint32_t blocks_
             if (act) {
                 const uint32_t off = base + incl - k;
                 p.nsrc[o] = off;
-                const double pr = p.tot.wide_prob ? nprob[o] : ptab[noise_pidx(w)];
-                const double pe = kind == 2 ? __ddiv_rn(pr, 3.0) : kind == 3 ? __ddiv_rn(pr, 15.0) : pr;
-                double *dst = p.prob + m.src_base + off;
-                if (!fused_prob)
+                if (!fused_prob) {  // (fused items take them from ptab3 in the traversal)
+                    const double pr = p.tot.wide_prob ? nprob[o] : ptab[noise_pidx(w)];
+                    const double pe = kind == 2 ? __ddiv_rn(pr, 3.0) : kind == 3 ? __ddiv_rn(pr, 15.0) : pr;
+                    double *dst = p.prob + m.src_base + off;
                     for (uint32_t j = 0; j < k; j++) dst[j] = pe;
+                }
             }
             base += __shfl_sync(0xffffffffu, incl, 31);
         }
