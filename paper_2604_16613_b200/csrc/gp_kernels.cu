@@ -889,7 +889,11 @@ reduce:
     }
     mark(kProfWrite);
     if (written) cudaEventRecord(written, st);
-    if (p.out_mapped) red::copy_out_kernel<<<32, 256, 0, st>>>(p), launches++;
+    if (p.out_mapped) {
+        const char *ce = std::getenv("GP_COPY_CTAS");  // (tuning)
+        const uint32_t cc = ce ? (uint32_t)std::max(1, std::atoi(ce)) : 32u;
+        red::copy_out_kernel<<<cc, 256, 0, st>>>(p), launches++;
+    }
     if (ev) cudaEventRecord(ev->reduced, st);
     *err = cudaGetLastError();
     return launches;
