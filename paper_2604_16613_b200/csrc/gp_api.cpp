@@ -1134,7 +1134,7 @@ gp_status run_batch_pipelined(gp_ctx *ctx, const gp_circuit_view *cs, size_t cou
     const char *ps_env = std::getenv("GP_PIPE_SUB");  // tuning knobs (read per call)
     const size_t sub = ps_env ? std::max<size_t>(64, (size_t)std::atoi(ps_env)) : kSubCircuits;
     const char *pl_env = std::getenv("GP_PIPE_LANES");
-    const size_t NL = pl_env ? std::min<size_t>(gp::kLanes, std::max(2, std::atoi(pl_env))) : gp::kLanesDefault;
+    const size_t NL = pl_env ? std::min<size_t>(gp::kLanes, std::max(1, std::atoi(pl_env))) : gp::kLanesDefault;
     const char *pr_env = std::getenv("GP_PIPE_RAMP");
     const bool ramp = pr_env ? std::atoi(pr_env) != 0 : kRampDefault;
     // (device generation: GP_GEN_SUB tunes its sub-batch size separately;
