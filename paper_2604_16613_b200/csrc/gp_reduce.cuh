@@ -788,9 +788,12 @@ __device__ bool group_bucket(const DevPlan &p, const Team &tm, uint32_t b, uint3
     tm.sync();
     // 1. representatives: hash + full key compare
     bool inc = false;
+    double pc0 = 0.0, pc1 = 0.0;  // this thread's first two items' probabilities (the placement and move reuse them)
     for (uint32_t i = t0; i < n; i += nt) {
         const Item me = it.load(i);
         inc |= !me.complete();
+        if (i == t0) pc0 = me.prob;
+        else if (i == t0 + nt) pc1 = me.prob;
         uint32_t h = item_hash(me) & (w.tcap - 1), r = i;
         while (true) {
             uint32_t cur = w.tab[h];
@@ -817,7 +820,7 @@ __device__ bool group_bucket(const DevPlan &p, const Team &tm, uint32_t b, uint3
     for (uint32_t i = t0; i < n; i += nt) {
         const uint32_t r = w.rep[i];
         const uint32_t pos = w.off[r] + atomicSub(&w.cnt[r], 1u) - 1;
-        w.mp[pos] = it.prob(i);
+        w.mp[pos] = i == t0 ? pc0 : i == t0 + nt ? pc1 : it.prob(i);
         w.tab[i] = (uint16_t)pos;
     }
     tm.sync();
@@ -840,7 +843,7 @@ __device__ bool group_bucket(const DevPlan &p, const Team &tm, uint32_t b, uint3
     }
     const bool any_nan = tm.any(nan);  // (also the barrier between the ranks and the moves)
     if (!any_nan) {
-        for (uint32_t i = t0; i < n; i += nt) w.mp[w.tab[i]] = it.prob(i);
+        for (uint32_t i = t0; i < n; i += nt) w.mp[w.tab[i]] = i == t0 ? pc0 : i == t0 + nt ? pc1 : it.prob(i);
         tm.sync();
     }
     for (uint32_t g = t0; g < G; g += nt) {
