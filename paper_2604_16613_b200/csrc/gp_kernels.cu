@@ -205,6 +205,11 @@ __global__ void lower_kernel(__grid_constant__ const DevPlan p, uint32_t blocks_
         // fused items: the traversal takes each source's probability from the
         // flips / ptab3 itself (no per-source array)
         const bool fused_prob = p.fused && !p.tot.wide_prob;
+        if (p.fused && i > 0) {  // batches: this warp owns boundary i - 1's ELL row -- idle (0) first, coalesced
+            uint32_t *row = p.ell + m.ell_base + (uint64_t)(i - 1) * ell_stride(m.n);
+            for (uint32_t x = lane; x < ell_stride(m.n); x += 32) row[x] = kEllIdle;
+            __syncwarp();
+        }
         for (uint32_t g = lay_gate[li] + lane; g < lay_gate[li + 1]; g += 32) {
             const uint64_t w = narrow ? widen_gate(gates32[g]) : gates[g];
             const uint32_t lo = (uint32_t)w, hi = (uint32_t)(w >> 32);
@@ -766,7 +771,10 @@ int enqueue_pipeline(const DevPlan &p, cudaStream_t st, const StageEvents *ev, c
             z.count++;
         };
         if (p.mode != kModeMerge) {  // (merge: counts and records are uploaded)
-            add(p.ell, p.tot.ell * 4);
+            // (batches with fused items: each ELL row is idle-filled by its
+            // lowering warp; a single circuit's few layer warps would
+            // serialise that, the fill kernel spreads it)
+            if (!p.fused) add(p.ell, p.tot.ell * 4);
             add(p.leaf, p.tot.leaf * 8);
             // fused items: records are written (and read) only for incomplete keys
             if (!p.fused) add(p.cnt, S * 4 + 4);
