@@ -873,8 +873,10 @@ reduce:
     mark(kProfScatter);
     {
         const uint64_t ctas = (NB + red::kBucketThreads / 32 - 1) / (red::kBucketThreads / 32);
-        red::bucket_kernel<<<(uint32_t)std::min<uint64_t>(std::max<uint64_t>(ctas, 1), 148 * 256),
-                             red::kBucketThreads, 0, st>>>(p);
+        const char *be = std::getenv("GP_BUCKET_CTAS");  // (tuning)
+        const uint64_t cap = be ? (uint64_t)std::max(1, std::atoi(be)) : 148 * 16;
+        red::bucket_kernel<<<(uint32_t)std::min<uint64_t>(std::max<uint64_t>(ctas, 1), cap), red::kBucketThreads, 0,
+                             st>>>(p);
         smem_optin(red::huge_kernel);
         // (listed buckets: over kWarpItems sources, or holding an incomplete key)
         const uint32_t hgrid = (uint32_t)std::min<uint64_t>(kHugeCtas, std::max<uint64_t>(1, S / 64));

@@ -165,7 +165,7 @@ struct DeviceHeader {
     uint32_t huge_count;       // buckets too large for shared memory
     uint32_t items_overflow;   // nonempty signatures beyond the item capacity (re-run larger)
     uint32_t bad_input;        // merge: malformed partial-table entries (dropped; the call fails)
-    uint32_t pad;
+    uint32_t bucket_next;      // bucket_kernel's work counter (warps take buckets in order)
 };
 
 }  // namespace gp

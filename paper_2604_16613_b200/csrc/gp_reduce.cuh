@@ -1071,9 +1071,14 @@ __global__ void __launch_bounds__(kBucketThreads) bucket_kernel(__grid_constant_
     GroupWs w;
     w.carve(ws + warp * kWarpWs, kWarpItems, kWarpTab);
     const uint64_t NB = p.tot.buckets;
-    const uint64_t warps = (uint64_t)gridDim.x * (kBucketThreads / 32);
     if (p.hdr->items_overflow) return;  // re-run with a larger item array
-    for (uint64_t b = ((uint64_t)blockIdx.x * kBucketThreads + threadIdx.x) >> 5; b < NB; b += warps) {
+    // buckets taken in order from a counter (bucket sizes vary 1-256: a
+    // fixed stride would leave the warps with the larger shares as the tail)
+    for (uint64_t b;;) {
+        uint32_t nb = 0;
+        if (lane == 0) nb = atomicAdd(&p.hdr->bucket_next, 1u);
+        b = __shfl_sync(0xffffffffu, nb, 0);
+        if (b >= NB) break;
         const uint32_t base = p.boff[b].x, n = bucket_size(p, b);
         if (n == 0) {
             if (lane == 0) {
