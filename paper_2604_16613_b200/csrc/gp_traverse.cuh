@@ -135,20 +135,23 @@ struct KeyCtx {
 template <int TM>
 __device__ __forceinline__ void emit_item(const DevPlan &p, uint64_t src, uint32_t tw, const uint64_t (&v)[TM],
                                           const KeyCtx &kc, double prob) {
-    uint32_t nz = 0;
+    uint64_t any = 0;
 #pragma unroll
-    for (int w = 0; w < TM; w++) nz += ((uint32_t)w < tw && v[w] != 0);
+    for (int w = 0; w < TM; w++) any |= (uint32_t)w < tw ? v[w] : 0ull;
     const uint32_t am = __activemask(), lane = threadIdx.x & 31;
-    const uint32_t want = __ballot_sync(am, nz != 0);
+    const uint32_t want = __ballot_sync(am, any != 0);
     if (!want) return;
     const uint32_t leader = __ffs(want) - 1;
     uint32_t k = 0;
     if (lane == leader) k = atomicAdd(kc.nitems, (uint32_t)__popc(want));
     k = __shfl_sync(am, k, leader) + __popc(want & ((1u << lane) - 1));
-    if (nz == 0) return;
+    if (any == 0) return;
     uint32_t local;
     const red::Item it = red::item_of_words<TM>(v, tw, kc.D, prob, (uint32_t)src, p.force_collisions != 0, &local);
     if (!it.complete()) {  // the exact comparator reads this source's records
+        uint32_t nz = 0;
+#pragma unroll
+        for (int w = 0; w < TM; w++) nz += ((uint32_t)w < tw && v[w] != 0);
         p.cnt[src] = nz;
         if (nz > p.K) {
             atomicMax(&p.hdr->record_overflow, nz);
