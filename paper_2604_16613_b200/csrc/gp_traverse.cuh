@@ -391,7 +391,7 @@ __global__ void __launch_bounds__(800, 1) traverse_kernel(__grid_constant__ cons
                 bool ok = false;
                 while (!(ok = mbar_try_wait_sleep(&stage_empty[k], par, 2000))) {  // (re-checks s_stop)
                     if (b < s_stop) break;
-                    __nanosleep(512);
+                    __nanosleep(4096);
                 }
                 if (!ok) break;
             }
