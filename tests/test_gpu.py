@@ -532,6 +532,24 @@ def test_device_generated_branches_match_reference():
     check_branch_batch(comp, out, 3000, 1096)
 
 
+def test_every_rank_range_of_the_scaling_run_matches_reference():
+    """The N = 8 scaling run's whole workload: rank r compiles branch ids
+    4,096 r .. 4,096 r + 4,095, so 32,768 branches in all -- every one of them
+    generated on the device and compiled in rank-sized batches, each DEM equal
+    to the reference's (the golden digests cover all 32,768); rank 7's range
+    also from host circuits through the pipelined batch path."""
+    comp = gp.Compiler(0)
+    spec = gp.bb72_branch_spec()
+    for first in range(0, 8 * 4096, 4096):
+        out, _ = comp.compile_bb_branches_raw(spec, first, 4096, 0)
+        check_branch_batch(comp, out, first, 4096)
+    gens, views = branch_views(7 * 4096, 4096)
+    comp.set_option(4, -1)
+    for _ in range(2):
+        out, _ = comp.compile_batch_raw(views, 0)
+        check_branch_batch(comp, out, 7 * 4096, 4096)
+
+
 @pytest.mark.parametrize("case", ["bb72-cp0.3-L2", "bb72-cp0.9-L1", "bb144-full-L0", "bb72-si1000-L0"])
 def test_device_generated_branches_equal_host_generated(case):
     """Other specs (check probability, level, code, noise model): the device
