@@ -1293,20 +1293,27 @@ __global__ void write_kernel(__grid_constant__ const DevPlan p, const uint4 *out
 
 // Mapped output: the output region and the header into mapped pinned host
 // memory (coalesced stores over PCIe; sizes from the device header).
+// 16-byte stores (larger PCIe writes than 4- or 8-byte ones); both sides
+// 16-byte aligned, the tail byte by byte.
+__device__ __forceinline__ void copy_bytes16(void *dst, const void *src, uint64_t bytes, uint64_t t0, uint64_t stride) {
+    const uint64_t n16 = bytes / 16;
+    for (uint64_t i = t0; i < n16; i += stride) reinterpret_cast<uint4 *>(dst)[i] = reinterpret_cast<const uint4 *>(src)[i];
+    if (t0 < bytes - n16 * 16)
+        reinterpret_cast<uint8_t *>(dst)[n16 * 16 + t0] = reinterpret_cast<const uint8_t *>(src)[n16 * 16 + t0];
+}
+
 __global__ void copy_out_kernel(__grid_constant__ const DevPlan p) {
     const DeviceHeader hd = *p.hdr;
     const bool ok = hd.num_det_ids != 0xFFFFFFFFu && !hd.items_overflow && !hd.record_overflow && !hd.pool_overflow;
     const uint64_t E = hd.num_edges, nd = ok ? hd.num_det_ids : 0, no = hd.num_obs_ids, C = p.tot.C;
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x, t0 = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (ok) {
-        for (uint64_t i = t0; i <= E; i += stride) {
-            p.hmap.det_off[i] = p.o_det_off[i];
-            p.hmap.obs_off[i] = p.o_obs_off[i];
-            if (i < E) p.hmap.probs[i] = p.o_prob[i];
-        }
-        for (uint64_t i = t0; i < nd; i += stride) p.hmap.det_ids[i] = p.o_det[i];
-        for (uint64_t i = t0; i < no; i += stride) p.hmap.obs_ids[i] = p.o_obs[i];
-        for (uint64_t i = t0; i <= C; i += stride) p.hmap.edge_off[i] = p.o_edge_off[i];
+        copy_bytes16(p.hmap.det_off, p.o_det_off, (E + 1) * 4, t0, stride);
+        copy_bytes16(p.hmap.obs_off, p.o_obs_off, (E + 1) * 4, t0, stride);
+        copy_bytes16(p.hmap.probs, p.o_prob, E * 8, t0, stride);
+        copy_bytes16(p.hmap.det_ids, p.o_det, nd * 4, t0, stride);
+        copy_bytes16(p.hmap.obs_ids, p.o_obs, no * 4, t0, stride);
+        copy_bytes16(p.hmap.edge_off, p.o_edge_off, (C + 1) * 8, t0, stride);
     }
     if (t0 == 0) *p.hmap.hdr = hd;
 }
