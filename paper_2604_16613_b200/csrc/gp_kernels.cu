@@ -183,12 +183,18 @@ __device__ __forceinline__ void fence_proxy_async() {
 // Part B: one thread per detector / observable toggles its bit into the leaf
 // rows of its measurements (init_leaves, eec.cpp:40-58).
 
+// Part A runs a warp per layer (batches: many layers) or, with cta_layer, a
+// whole CTA per layer (single circuits: few, wide layers -- the gates split
+// over the CTA, the noise ops' component offsets from a CTA scan per chunk).
+template <bool cta_layer>
 __global__ void lower_kernel(__grid_constant__ const DevPlan p, uint32_t blocks_a) {
     const uint32_t C = p.tot.C;
     const CircuitMeta *meta = arr<CircuitMeta>(p, p.lay.meta);
     if (blockIdx.x < blocks_a) {
-        const uint64_t gw = (uint64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+        const uint64_t gw = cta_layer ? blockIdx.x : (uint64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
         const uint32_t lane = threadIdx.x & 31;
+        // threads of one layer: the warp, or the CTA
+        const uint32_t lt = cta_layer ? threadIdx.x : lane, ln = cta_layer ? blockDim.x : 32u;
         if (gw >= p.tot.layers) return;
         const uint32_t *circ_layer = arr<uint32_t>(p, p.lay.circ_layer);
         const uint32_t c = find_u32_warp(circ_layer, C, (uint32_t)gw);  // (gw is warp-uniform)
@@ -207,10 +213,11 @@ __global__ void lower_kernel(__grid_constant__ const DevPlan p, uint32_t blocks_
         const bool fused_prob = p.fused && !p.tot.wide_prob;
         if (p.fused && i > 0) {  // batches: this warp owns boundary i - 1's ELL row -- idle (0) first, coalesced
             uint32_t *row = p.ell + m.ell_base + (uint64_t)(i - 1) * ell_stride(m.n);
-            for (uint32_t x = lane; x < ell_stride(m.n); x += 32) row[x] = kEllIdle;
-            __syncwarp();
+            for (uint32_t x = lt; x < ell_stride(m.n); x += ln) row[x] = kEllIdle;
+            if constexpr (cta_layer) __syncthreads();
+            else __syncwarp();
         }
-        for (uint32_t g = lay_gate[li] + lane; g < lay_gate[li + 1]; g += 32) {
+        for (uint32_t g = lay_gate[li] + lt; g < lay_gate[li + 1]; g += ln) {
             const uint64_t w = narrow ? widen_gate(gates32[g]) : gates[g];
             const uint32_t lo = (uint32_t)w, hi = (uint32_t)(w >> 32);
             const uint32_t q = lo & ((1u << kGateKindShift) - 1), kind = lo >> kGateKindShift;
@@ -252,8 +259,8 @@ __global__ void lower_kernel(__grid_constant__ const DevPlan p, uint32_t blocks_
         const double *nprob = arr<double>(p, p.lay.noise_prob);
         const double *ptab = arr<double>(p, p.lay.prob_table);
         uint32_t base = arr<uint32_t>(p, p.lay.lay_src)[li];
-        for (uint32_t o0 = lay_noise[li]; o0 < lay_noise[li + 1]; o0 += 32) {
-            const uint32_t o = o0 + lane;
+        for (uint32_t o0 = lay_noise[li]; o0 < lay_noise[li + 1]; o0 += ln) {
+            const uint32_t o = o0 + lt;
             const bool act = o < lay_noise[li + 1];
             const uint64_t w = act ? (narrow ? widen_noise(noise32[o]) : noise[o]) : 0;
             if (act && narrow) p.noise_w[o] = w;  // the traversal's 8-byte words
@@ -265,6 +272,22 @@ __global__ void lower_kernel(__grid_constant__ const DevPlan p, uint32_t blocks_
                 const uint32_t x = __shfl_up_sync(0xffffffffu, incl, d);
                 if (lane >= (uint32_t)d) incl += x;
             }
+            uint32_t chunk = __shfl_sync(0xffffffffu, incl, 31);
+            if constexpr (cta_layer) {  // the CTA's chunk: warp totals, then each warp's prefix
+                __shared__ uint32_t s_wsum[32];
+                const uint32_t wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+                if (lane == 31) s_wsum[wid] = incl;
+                __syncthreads();
+                uint32_t pre = 0;
+                chunk = 0;
+                for (uint32_t x = 0; x < nw; x++) {
+                    const uint32_t v = s_wsum[x];
+                    pre += x < wid ? v : 0u;
+                    chunk += v;
+                }
+                incl += pre;
+                __syncthreads();  // (s_wsum is rewritten by the next chunk)
+            }
             if (act) {
                 const uint32_t off = base + incl - k;
                 p.nsrc[o] = off;
@@ -275,7 +298,7 @@ __global__ void lower_kernel(__grid_constant__ const DevPlan p, uint32_t blocks_
                     for (uint32_t j = 0; j < k; j++) dst[j] = pe;
                 }
             }
-            base += __shfl_sync(0xffffffffu, incl, 31);
+            base += chunk;
         }
         return;
     }
@@ -798,9 +821,15 @@ int enqueue_pipeline(const DevPlan &p, cudaStream_t st, const StageEvents *ev, c
     // K1 lowering.
     {
         const uint32_t tpb = 256;
-        const uint32_t ba = blocks_for(p.tot.layers, tpb / 32);
+        // a CTA per layer when a warp per layer would not fill the machine
+        const uint32_t cta_layer = p.tot.layers < 148u * 8u ? 1u : 0u;
+        const uint32_t ba = cta_layer ? (uint32_t)p.tot.layers : blocks_for(p.tot.layers, tpb / 32);
         const uint32_t bb = blocks_for(p.tot.dets + p.tot.obss + (p.fused ? p.tot.prob_table_n : 0), tpb);
-        if (ba + bb) lower_kernel<<<ba + bb, tpb, 0, st>>>(p, ba), launches++;
+        if (ba + bb) {
+            if (cta_layer) lower_kernel<true><<<ba + bb, tpb, 0, st>>>(p, ba);
+            else lower_kernel<false><<<ba + bb, tpb, 0, st>>>(p, ba);
+            launches++;
+        }
     }
     mark(kProfLower);
     if (ev) cudaEventRecord(ev->lowered, st);
