@@ -473,6 +473,19 @@ def test_headline_branch_batch_matches_reference(pipeline):
     check_branch_batch(comp, out, 0, 4096)
 
 
+def test_pipelined_batch_one_lane_matches_reference(monkeypatch):
+    """The pipelined batch with one compute lane (GP_PIPE_LANES=1: every
+    sub-batch's kernels in one stream, its image and workspace reused in
+    stream order) gives the reference DEMs of the headline branches."""
+    monkeypatch.setenv("GP_PIPE_LANES", "1")
+    gens, views = branch_views(0, 4096)
+    comp = gp.Compiler(0)
+    comp.set_option(4, -1)
+    for _ in range(2):
+        out, _ = comp.compile_batch_raw(views, 0)
+        check_branch_batch(comp, out, 0, 4096)
+
+
 def test_headline_branch_batch_rank1_range():
     """Branch ids 4096..8191 (rank 1's shard at N = 2), small item hint first:
     the items-capacity re-run at the bench's scale."""
