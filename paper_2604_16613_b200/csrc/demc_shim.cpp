@@ -4,6 +4,7 @@
 // behaviour (stepg.cpp:172-174, eec.cpp:44-46 / 52-54).
 #include <algorithm>
 #include <chrono>
+#include <cstdio>
 #include <cstdlib>
 #include <functional>
 #include <memory>
@@ -152,9 +153,11 @@ Dem compile_circuit(const Circuit &c, CorrelationLevel level, uint32_t threads, 
     thread_local Flat flat;
     gp_ctx *ctx = thread_ctx();
     const gp_circuit_view v = flatten(c, flat);
+    const auto t_flat = std::chrono::steady_clock::now();
     gp_dem_view out{};
     gp_stats st{};
     const gp_status rc = gp_compile(ctx, &v, (uint8_t)level, &out, stats ? &st : nullptr);
+    const auto t_comp = std::chrono::steady_clock::now();
     if (rc == GP_ERR_INVALID_ARGUMENT) throw std::invalid_argument(gp_last_error(ctx));
     if (rc != GP_OK) throw std::runtime_error(std::string("greenpeas: ") + gp_last_error(ctx));
     Dem d;
@@ -171,6 +174,14 @@ Dem compile_circuit(const Circuit &c, CorrelationLevel level, uint32_t threads, 
             h.probability = out.probs[e];
         }
     });
+    static const bool lat = std::getenv("GP_LAT_TRACE") != nullptr;  // experiments: drop-in phase times
+    if (lat) {
+        const auto ms = [&](std::chrono::steady_clock::time_point a, std::chrono::steady_clock::time_point b) {
+            return std::chrono::duration<double, std::micro>(b - a).count();
+        };
+        std::fprintf(stderr, "shim: flatten %.1f  compile %.1f  dem %.1f us\n", ms(t0, t_flat), ms(t_flat, t_comp),
+                     ms(t_comp, std::chrono::steady_clock::now()));
+    }
     if (stats) {
         stats->lower_ns = st.lower_ns;
         stats->traverse_ns = st.traverse_ns;
