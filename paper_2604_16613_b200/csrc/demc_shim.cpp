@@ -18,6 +18,7 @@
 
 namespace gp {
 void host_parallel_for(size_t n, const std::function<void(size_t)> &f);  // gp_api.cpp
+void set_compile_overlap(gp_ctx *ctx, std::function<void()> f);           // gp_api.cpp
 }
 
 namespace demc {
@@ -27,6 +28,8 @@ namespace {
 // Work below this many elements stays on the calling thread (a pool wake-up
 // costs more than it saves on small circuits).
 constexpr size_t kParallelMin = 1 << 15;
+// DEMs from this many hyperedges up have their array built during the compile.
+constexpr size_t kPrebuildMin = 4096, kPrebuildMax = 1 << 21;
 
 // Contiguous pieces of [0, n) for the pool.
 template <class F>
@@ -156,14 +159,24 @@ Dem compile_circuit(const Circuit &c, CorrelationLevel level, uint32_t threads, 
     const auto t_flat = std::chrono::steady_clock::now();
     gp_dem_view out{};
     gp_stats st{};
+    // The hyperedge array's value-initialisation (56 bytes per edge, one
+    // thread) is built while the kernels run, sized like this thread's last
+    // DEM, and trimmed or grown to the real size afterwards.
+    thread_local size_t last_edges = 0;
+    std::vector<Hyperedge> pre;
+    const size_t guess = last_edges;
+    if (guess >= kPrebuildMin && guess <= kPrebuildMax) gp::set_compile_overlap(ctx, [&pre, guess] { pre.resize(guess); });
     const gp_status rc = gp_compile(ctx, &v, (uint8_t)level, &out, stats ? &st : nullptr);
+    gp::set_compile_overlap(ctx, nullptr);
     const auto t_comp = std::chrono::steady_clock::now();
     if (rc == GP_ERR_INVALID_ARGUMENT) throw std::invalid_argument(gp_last_error(ctx));
     if (rc != GP_OK) throw std::runtime_error(std::string("greenpeas: ") + gp_last_error(ctx));
     Dem d;
     d.num_detectors = out.num_detectors;
     d.num_observables = out.num_observables;
+    if (2 * out.num_edges >= pre.size()) d.hyperedges = std::move(pre);  // (not for a much smaller DEM: capacity)
     d.hyperedges.resize(out.num_edges);
+    last_edges = out.num_edges;
     // one allocation per id list, made on the pool's threads for large DEMs
     // (malloc arenas are per thread)
     pieces(out.num_edges, out.num_edges * 4, [&](size_t a, size_t b) {

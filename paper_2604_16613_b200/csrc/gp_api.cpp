@@ -18,6 +18,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
 #include <string>
 #include <vector>
 
@@ -41,6 +42,7 @@ void pipe_destroy(PipeState *ps);
 struct gp_ctx {
     int device = 0;
     cudaStream_t stream = nullptr;
+    std::function<void()> overlap;  // host work of the caller, run once while a compile's kernels run
     std::string err;
     int force_collisions = 0;
     uint32_t trav_debug = 0;
@@ -155,6 +157,10 @@ gp_status fail(gp_ctx *ctx, gp_status st, const std::string &msg) {
 namespace gp {
 // Host tasks [0, n) on the shared pool when it is free (else on the caller):
 // the C++ drop-in's circuit flattening and demc::Dem materialisation.
+// Drop-in shim (demc_shim.cpp): host work to run while the next gp_compile's
+// kernels run (cleared by passing nullptr; runs at most once).
+void set_compile_overlap(gp_ctx *ctx, std::function<void()> f) { ctx->overlap = std::move(f); }
+
 void host_parallel_for(size_t n, const std::function<void(size_t)> &f) {
     PoolLease lease(n > 1);
     if (lease.pool) lease.pool->run(n, f);
@@ -633,6 +639,11 @@ repack:  // (again with per-op probabilities when the table overflowed)
             e = cudaMemcpyAsync(ctx->h_hdr, p.hdr, sizeof(DeviceHeader), cudaMemcpyDeviceToHost, ctx->stream);
         cudaEventRecord(ctx->ev_end, ctx->stream);
         const uint64_t t_launch = lat ? ns_since(t0) : 0;
+        if (ctx->overlap) {  // the caller's host work, instead of idling in the synchronize
+            const std::function<void()> f = std::move(ctx->overlap);
+            ctx->overlap = nullptr;
+            f();
+        }
         if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
         if (lat)
             std::fprintf(stderr, "lat: pack %.1f  carve+plan %.1f  launch %.1f  sync %.1f us\n", pack_ns / 1e3,
