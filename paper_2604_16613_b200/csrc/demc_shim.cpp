@@ -27,14 +27,16 @@ namespace {
 
 // Work below this many elements stays on the calling thread (a pool wake-up
 // costs more than it saves on small circuits).
-constexpr size_t kParallelMin = 1 << 15;
+constexpr size_t kParallelMin = 2048, kGrain = 1024;  // measured: tools/shim_trace.py sweeps
 // DEMs from this many hyperedges up have their array built during the compile.
 constexpr size_t kPrebuildMin = 4096, kPrebuildMax = 1 << 21;
 
 // Contiguous pieces of [0, n) for the pool.
 template <class F>
 void pieces(size_t n, size_t work, F &&f) {
-    const size_t k = work < kParallelMin ? 1 : std::min<size_t>({64, n, std::max<size_t>(1, work / 8192)});
+    static const size_t pmin = std::getenv("GP_SHIM_PAR_MIN") ? std::atol(std::getenv("GP_SHIM_PAR_MIN")) : kParallelMin;
+    static const size_t grain = std::getenv("GP_SHIM_GRAIN") ? std::atol(std::getenv("GP_SHIM_GRAIN")) : kGrain;
+    const size_t k = work < pmin ? 1 : std::min<size_t>({64, n, std::max<size_t>(1, work / grain)});
     if (k <= 1) {
         f(0, n);
         return;
