@@ -3,6 +3,7 @@
 // Restores the reference signature (compile.hpp:35-36) and its exception
 // behaviour (stepg.cpp:172-174, eec.cpp:44-46 / 52-54).
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
@@ -31,12 +32,23 @@ constexpr size_t kParallelMin = 2048, kGrain = 1024;  // measured: tools/shim_tr
 // DEMs from this many hyperedges up have their array built during the compile.
 constexpr size_t kPrebuildMin = 4096, kPrebuildMax = 1 << 21;
 
+// compile_circuit calls in flight in this process: with more than one (host
+// threads compiling at once, demc_main.cpp:184-195) the callers already are
+// the parallelism and every call stays on its own thread.
+std::atomic<int> g_calls{0};
+struct CallCount {
+    CallCount() { g_calls.fetch_add(1, std::memory_order_relaxed); }
+    ~CallCount() { g_calls.fetch_sub(1, std::memory_order_relaxed); }
+};
+
 // Contiguous pieces of [0, n) for the pool.
 template <class F>
 void pieces(size_t n, size_t work, F &&f) {
     static const size_t pmin = std::getenv("GP_SHIM_PAR_MIN") ? std::atol(std::getenv("GP_SHIM_PAR_MIN")) : kParallelMin;
     static const size_t grain = std::getenv("GP_SHIM_GRAIN") ? std::atol(std::getenv("GP_SHIM_GRAIN")) : kGrain;
-    const size_t k = work < pmin ? 1 : std::min<size_t>({64, n, std::max<size_t>(1, work / grain)});
+    const size_t k = work < pmin || g_calls.load(std::memory_order_relaxed) > 1
+                         ? 1
+                         : std::min<size_t>({64, n, std::max<size_t>(1, work / grain)});
     if (k <= 1) {
         f(0, n);
         return;
@@ -155,6 +167,7 @@ gp_circuit_view flatten(const Circuit &c, Flat &f) {
 Dem compile_circuit(const Circuit &c, CorrelationLevel level, uint32_t threads, CompileStats *stats) {
     (void)threads;
     const auto t0 = std::chrono::steady_clock::now();
+    const CallCount in_flight;
     thread_local Flat flat;
     gp_ctx *ctx = thread_ctx();
     const gp_circuit_view v = flatten(c, flat);
