@@ -12,6 +12,8 @@
 #include <barrier>
 #include <chrono>
 #include <cstdint>
+#include <cstring>
+#include <stdexcept>
 #include <thread>
 #include <vector>
 
@@ -115,6 +117,48 @@ int64_t sb_shim_pool(const gp_circuit_view *views, uint32_t count, int level, ui
     for (auto &th : pool) th.join();
     if (wall_ns) *wall_ns = total / (reps - 1);
     return failed ? -1 : one;
+}
+
+// The same pattern for parity: `threads` host threads take circuits from a
+// counter, each compile_circuit(c, levels[i], 1) through the drop-in; per
+// circuit, status[i] = 0 and digest[i] = gp_dem_digest of the returned
+// demc::Dem, or status 1 for std::invalid_argument (its message copied to
+// msg[i * 128]), or 2 for any other exception.
+int sb_shim_pool_digests(const gp_circuit_view *views, uint32_t count, const uint8_t *levels, uint32_t threads,
+                         uint64_t *digest, int32_t *status, char *msg) {
+    std::vector<demc::Circuit> cs;
+    cs.reserve(count);
+    for (uint32_t i = 0; i < count; i++) cs.push_back(to_circuit(views[i]));
+    std::atomic<uint32_t> next{0};
+    std::vector<std::thread> pool;
+    for (uint32_t t = 0; t < std::max<uint32_t>(threads, 1); t++)
+        pool.emplace_back([&] {
+            for (uint32_t s = next++; s < count; s = next++) {
+                try {
+                    const demc::Dem d = demc::compile_circuit(cs[s], (demc::CorrelationLevel)levels[s], 1);
+                    std::vector<uint32_t> doff{0}, ooff{0}, dids, oids;
+                    std::vector<double> pr;
+                    for (const auto &h : d.hyperedges) {
+                        dids.insert(dids.end(), h.detectors.begin(), h.detectors.end());
+                        oids.insert(oids.end(), h.observables.begin(), h.observables.end());
+                        doff.push_back((uint32_t)dids.size());
+                        ooff.push_back((uint32_t)oids.size());
+                        pr.push_back(h.probability);
+                    }
+                    gp_dem_view v{d.num_detectors, d.num_observables, d.hyperedges.size(), doff.data(),
+                                  dids.data(), ooff.data(), oids.data(), pr.data()};
+                    digest[s] = gp_dem_digest(&v);
+                    status[s] = 0;
+                } catch (const std::invalid_argument &e) {
+                    status[s] = 1;
+                    std::strncpy(msg + (size_t)s * 128, e.what(), 127);
+                } catch (...) {
+                    status[s] = 2;
+                }
+            }
+        });
+    for (auto &th : pool) th.join();
+    return 0;
 }
 
 }  // extern "C"

@@ -756,3 +756,62 @@ def test_signature_spanning_many_words(ref):
     want, _ = ref.parse(text).compile(0)
     comp = gp.Compiler(0)
     assert comp.compile(gp.parse_circuit(text), 0).to_text() == want
+
+
+# ---------------------------------------------------------------- drop-in under concurrent callers
+def _shim_pool_digests(views, levels, threads):
+    import ctypes as C
+    from paper_2604_16613_b200 import _native as N
+    L = C.CDLL(str(N.LIB_PATH.parent / "libgp_shimbench.so"))
+    n = len(levels)
+    lv = np.asarray(levels, np.uint8)
+    dig = np.zeros(n, np.uint64)
+    st = np.full(n, -1, np.int32)
+    msg = C.create_string_buffer(128 * n)
+    L.sb_shim_pool_digests.restype = C.c_int
+    L.sb_shim_pool_digests(views, C.c_uint32(n), lv.ctypes.data_as(C.c_void_p), C.c_uint32(threads),
+                           dig.ctypes.data_as(C.c_void_p), st.ctypes.data_as(C.c_void_p), msg)
+    msgs = [msg.raw[i * 128:(i + 1) * 128].split(b"\0")[0].decode() for i in range(n)]
+    return dig, st, msgs
+
+
+def test_dropin_concurrent_callers_match_reference():
+    """Reentrancy at scale, the demc_main.cpp:184-195 pattern: 16 host threads
+    calling demc::compile_circuit at once (one GPU context each, one shared
+    packing pool): every branch DEM equals the reference's."""
+    gens, views = branch_views(0, 1024)
+    dig, st, _ = _shim_pool_digests(views, [0] * 1024, 16)
+    assert (st == 0).all()
+    bad = np.nonzero(dig != BRANCHES["digests"][:1024])[0]
+    assert bad.size == 0, f"{bad.size} DEMs differ (first: {int(bad[0])})"
+
+
+def test_dropin_concurrent_mixed_levels_and_invalid_circuits():
+    """Concurrent drop-in calls of different levels, with invalid circuits among
+    them: each invalid one raises its own invalid_argument with the
+    reference's message, the others are exact."""
+    from paper_2604_16613_b200 import _native as N
+    n = 192
+    gens = [gp.gen_bb72_branch(b) for b in range(n)]
+    levels = [2 if i % 5 == 0 else 0 for i in range(n)]
+    keep, arr = [], (N.CircuitView * n)()
+    for i, g in enumerate(gens):
+        c = g.to_circuit()
+        if i % 37 == 3:
+            c = gp.Circuit(**{**c.__dict__, "det_meas": c.det_meas + 100000})
+        v, a = N.view_of(c)
+        keep.append(a)
+        arr[i] = v
+    dig, st, msgs = _shim_pool_digests(arr, levels, 16)
+    comp = gp.Compiler(0)
+    l2 = [i for i in range(n) if levels[i] == 2 and i % 37 != 3]
+    sub = (N.CircuitView * len(l2))(*[arr[i] for i in l2])
+    out, _ = comp.compile_batch_raw(sub, 2)
+    want_l2 = dict(zip(l2, comp.batch_digests(out)))
+    for i in range(n):
+        if i % 37 == 3:
+            assert st[i] == 1 and msgs[i] == "detector references a measurement without a leaf", (i, st[i], msgs[i])
+        elif levels[i] == 2:
+            assert st[i] == 0 and dig[i] == want_l2[i], i
+        else:
+            assert st[i] == 0 and dig[i] == BRANCHES["digests"][i], i
