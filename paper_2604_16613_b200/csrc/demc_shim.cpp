@@ -30,7 +30,7 @@ namespace {
 // costs more than it saves on small circuits).
 constexpr size_t kParallelMin = 2048, kGrain = 1024;  // measured: tools/shim_trace.py sweeps
 // DEMs from this many hyperedges up have their array built during the compile.
-constexpr size_t kPrebuildMin = 4096, kPrebuildMax = 1 << 21;
+constexpr size_t kPrebuildMin = 4096, kPrebuildMax = 1 << 18;  // (a wrong guess costs at most ~15 MB of zeroing)
 
 // compile_circuit calls in flight in this process: with more than one (host
 // threads compiling at once, demc_main.cpp:184-195) the callers already are
