@@ -264,13 +264,26 @@ def single_circuit_block(compiler, ref_ok: bool, quick: bool, gpu_iters: int, re
             sns = (C.c_uint64 * gpu_iters)()
             se = shim.sb_time_shim(C.byref(view), lv, 20, gpu_iters, sns)
             s50 = pct(list(sns), 0.5) / 1e6
+            # serialize_dem (dem.cpp:144-157) of the DEM: gp_serialize_dem (host, std::to_chars)
+            from paper_2604_16613_b200 import _native as N
+            dv, keep = dem.view()
+            sz = C.c_size_t()
+            zs = []
+            for _ in range(30):
+                t0 = time.perf_counter_ns()
+                ptxt = N.lib().gp_serialize_dem(C.byref(dv), C.byref(sz))
+                zs.append(time.perf_counter_ns() - t0)
+                N.lib().gp_free(ptxt)
             entry = {"edges": dem.num_edges, "iters": gpu_iters, "p50_ms": p50, "p99_ms": pct(ts, 0.99) / 1e6,
+                     "serialize_p50_ms": pct(zs, 0.5) / 1e6, "text_bytes": int(sz.value),
                      "kernel_p50_ms": pct(ks, 0.5) / 1e6, "hyperedges_per_s": dem.num_edges / (p50 / 1e3),
                      "dem_endpoint_p50_ms": s50, "dem_endpoint_p99_ms": pct(list(sns), 0.99) / 1e6,
                      "dem_endpoint_ok": int(se) == dem.num_edges}
             if ref is not None and not (quick and "d25" in name):
                 e, ns = ref.parse(text).time_compile(lv, ref_iters)
                 rp50 = pct(list(ns), 0.5) / 1e6
+                _, rz = ref.parse(text).time_serialize(lv, 5 if "d25" in name else 20)
+                entry["ref_serialize_p50_ms"] = pct(list(rz), 0.5) / 1e6
                 entry.update({"ref_iters": ref_iters, "ref_p50_ms": rp50, "ref_hyperedges_per_s": e / (rp50 / 1e3),
                               "speedup_p50": rp50 / p50, "speedup_p50_dem_endpoint": rp50 / s50})
             out[f"{name}_L{lv}"] = entry

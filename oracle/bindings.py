@@ -54,6 +54,8 @@ class RefLib:
         L.ref_adaptive_shot.restype = vp
         L.ref_time_compile.argtypes = [vp, C.c_int, C.c_uint32, C.POINTER(C.c_uint64)]
         L.ref_time_compile.restype = C.c_int64
+        L.ref_time_serialize.argtypes = [vp, C.c_int, C.c_uint32, C.POINTER(C.c_uint64)]
+        L.ref_time_serialize.restype = C.c_int64
         L.ref_compile_pool.argtypes = [C.POINTER(vp), C.c_uint32, C.c_int, C.c_uint32, C.POINTER(C.c_uint64)]
         L.ref_compile_pool.restype = C.c_int64
         L.ref_gen_bb72_branches.argtypes = [C.c_uint64, C.c_uint32, C.c_uint32, C.c_double, C.c_double,
@@ -160,6 +162,14 @@ class RefCircuit:
     def oracle(self, level: int) -> str:
         n = C.c_size_t()
         return self.lib._str(self.lib.L.ref_oracle(self.h, level, C.byref(n)), n)
+
+    def time_serialize(self, level: int, iters: int):
+        """serialize_dem of this circuit's DEM, `iters` timed calls: (text length, ns)."""
+        ns = (C.c_uint64 * iters)()
+        n = self.lib.L.ref_time_serialize(self.h, level, iters, ns)
+        if n < 0:
+            raise ValueError(self.lib.L.ref_last_error().decode())
+        return int(n), np.array(ns[:], dtype=np.uint64)
 
     def time_compile(self, level: int, iters: int):
         ns = (C.c_uint64 * iters)()

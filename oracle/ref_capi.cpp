@@ -205,6 +205,26 @@ int64_t ref_time_compile(void *h, int level, uint32_t iters, uint64_t *ns_out) {
     }
 }
 
+// serialize_dem (dem.cpp:144-157) of the circuit's DEM, `iters` timed calls
+// (the compile itself untimed). Returns the text length, -1 on error.
+int64_t ref_time_serialize(void *h, int level, uint32_t iters, uint64_t *ns_out) {
+    try {
+        const demc::Dem d = demc::compile_circuit(*(demc::Circuit *)h, (demc::CorrelationLevel)level, 1);
+        size_t n = 0;
+        for (uint32_t i = 0; i < iters; i++) {
+            auto t0 = std::chrono::steady_clock::now();
+            const std::string text = demc::serialize_dem(d);
+            auto t1 = std::chrono::steady_clock::now();
+            ns_out[i] = (uint64_t)std::chrono::duration_cast<std::chrono::nanoseconds>(t1 - t0).count();
+            n = text.size();
+        }
+        return (int64_t)n;
+    } catch (const std::exception &e) {
+        g_err = e.what();
+        return -1;
+    }
+}
+
 // Compiles `count` circuits on a std::thread pool of `threads` workers with an
 // atomic work counter, one compile_circuit(..., 1) per circuit (the
 // demc_main.cpp:184-195 pattern). Returns the total hyperedge count; *wall_ns

@@ -1937,19 +1937,48 @@ gp_status gp_circuit_metrics(const gp_circuit_view *v, uint8_t level, gp_metrics
 
 char *gp_serialize_dem(const gp_dem_view *d, size_t *len) {
     // serialize_dem (dem.cpp:144-157) with format_double = std::to_chars
-    // shortest round-trip (util.hpp:24-28). Large DEMs are formatted in edge
-    // pieces on the shared host pool: a first pass formats each piece into the
-    // worker's scratch buffer (kept across calls) for its exact length, the
-    // second formats it again straight into its place in the output.
+    // shortest round-trip (util.hpp:24-28). Large DEMs are formatted once, in
+    // edge pieces on the shared host pool, each into its worker's scratch
+    // (kept across calls), then copied into place. A DEM holds few distinct
+    // folded probabilities (37 over the 87k hyperedges of surface d25), so
+    // each piece keeps the text of the doubles it formatted (direct-mapped by
+    // their bits) and copies it for repeats: the same std::to_chars bytes.
     const uint64_t E = d->num_edges;
     const size_t k = E < 4096 ? 1 : std::min<uint64_t>(256, E / 1024);
-    auto format = [&](uint64_t e0, uint64_t e1, char *p) {
-        char *const end = p + (e1 - e0) * 40 +
-                          ((uint64_t)(d->det_offsets[e1] - d->det_offsets[e0]) + (d->obs_offsets[e1] - d->obs_offsets[e0])) * 12;
+    // bound of a piece: error(<= 24 chars)\n per edge, " D" / " L" + <= 10 digits per id
+    auto bound = [&](uint64_t e0, uint64_t e1) {
+        return (size_t)((e1 - e0) * 40 +
+                        ((uint64_t)(d->det_offsets[e1] - d->det_offsets[e0]) + (d->obs_offsets[e1] - d->obs_offsets[e0])) * 12);
+    };
+    struct ProbText {
+        uint64_t bits[64];
+        uint8_t n[64];
+        char s[64][32];
+    };
+    auto format = [&](uint64_t e0, uint64_t e1, char *p, char *const end) {
+        ProbText pt;
+        std::memset(pt.n, 0, sizeof pt.n);
         char *const start = p;
         for (uint64_t e = e0; e < e1; e++) {
             std::memcpy(p, "error(", 6);
-            p = std::to_chars(p + 6, end, d->probs[e]).ptr;
+            p += 6;
+            const double v = d->probs[e];
+            uint64_t b;
+            std::memcpy(&b, &v, 8);
+            const uint32_t h = (uint32_t)((b * 0x9E3779B97F4A7C15ull) >> 58);
+            if (pt.n[h] && pt.bits[h] == b) {
+                std::memcpy(p, pt.s[h], 32);  // (fixed-size copy; the bound leaves room)
+                p += pt.n[h];
+            } else {
+                char *const q = std::to_chars(p, end, v).ptr;
+                const size_t m = (size_t)(q - p);
+                if (m < 32) {
+                    std::memcpy(pt.s[h], p, m);
+                    pt.n[h] = (uint8_t)m;
+                    pt.bits[h] = b;
+                }
+                p = q;
+            }
             *p++ = ')';
             for (uint64_t x = d->det_offsets[e]; x < d->det_offsets[e + 1]; x++) {
                 p[0] = ' ';
@@ -1965,27 +1994,38 @@ char *gp_serialize_dem(const gp_dem_view *d, size_t *len) {
         }
         return (size_t)(p - start);
     };
-    // bound of a piece: error(<= 24 chars)\n per edge, " D" / " L" + <= 10 digits per id
-    auto bound = [&](uint64_t e0, uint64_t e1) {
-        return (size_t)((e1 - e0) * 40 +
-                        ((uint64_t)(d->det_offsets[e1] - d->det_offsets[e0]) + (d->obs_offsets[e1] - d->obs_offsets[e0])) * 12);
-    };
-    std::vector<size_t> at(k + 1, 0);
+    if (k == 1) {
+        char *out = (char *)std::malloc(bound(0, E) + 1 + 64);
+        const size_t n = format(0, E, out, out + bound(0, E) + 32);
+        out[n] = 0;
+        if (len) *len = n;
+        return out;
+    }
+    // pass 1: piece i formatted at scratch `buf[i]` + `off[i]` (the worker's
+    // scratch, reset by the first piece it takes in this call)
+    static std::atomic<uint64_t> calls{0};
+    const uint64_t call = ++calls;
+    std::vector<std::vector<char> *> buf(k);
+    std::vector<size_t> off(k), at(k + 1, 0);
     gp::host_parallel_for(k, [&](size_t i) {
         thread_local std::vector<char> scratch;
+        thread_local uint64_t used = 0, gen = 0;
+        if (gen != call) {
+            gen = call;
+            used = 0;
+        }
         const uint64_t e0 = E * i / k, e1 = E * (i + 1) / k;
-        if (scratch.size() < bound(e0, e1)) scratch.resize(bound(e0, e1));
-        at[i + 1] = format(e0, e1, scratch.data());
+        const size_t b = bound(e0, e1) + 32;
+        if (scratch.size() < used + b) scratch.resize(std::max(used + b, 2 * scratch.size()));
+        const size_t n = format(e0, e1, scratch.data() + used, scratch.data() + used + b);
+        buf[i] = &scratch;
+        off[i] = used;
+        at[i + 1] = n;
+        used += n;
     });
     for (size_t i = 0; i < k; i++) at[i + 1] += at[i];
     char *out = (char *)std::malloc(at[k] + 1 + 64);
-    gp::host_parallel_for(k, [&](size_t i) {
-        const uint64_t e0 = E * i / k, e1 = E * (i + 1) / k;
-        thread_local std::vector<char> scratch;
-        if (scratch.size() < bound(e0, e1)) scratch.resize(bound(e0, e1));
-        const size_t n = format(e0, e1, scratch.data());  // (to_chars needs the bound's room)
-        std::memcpy(out + at[i], scratch.data(), n);
-    });
+    gp::host_parallel_for(k, [&](size_t i) { std::memcpy(out + at[i], buf[i]->data() + off[i], at[i + 1] - at[i]); });
     out[at[k]] = 0;
     if (len) *len = at[k];
     return out;

@@ -90,3 +90,53 @@ def test_context_without_device_fails_loudly():
     assert N.lib().gp_ctx_create(0, C.byref(ctx)) == 4  # GP_ERR_NO_DEVICE
     with pytest.raises(gp.GreenpeasError):
         gp.Compiler(0)
+
+
+def _dem_view(edges):
+    doff = np.zeros(len(edges) + 1, np.uint32)
+    ooff = np.zeros(len(edges) + 1, np.uint32)
+    dids, oids = [], []
+    pr = np.zeros(max(len(edges), 1))
+    for i, (d, o, p) in enumerate(edges):
+        dids += d
+        oids += o
+        doff[i + 1], ooff[i + 1], pr[i] = len(dids), len(oids), p
+    arrs = (doff, np.array(dids + [0], np.uint32), ooff, np.array(oids + [0], np.uint32), pr)
+    u32 = C.POINTER(C.c_uint32)
+    v = N.DemView(0, 0, len(edges), *(a.ctypes.data_as(u32) for a in arrs[:4]),
+                  arrs[4].ctypes.data_as(C.POINTER(C.c_double)))
+    return v, arrs
+
+
+def _serialize(v):
+    n = C.c_size_t()
+    return N.take_string(N.lib().gp_serialize_dem(C.byref(v), C.byref(n)), n.value)
+
+
+def test_serialize_large_dem_byte_identical_to_reference():
+    """gp_serialize_dem on a DEM large enough for the parallel pieces and the
+    repeated-probability text cache (surface d11 SI1000 L2: 24k hyperedges,
+    64 distinct probabilities) equals the reference's serialize_dem."""
+    from oracle.bindings import RefLib, parse_dem_text
+    g = gp.gen_surface(11, 11, 1e-3, gp.NOISE_MODEL_SI1000)
+    text, _ = RefLib().parse(g.to_text()).compile(2)
+    body = "".join(line + "\n" for line in text.splitlines() if line.startswith("error"))
+    v, keep = _dem_view(parse_dem_text(text))
+    assert _serialize(v) == body
+
+
+def test_serialize_many_distinct_probabilities_round_trip():
+    """Colliding and repeated probabilities in the text cache: every printed
+    probability parses back to its own double, ids intact."""
+    rng = np.random.default_rng(5)
+    pool = np.concatenate([rng.random(300) * 1e-2, [0.0, -0.0, 1.0, 5e-324, 1e-300, 0.5]])
+    edges = [((int(i), int(i) + 3), (1,) if i % 7 == 0 else (), float(pool[rng.integers(pool.size)]))
+             for i in range(20000)]
+    v, keep = _dem_view(edges)
+    lines = _serialize(v).splitlines()
+    assert len(lines) == len(edges)
+    for line, (d, o, p) in zip(lines, edges):
+        head, *ids = line.split(" ")
+        q = float(head[6:-1])
+        assert q == p and np.signbit(q) == np.signbit(p), (line, p)
+        assert ids == [f"D{x}" for x in d] + [f"L{x}" for x in o]
